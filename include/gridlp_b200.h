@@ -1,0 +1,236 @@
+/*
+ * gridlp_b200.h — C ABI of libgridlp_b200.so, the sm_100a (B200) kernels for
+ * the hot path of arXiv 2601.07628 ("distributed PDHG over a 2D grid
+ * partition of A"): FP64 CSR products A·x̄ and Aᵀ·y fused with the
+ * restarted-Halpern PDHG update and with the KKT / restart reductions.
+ *
+ * Every entry point here replaces a call site of the reference package
+ * `gridlp` (pure Python; /root/reference/pkg/src/gridlp). The replaced
+ * reference interface is cited (file:line) on each declaration.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch types. All pointers are DEVICE
+ *    pointers unless a parameter says "host". The caller (Python/PyTorch)
+ *    owns every allocation; the library allocates nothing and keeps no
+ *    state except the thread-local error string.
+ *  - Every function returns 0 on success or a positive gridlp error code;
+ *    gridlp_last_error() returns a description of the last failure on the
+ *    calling thread. Launches are asynchronous and stream-ordered
+ *    (`stream` is a cudaStream_t passed as void*), so they can be captured
+ *    into CUDA graphs.
+ *  - Arithmetic is IEEE FP64 with explicit round-to-nearest multiplies and
+ *    adds (no FMA contraction), mirroring the reference's numpy/scipy
+ *    expressions operation for operation. Row sums are sequential
+ *    left-to-right from +0.0 like scipy's csr_matvec for every row of at
+ *    most `exact_row_max` entries (bit-identical to the reference); longer
+ *    rows use a deterministic tree sum (run-to-run reproducible, FP64
+ *    tolerance vs the reference).
+ *  - Reductions (norms, dots) are deterministic: per-CTA partials in a fixed
+ *    tree order, then one fixed-order final pass.
+ */
+#ifndef GRIDLP_B200_H
+#define GRIDLP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRIDLP_ABI_VERSION 1
+
+enum gridlp_status {
+  GRIDLP_OK = 0,
+  GRIDLP_ERR_ARG = 1,      /* invalid argument (ValueError in the reference) */
+  GRIDLP_ERR_CUDA = 2,     /* CUDA launch / runtime failure                   */
+  GRIDLP_ERR_WORKSPACE = 3 /* reduction workspace too small                   */
+};
+
+/* Max number of reduction slots an op can produce (see gridlp_red_t). */
+#define GRIDLP_MAX_RED 8
+/* Max partial products summed by an unfused epilogue (grid rows/cols). */
+#define GRIDLP_MAX_PARTS 16
+/* Nonzeros a light tile may hold (shared-memory product buffer). */
+#define GRIDLP_TILE_NNZ_CAP 4096
+/* Rows a light tile may hold (one thread per row in the row-sum phase). */
+#define GRIDLP_TILE_ROWS 256
+
+/*
+ * One device-resident block A_ij (or its stored transpose) in tiled CSR.
+ * Replaces SparseMatrix (lp_model.py:40-150) for a LocalBlock matrix /
+ * matrix_transpose (partition.py:93-122): int32 column indices (12 B/nnz
+ * instead of the reference's 16) and a tile directory. Tiles are row
+ * ranges [tile_ptr[t], tile_ptr[t+1]) that either hold at most
+ * GRIDLP_TILE_ROWS rows and GRIDLP_TILE_NNZ_CAP nonzeros ("light"), or a
+ * single row longer than exact_row_max ("heavy", tree-summed).
+ */
+typedef struct gridlp_csr {
+  int64_t num_rows;
+  int64_t num_cols;
+  int64_t nnz;
+  const int32_t* row_ptr;   /* [num_rows+1], nnz < 2^31 */
+  const int32_t* col_idx;   /* [nnz] strictly increasing within a row */
+  const double* values;     /* [nnz] */
+  const int32_t* tile_ptr;  /* [num_tiles+1] */
+  int64_t num_tiles;
+  int32_t exact_row_max;    /* <= GRIDLP_TILE_NNZ_CAP/2 */
+  int32_t reserved;
+} gridlp_csr_t;
+
+/*
+ * Source of the per-row sums an op consumes: either a product with a
+ * matrix block (A != NULL: sum_r = (A · gather)_r), or an ascending-order
+ * sum of partial vectors (A == NULL: sum_r = ((parts[0]_r + parts[1]_r) +
+ * ...), the reduction order of the reference communicator, comm.py:75-84;
+ * nparts == 1 after an NCCL allreduce; nparts == 0 means all-zero sums).
+ */
+typedef struct gridlp_src {
+  const gridlp_csr_t* A;
+  const double* gather;
+  const double* parts[GRIDLP_MAX_PARTS];
+  int32_t nparts;
+  int32_t reserved;
+  int64_t num_rows;         /* rows when A == NULL */
+} gridlp_src_t;
+
+/* Step parameters, DEVICE-resident so captured graphs pick up updates.
+ * tau = eta/omega, sigma = eta*omega (pdhg_engine.py:61-67); the Halpern
+ * counter of an op launched with `iter` is inner_k + iter
+ * (pdhg_engine.py:184-189, :396-400). */
+typedef struct gridlp_step {
+  double tau;
+  double sigma;
+  double gamma;
+  int64_t inner_k;
+} gridlp_step_t;
+
+/* Primal-side vectors of one grid column j (length n). x_bar is written by
+ * the primal op and gathered by the dual op. */
+typedef struct gridlp_primal {
+  double* x;
+  double* x_bar;
+  double* x_anchor;
+  const double* c;
+  const double* lo;
+  const double* hi;
+  int64_t n;
+} gridlp_primal_t;
+
+/* Dual-side vectors of one grid row i (length m). */
+typedef struct gridlp_dual {
+  double* y;
+  double* y_anchor;
+  const double* lo;   /* con_lower */
+  const double* hi;   /* con_upper */
+  int64_t m;
+} gridlp_dual_t;
+
+/* Reduction workspace: `partials` holds capacity * GRIDLP_MAX_RED doubles;
+ * the op writes its final sums to out[0..k). */
+typedef struct gridlp_red {
+  double* partials;
+  int64_t capacity;
+  double* out;
+} gridlp_red_t;
+
+/* flags */
+#define GRIDLP_F_HALPERN 1u   /* EngineConfig.halpern (pdhg_engine.py:396-399) */
+#define GRIDLP_F_SUMSQ 2u     /* op_store: also reduce sum of squares */
+
+/* --- library / device ---------------------------------------------------- */
+int gridlp_abi_version(void);
+const char* gridlp_last_error(void);
+/* SM count and L2 size of `device` (host ints). */
+int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes);
+/* Number of CTAs (reduction slots) an op over `src` launches. */
+int64_t gridlp_op_slots(const gridlp_src_t* src);
+
+/* --- products ------------------------------------------------------------ */
+/* out = sums(src). Replaces spmv (sparse_kernels.py:18-24) and
+ * spmv_transpose (:39-45) when src->A is set, and the vector AllReduce's
+ * ascending reduction (comm.py:75-84, :322-329) when src->parts is used.
+ * With GRIDLP_F_SUMSQ also red->out[0] = sum of out_r^2 (the power
+ * iteration's u_sq / s_sq, sparse_kernels.py:83, :89). */
+int gridlp_op_store(const gridlp_src_t* src, double* out, uint32_t flags,
+                    const gridlp_red_t* red, void* stream);
+
+/* --- PDHG iteration halves ------------------------------------------------ */
+/* Primal half over grid column j, rows = variables, sums = [Aᵀ y]_j:
+ *   x̂ = clip(x - tau (c - aty), lo, hi)             pdhg_engine.py:171-173
+ *   x_bar = 2 x̂ - x                                 pdhg_engine.py:233
+ *   x <- (w x̂ - gamma x) + x_anchor/(k+2)            pdhg_engine.py:184-189
+ * Replaces primal_step + the primal part of halpern_step
+ * (pdhg_engine.py:223-228, :238-242; solver_driver.py:376-382). */
+int gridlp_op_primal(const gridlp_src_t* src, const gridlp_primal_t* pv,
+                     const gridlp_step_t* d_step, int32_t iter, uint32_t flags,
+                     void* stream);
+
+/* Dual half over grid row i, rows = constraints, sums = z = [A x̄]_i:
+ *   v = y/sigma - z;  ŷ = sigma (v - clip(v, -hi, -lo))   pdhg_engine.py:176-181
+ *   y <- (w ŷ - gamma y) + y_anchor/(k+2)
+ * Replaces dual_step + the dual part of halpern_step
+ * (pdhg_engine.py:231-242; solver_driver.py:378-383). */
+int gridlp_op_dual(const gridlp_src_t* src, const gridlp_dual_t* dv,
+                   const gridlp_step_t* d_step, int32_t iter, uint32_t flags,
+                   void* stream);
+
+/* --- KKT pass (pdhg_engine.py:310-346; solver_driver.py:335-358) -------- */
+/* Constraint side, sums = [A x]_i. Writes ax (may be NULL) and reduces
+ *   out[0] = ||range_violation(ax)||^2            pdhg_engine.py:206-208, :320-321
+ *   out[1] = sum over finite hi of hi * max(-y,0)  (bound_penalty(-y), :192-203)
+ *   out[2] = sum over finite lo of lo * max(y,0)
+ *   out[3] = count of infinite-bound violations (penalty = +inf if > 0). */
+int gridlp_op_kkt_rows(const gridlp_src_t* src, const gridlp_dual_t* dv,
+                       double* ax, const gridlp_red_t* red, void* stream);
+
+/* Variable side, sums = [Aᵀ y]_j. Writes x_probe_bar = 2 x_probe - x
+ * (restart probe input, pdhg_engine.py:420) and reduces
+ *   out[0] = ||(x_probe - x)/tau||^2   out[1] = c·x
+ *   out[2] = ((x_probe - shifted)/tau)·x   out[3] = ||x - x_probe||^2
+ * (pdhg_engine.py:324-336, :424, :255). */
+int gridlp_op_kkt_cols(const gridlp_src_t* src, const gridlp_primal_t* pv,
+                       double* x_probe_bar, const gridlp_step_t* d_step,
+                       const gridlp_red_t* red, void* stream);
+
+/* Restart probe, sums = z_probe = [A x_probe_bar]_i:
+ *   y_probe = dual_update(y, z_probe)  dy = y - y_probe
+ *   out[0] = ||dy||^2
+ *   out[1] = sum 0.5 (ax - z_probe)_r dy_r   (only when ax != NULL; the
+ *            fused single-block form of the cross term, pdhg_engine.py:426)
+ * dy_out (may be NULL) receives dy for the grid form of the cross term.
+ * (pdhg_engine.py:419-427, :245-259; solver_driver.py:403-413). */
+int gridlp_op_probe(const gridlp_src_t* src, const gridlp_dual_t* dv,
+                    const double* ax, double* dy_out, const gridlp_step_t* d_step,
+                    const gridlp_red_t* red, void* stream);
+
+/* out[0] = sum_r 0.5 (a_r - b_r) d_r — the per-block cross term
+ * <A_ij dx_j, dy_i> from block-local partial products (pdhg_engine.py:257,
+ * :426). */
+int gridlp_op_halfdiff_dot(const double* a, const double* b, const double* d,
+                           int64_t n, const gridlp_red_t* red, void* stream);
+
+/* out[0] = ||v - anchor||^2 then anchor <- v (restart application:
+ * anchor distances pdhg_engine.py:433-442 and anchor reset :448-449). */
+int gridlp_op_anchor(double* v, double* anchor, int64_t n,
+                     const gridlp_red_t* red, void* stream);
+
+/* out[0] = a·b (power iteration v_sq, sparse_kernels.py:84). */
+int gridlp_op_dot(const double* a, const double* b, int64_t n,
+                  const gridlp_red_t* red, void* stream);
+
+/* out_r = in_r / divisor (v = s / sqrt(s_sq), sparse_kernels.py:92). */
+int gridlp_op_div(const double* in, double* out, int64_t n, double divisor,
+                  void* stream);
+
+/* out_r = lo/hi projection of 0 (initial_device_state, pdhg_engine.py:349-353),
+ * anchor_r = out_r. */
+int gridlp_op_init_primal(const gridlp_primal_t* pv, void* stream);
+
+/* d_step->inner_k += delta on the device (a captured chunk of `delta`
+ * iterations advances the Halpern counter itself, pdhg_engine.py:400). */
+int gridlp_op_step_advance(gridlp_step_t* d_step, int64_t delta, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRIDLP_B200_H */

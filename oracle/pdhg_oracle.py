@@ -402,16 +402,27 @@ class _Grid:
         self.lc = [lc[a0:a1].copy() for a0, a1 in self.rr]
         self.uc = [uc[a0:a1].copy() for a0, a1 in self.rr]
 
+    pool = None   # optional ThreadPoolExecutor: one host thread per block, like the
+    #               reference's "threads" executor (comm.py:197-222); scipy releases
+    #               the GIL so block products overlap. Results are unchanged.
+
+    def _map(self, f, keys):
+        if self.pool is None:
+            return {k: f(k) for k in keys}
+        return dict(zip(keys, self.pool.map(f, keys)))
+
     # axis-reduced products --------------------------------------------------
     def col_products(self, xs):
         """z_i = AllReduce_C(A_ij x_j), plus the partials."""
-        part = {(i, j): seq_spmv(self.A[i, j], xs[j]) for i in range(self.R) for j in range(self.C)}
+        keys = [(i, j) for i in range(self.R) for j in range(self.C)]
+        part = self._map(lambda k: seq_spmv(self.A[k], xs[k[1]]), keys)
         red = [_asc([part[i, j] for j in range(self.C)]) for i in range(self.R)]
         return red, part
 
     def row_products(self, ys):
         """s_j = AllReduce_R(A_ij^T y_i)."""
-        part = {(i, j): seq_spmv(self.AT[i, j], ys[i]) for i in range(self.R) for j in range(self.C)}
+        keys = [(i, j) for i in range(self.R) for j in range(self.C)]
+        part = self._map(lambda k: seq_spmv(self.AT[k], ys[k[0]]), keys)
         return [_asc([part[i, j] for i in range(self.R)]) for j in range(self.C)]
 
     def g_sum(self, f):
@@ -595,3 +606,43 @@ def power_estimate(problem, seed=0, iters=30, **layout_opts) -> float:
                       seed, layout_opts.get("permutation", "block_random"),
                       layout_opts.get("partitioning", "nnz"), layout_opts.get("grid"))
     return _power(_Grid(problem, lay), iters, probe_vector(a.shape[1], seed))
+
+
+def iteration_rate(problem, iters: int, grid=(1, 1), threads: int = 1, eta: float = 0.01,
+                   seed: int = 0) -> dict:
+    """Throughput of the reference's main-loop iteration (pdhg_engine.py:394-403,
+    solver_driver.py:376-386) on the host: builds the grid blocks untimed, then
+    times `iters` iterations (2 products + projections + Halpern per block).
+    With threads > 1 the block products run on a thread pool, as the
+    reference's threads executor does."""
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+
+    a = as_csr(problem.matrix)
+    lay = make_layout(a, grid[0] * grid[1], 64, seed, "block_random", "nnz", tuple(grid))
+    t0 = time.perf_counter()
+    g = _Grid(problem, lay)
+    setup = time.perf_counter() - t0
+    if threads > 1:
+        g.pool = ThreadPoolExecutor(max_workers=threads)
+    R, C = g.R, g.C
+    omega = 1.0
+    xs = [np.clip(np.zeros(c1 - c0), g.lv[j], g.uv[j]) for j, (c0, c1) in enumerate(g.cr)]
+    ys = [np.zeros(r1 - r0) for r0, r1 in g.rr]
+    x0 = [v.copy() for v in xs]
+    y0 = [v.copy() for v in ys]
+    tau, sigma = eta / omega, eta * omega
+    t0 = time.perf_counter()
+    for k in range(iters):
+        aty = g.row_products(ys)
+        xh = [primal_map(xs[j], g.c[j], aty[j], tau, g.lv[j], g.uv[j]) for j in range(C)]
+        xb = [2.0 * xh[j] - xs[j] for j in range(C)]
+        z, _ = g.col_products(xb)
+        yh = [dual_map(ys[i], z[i], sigma, g.lc[i], g.uc[i]) for i in range(R)]
+        xs = [anchor_mix(xh[j], xs[j], x0[j], k, 0.0) for j in range(C)]
+        ys = [anchor_mix(yh[i], ys[i], y0[i], k, 0.0) for i in range(R)]
+    dt = time.perf_counter() - t0
+    if g.pool is not None:
+        g.pool.shutdown()
+    return {"iterations": iters, "seconds": dt, "iters_per_s": iters / dt if dt > 0 else float("inf"),
+            "setup_seconds": setup, "grid": [R, C], "threads": threads}

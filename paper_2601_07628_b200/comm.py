@@ -1,0 +1,172 @@
+"""Collective contract of the grid and its two executors.
+
+Reference contract (/root/reference/pkg/src/gridlp/comm.py): axis-scoped
+sum-AllReduce — R reduces down a grid column (over i), C along a grid row
+(over j), G over all devices — with deterministic ascending-rank order
+(:75-84), replicated results and per-device logical counters that count
+every call, even on singleton groups (:322-335).
+
+Executors:
+  * `VirtualGrid` — one process, one GPU, every block of the R x C grid
+    resident in that GPU's HBM. A vector reduction is the ascending-order
+    sum of the block partials, fused into the consuming epilogue kernel
+    (bit-identical to the reference's simulated grid).
+  * `NcclGrid` — one process per GPU (torchrun), device (i, j) = rank
+    i*C + j, NCCL over NVLink on per-column (R axis) and per-row (C axis)
+    sub-communicators for the vector sums. Scalars of a pass are gathered
+    once over the world group and reduced on every rank in ascending order,
+    so every rank takes identical restart/termination decisions (the
+    reference's "replicated, never broadcast" rule, pdhg_engine.py:18-19).
+"""
+
+from __future__ import annotations
+
+from collections import Counter
+
+import numpy as np
+import torch
+
+AXES = ("R", "C", "G")
+
+
+class Ledger:
+    """Logical collective counters (comm.py:61-72, :322-335). Every device
+    issues the same sequence, so events are recorded once and expanded per
+    device with that device's vector lengths (m_i for C, n_j for R)."""
+
+    def __init__(self):
+        self.events = Counter()   # (axis, kind, length_key) -> calls
+
+    def vec(self, axis: str, length_key: str, times: int = 1):
+        self.events[(axis, "vec", length_key)] += times
+
+    def scalar(self, axis: str, times: int = 1):
+        self.events[(axis, "scalar", "1")] += times
+
+    def snapshot(self):
+        return Counter(self.events)
+
+    @staticmethod
+    def expand(events, layout) -> list:
+        R, C = layout.topology.rows, layout.topology.cols
+        out = []
+        for i in range(R):
+            m_i = int(layout.row_cuts[i + 1] - layout.row_cuts[i])
+            for j in range(C):
+                n_j = int(layout.col_cuts[j + 1] - layout.col_cuts[j])
+                size = {"m": m_i, "n": n_j, "1": 1}
+                axes = {a: {"vector_calls": 0, "scalar_calls": 0, "elements_reduced": 0} for a in AXES}
+                for (axis, kind, key), cnt in events.items():
+                    d = axes[axis]
+                    d["vector_calls" if kind == "vec" else "scalar_calls"] += cnt
+                    d["elements_reduced"] += cnt * size[key]
+                out.append({"device": [i, j], "axes": axes})
+        return out
+
+    @staticmethod
+    def diff(after, before):
+        d = Counter(after)
+        d.subtract(before)
+        return d
+
+    @staticmethod
+    def grid_total(per_device: list) -> dict:
+        tot = {a: {"vector_calls": 0, "scalar_calls": 0, "elements_reduced": 0} for a in AXES}
+        for entry in per_device:
+            for a in AXES:
+                for k in tot[a]:
+                    tot[a][k] += entry["axes"][a][k]
+        return tot
+
+
+def asc_sum(values):
+    """Ascending-order scalar reduction (comm.py:75-84)."""
+    acc = values[0]
+    for v in values[1:]:
+        acc = acc + v
+    return acc
+
+
+class VirtualGrid:
+    """All blocks in one process on one device."""
+
+    kind = "virtual"
+
+    def __init__(self, rows: int, cols: int):
+        self.rows, self.cols = rows, cols
+        self.local = [(i, j) for i in range(rows) for j in range(cols)]
+        self.rank = 0
+        self.world = 1
+        self.active = True
+
+    def reduce(self, axis, index, partials, scratch=None):
+        """Return the partial list (ascending); the consuming kernel sums it."""
+        return list(partials)
+
+    def table(self, local_rows: dict) -> dict:
+        return local_rows
+
+    def gather_vectors(self, local: dict, lengths: dict, device) -> dict:
+        return local
+
+    def barrier(self):
+        pass
+
+
+class NcclGrid:
+    """One device per rank over torch.distributed (NCCL on GPUs; gloo works
+    for the host-logic tests on CPU)."""
+
+    kind = "nccl"
+
+    def __init__(self, rows: int, cols: int, device):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise RuntimeError("NcclGrid needs an initialised torch.distributed process group")
+        self.dist = dist
+        self.rows, self.cols = rows, cols
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        if self.world < rows * cols:
+            raise ValueError(f"grid {rows}x{cols} needs {rows * cols} ranks, world size is {self.world}")
+        self.device = device
+        self.active = self.rank < rows * cols
+        self.coord = (self.rank // cols, self.rank % cols) if self.active else None
+        self.local = [self.coord] if self.active else []
+        # every rank must create every group, in the same order
+        self.col_groups = [dist.new_group([i * cols + j for i in range(rows)]) for j in range(cols)]
+        self.row_groups = [dist.new_group([i * cols + j for j in range(cols)]) for i in range(rows)]
+        self.active_group = dist.new_group(list(range(rows * cols)))
+
+    def reduce(self, axis, index, partials, scratch=None):
+        (p,) = partials
+        buf = p if scratch is None else scratch.copy_(p)
+        group = self.col_groups[index] if axis == "R" else self.row_groups[index]
+        if (axis == "R" and self.rows > 1) or (axis == "C" and self.cols > 1):
+            self.dist.all_reduce(buf, group=group)
+        return [buf]
+
+    def table(self, local_rows: dict) -> dict:
+        """All-gather each active rank's scalar row over the active group."""
+        (coord, row), = local_rows.items()
+        row = np.asarray(row, dtype=np.float64)
+        t = torch.as_tensor(row, device=self.device)
+        out = torch.empty((self.rows * self.cols, len(row)), dtype=torch.float64, device=self.device)
+        self.dist.all_gather_into_tensor(out, t, group=self.active_group)
+        full = out.cpu().numpy()
+        return {(r // self.cols, r % self.cols): full[r] for r in range(self.rows * self.cols)}
+
+    def gather_vectors(self, local: dict, lengths: dict, device) -> dict:
+        """{coord: tensor} of every active rank (padded all_gather)."""
+        (coord, vec), = local.items()
+        width = max(lengths.values()) if lengths else 0
+        buf = torch.zeros(width, dtype=torch.float64, device=self.device)
+        buf[: vec.numel()] = vec
+        out = torch.empty((self.rows * self.cols, width), dtype=torch.float64, device=self.device)
+        self.dist.all_gather_into_tensor(out, buf, group=self.active_group)
+        return {(r // self.cols, r % self.cols): out[r, : lengths[(r // self.cols, r % self.cols)]]
+                for r in range(self.rows * self.cols)}
+
+    def barrier(self):
+        self.dist.barrier()

@@ -1,0 +1,700 @@
+// gridlp_b200.cu — sm_100a kernels + C ABI for the distributed-PDHG hot path.
+//
+// Design:
+//  * Sparse products run over a tile directory of each CSR block. A light
+//    tile (<= 256 rows, <= 4096 nnz) is processed by one 256-thread CTA in
+//    two phases: (a) all threads stream values/column indices (coalesced,
+//    L2 evict-first) and gather the dense vector (L2 evict-last), writing
+//    the rounded products val*x into shared memory — this balances the
+//    gathers over the CTA regardless of row lengths; (b) one thread per row
+//    adds its products left to right from +0.0 and applies the fused PDHG
+//    epilogue. Because each product is rounded and then added in index
+//    order, the row sum is bit-identical to scipy's csr_matvec — the
+//    reference's kernel (sparse_kernels.py:18-24). A heavy tile (one row
+//    longer than exact_row_max) is tree-summed by the whole CTA.
+//  * The epilogue's per-row vector reads (x, c, bounds, anchor) are issued
+//    before phase (a) so their DRAM latency overlaps the gathers.
+//  * No FMA contraction anywhere: every multiply/add/divide is an explicit
+//    __d*_rn so each numpy expression of the reference is reproduced
+//    operation for operation.
+//  * Reductions are deterministic: fixed warp-shuffle tree per CTA, one
+//    slot per CTA, then one fixed-order final pass.
+#include "../../include/gridlp_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+namespace {
+
+constexpr int TPB = 256;
+constexpr int WARPS = TPB / 32;
+constexpr int CAP = GRIDLP_TILE_NNZ_CAP;
+constexpr int UNROLL = 8;
+constexpr int64_t ROWS_MAX_BLOCKS = 1184;  // 8 x 148 SMs
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return GRIDLP_OK;
+}
+
+// ---------------------------------------------------------------- device math
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// numpy.maximum for float64: NaN-propagating, returns b on ties (incl. ±0).
+__device__ __forceinline__ double np_maximum(double a, double b) {
+  return (isnan(a) || a > b) ? a : b;
+}
+// numpy.clip(x, lo, hi) = _NPY_MIN(_NPY_MAX(x, lo), hi) (numpy clip.cpp).
+__device__ __forceinline__ double np_clip(double x, double lo, double hi) {
+  double t = isnan(x) ? x : (x > lo ? x : lo);
+  return isnan(t) ? t : (t < hi ? t : hi);
+}
+
+// Halpern weights, bit-identical to the Python float expressions
+// (1.0 + gamma) * (k + 1.0) / (k + 2.0) and 1.0 / (k + 2.0)
+// (pdhg_engine.py:187-188).
+__device__ __forceinline__ void halpern_weights(double gamma, int64_t k, double& wm, double& wa) {
+  const double kd = (double)k;
+  const double k2 = dadd(kd, 2.0);
+  wm = ddiv(dmul(dadd(1.0, gamma), dadd(kd, 1.0)), k2);
+  wa = ddiv(1.0, k2);
+}
+// (w_map * mapped - gamma * current) + w_anchor * anchor (pdhg_engine.py:189)
+__device__ __forceinline__ double halpern_mix(double t, double cur, double anc, double wm,
+                                              double gamma, double wa) {
+  return dadd(dsub(dmul(wm, t), dmul(gamma, cur)), dmul(wa, anc));
+}
+
+// ------------------------------------------------------------ cache policies
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p, uint64_t pol) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// ------------------------------------------------------- deterministic sums
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum NR per-thread accumulators over the CTA; result valid in thread 0.
+template <int NR>
+__device__ __forceinline__ void block_sum(double (&acc)[NR], double (*scratch)[WARPS]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    double v = warp_sum(acc[q]);
+    if (lane == 0) scratch[q][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      double s = scratch[q][0];
+#pragma unroll
+      for (int w = 1; w < WARPS; ++w) s = dadd(s, scratch[q][w]);
+      acc[q] = s;
+    }
+  }
+}
+
+// --------------------------------------------------------------- epilogues
+// Each op: NRED reduction slots; load(r) fetches the row's operands (issued
+// early); row(r, sum, data, acc) applies the epilogue.
+
+struct Empty {};
+
+template <bool SUMSQ>
+struct OpStore {
+  static constexpr int NRED = SUMSQ ? 1 : 0;
+  double* out;
+  using Data = Empty;
+  __device__ void prepare() {}
+  __device__ Data load(int64_t) const { return {}; }
+  __device__ void row(int64_t r, double s, const Data&, double* acc) const {
+    out[r] = s;
+    if (SUMSQ) acc[0] = dadd(acc[0], dmul(s, s));
+  }
+};
+
+struct OpPrimal {
+  static constexpr int NRED = 0;
+  double* x;
+  double* xbar;
+  const double* x0;
+  const double* c;
+  const double* lo;
+  const double* hi;
+  const gridlp_step_t* step;
+  int32_t iter;
+  bool halpern;
+  double tau, gamma, wm, wa;
+  struct Data { double x, c, lo, hi, x0; };
+  __device__ void prepare() {
+    tau = step->tau;
+    gamma = step->gamma;
+    halpern_weights(gamma, step->inner_k + iter, wm, wa);
+  }
+  __device__ Data load(int64_t r) const {
+    Data d;
+    d.x = x[r]; d.c = c[r]; d.lo = lo[r]; d.hi = hi[r];
+    d.x0 = halpern ? x0[r] : 0.0;
+    return d;
+  }
+  __device__ void row(int64_t r, double aty, const Data& d, double*) const {
+    const double xh = np_clip(dsub(d.x, dmul(tau, dsub(d.c, aty))), d.lo, d.hi);
+    xbar[r] = dsub(dmul(2.0, xh), d.x);
+    x[r] = halpern ? halpern_mix(xh, d.x, d.x0, wm, gamma, wa) : xh;
+  }
+};
+
+// v = y/sigma - z; sigma * (v - clip(v, -hi, -lo))  (pdhg_engine.py:176-181)
+__device__ __forceinline__ double dual_map(double y, double z, double sigma, double lo, double hi) {
+  const double v = dsub(ddiv(y, sigma), z);
+  return dmul(sigma, dsub(v, np_clip(v, -hi, -lo)));
+}
+
+struct OpDual {
+  static constexpr int NRED = 0;
+  double* y;
+  const double* y0;
+  const double* lo;
+  const double* hi;
+  const gridlp_step_t* step;
+  int32_t iter;
+  bool halpern;
+  double sigma, gamma, wm, wa;
+  struct Data { double y, lo, hi, y0; };
+  __device__ void prepare() {
+    sigma = step->sigma;
+    gamma = step->gamma;
+    halpern_weights(gamma, step->inner_k + iter, wm, wa);
+  }
+  __device__ Data load(int64_t r) const {
+    Data d;
+    d.y = y[r]; d.lo = lo[r]; d.hi = hi[r];
+    d.y0 = halpern ? y0[r] : 0.0;
+    return d;
+  }
+  __device__ void row(int64_t r, double z, const Data& d, double*) const {
+    const double yh = dual_map(d.y, z, sigma, d.lo, d.hi);
+    y[r] = halpern ? halpern_mix(yh, d.y, d.y0, wm, gamma, wa) : yh;
+  }
+};
+
+struct OpKktRows {
+  static constexpr int NRED = 4;
+  const double* y;
+  const double* lo;
+  const double* hi;
+  double* ax;
+  struct Data { double y, lo, hi; };
+  __device__ void prepare() {}
+  __device__ Data load(int64_t r) const { return {y[r], lo[r], hi[r]}; }
+  __device__ void row(int64_t r, double s, const Data& d, double* acc) const {
+    if (ax) ax[r] = s;
+    // range_violation (pdhg_engine.py:206-208)
+    const double rv = dsub(np_maximum(dsub(s, d.hi), 0.0), np_maximum(dsub(d.lo, s), 0.0));
+    acc[0] = dadd(acc[0], dmul(rv, rv));
+    // bound_penalty(-y) (pdhg_engine.py:192-203)
+    const double v = -d.y;
+    const double pos = np_maximum(v, 0.0);
+    const double neg = np_maximum(-v, 0.0);
+    const bool fu = isfinite(d.hi), fl = isfinite(d.lo);
+    if (fu) acc[1] = dadd(acc[1], dmul(d.hi, pos));
+    else if (pos > 0.0) acc[3] = dadd(acc[3], 1.0);
+    if (fl) acc[2] = dadd(acc[2], dmul(d.lo, neg));
+    else if (neg > 0.0) acc[3] = dadd(acc[3], 1.0);
+  }
+};
+
+struct OpKktCols {
+  static constexpr int NRED = 4;
+  const double* x;
+  const double* c;
+  const double* lo;
+  const double* hi;
+  double* xpb;
+  const gridlp_step_t* step;
+  double tau;
+  struct Data { double x, c, lo, hi; };
+  __device__ void prepare() { tau = step->tau; }
+  __device__ Data load(int64_t r) const { return {x[r], c[r], lo[r], hi[r]}; }
+  __device__ void row(int64_t r, double aty, const Data& d, double* acc) const {
+    // pdhg_engine.py:325-336
+    const double shifted = dsub(d.x, dmul(tau, dsub(d.c, aty)));
+    const double xp = np_clip(shifted, d.lo, d.hi);
+    const double rd = ddiv(dsub(xp, d.x), tau);
+    const double rc = ddiv(dsub(xp, shifted), tau);
+    const double dx = dsub(d.x, xp);
+    acc[0] = dadd(acc[0], dmul(rd, rd));
+    acc[1] = dadd(acc[1], dmul(d.c, d.x));
+    acc[2] = dadd(acc[2], dmul(rc, d.x));
+    acc[3] = dadd(acc[3], dmul(dx, dx));
+    if (xpb) xpb[r] = dsub(dmul(2.0, xp), d.x);
+  }
+};
+
+struct OpProbe {
+  static constexpr int NRED = 2;
+  const double* y;
+  const double* lo;
+  const double* hi;
+  const double* ax;
+  double* dy_out;
+  const gridlp_step_t* step;
+  double sigma;
+  struct Data { double y, lo, hi, ax; };
+  __device__ void prepare() { sigma = step->sigma; }
+  __device__ Data load(int64_t r) const { return {y[r], lo[r], hi[r], ax ? ax[r] : 0.0}; }
+  __device__ void row(int64_t r, double z, const Data& d, double* acc) const {
+    const double yp = dual_map(d.y, z, sigma, d.lo, d.hi);
+    const double dy = dsub(d.y, yp);
+    acc[0] = dadd(acc[0], dmul(dy, dy));
+    if (ax) acc[1] = dadd(acc[1], dmul(dmul(0.5, dsub(d.ax, z)), dy));
+    if (dy_out) dy_out[r] = dy;
+  }
+};
+
+struct OpHalfDiffDot {
+  static constexpr int NRED = 1;
+  const double* a;
+  const double* b;
+  const double* d;
+  using Data = Empty;
+  __device__ void prepare() {}
+  __device__ Data load(int64_t) const { return {}; }
+  __device__ void row(int64_t r, double, const Data&, double* acc) const {
+    acc[0] = dadd(acc[0], dmul(dmul(0.5, dsub(a[r], b[r])), d[r]));
+  }
+};
+
+struct OpAnchor {
+  static constexpr int NRED = 1;
+  double* v;
+  double* anchor;
+  using Data = Empty;
+  __device__ void prepare() {}
+  __device__ Data load(int64_t) const { return {}; }
+  __device__ void row(int64_t r, double, const Data&, double* acc) const {
+    const double cur = v[r];
+    const double e = dsub(cur, anchor[r]);
+    acc[0] = dadd(acc[0], dmul(e, e));
+    anchor[r] = cur;
+  }
+};
+
+struct OpDot {
+  static constexpr int NRED = 1;
+  const double* a;
+  const double* b;
+  using Data = Empty;
+  __device__ void prepare() {}
+  __device__ Data load(int64_t) const { return {}; }
+  __device__ void row(int64_t r, double, const Data&, double* acc) const {
+    acc[0] = dadd(acc[0], dmul(a[r], b[r]));
+  }
+};
+
+struct OpDiv {
+  static constexpr int NRED = 0;
+  const double* in;
+  double* out;
+  double divisor;
+  using Data = Empty;
+  __device__ void prepare() {}
+  __device__ Data load(int64_t) const { return {}; }
+  __device__ void row(int64_t r, double, const Data&, double*) const { out[r] = ddiv(in[r], divisor); }
+};
+
+struct OpInitPrimal {
+  static constexpr int NRED = 0;
+  double* x;
+  double* anchor;
+  const double* lo;
+  const double* hi;
+  using Data = Empty;
+  __device__ void prepare() {}
+  __device__ Data load(int64_t) const { return {}; }
+  __device__ void row(int64_t r, double, const Data&, double*) const {
+    const double v = np_clip(0.0, lo[r], hi[r]);
+    x[r] = v;
+    anchor[r] = v;
+  }
+};
+
+// ------------------------------------------------------------------ kernels
+template <int NR>
+struct AccN { double v[NR > 0 ? NR : 1]; };
+
+template <class Op>
+__device__ __forceinline__ void store_partials(double (&acc)[Op::NRED > 0 ? Op::NRED : 1],
+                                               double* partials) {
+  if constexpr (Op::NRED > 0) {
+    __shared__ double scratch[Op::NRED][WARPS];
+    block_sum<Op::NRED>(acc, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < Op::NRED; ++q) partials[(int64_t)blockIdx.x * GRIDLP_MAX_RED + q] = acc[q];
+    }
+  }
+}
+
+// Sparse-product + fused-epilogue kernel over a tile directory.
+template <class Op>
+__global__ void __launch_bounds__(TPB) tile_kernel(gridlp_csr_t A, const double* __restrict__ g,
+                                                   Op op, double* __restrict__ partials) {
+  extern __shared__ double prod[];
+  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+
+  const int tid = threadIdx.x;
+  const int64_t t = blockIdx.x;
+  const int r0 = A.tile_ptr[t];
+  const int r1 = A.tile_ptr[t + 1];
+  const int p0 = A.row_ptr[r0];
+  const int p1 = A.row_ptr[r1];
+  op.prepare();
+  const uint64_t pf = policy_evict_first();
+  const uint64_t pl = policy_evict_last();
+  const int* __restrict__ col = A.col_idx;
+  const double* __restrict__ val = A.values;
+
+  if (r1 - r0 == 1 && p1 - p0 > A.exact_row_max) {
+    // heavy row: CTA-wide strided products, deterministic tree sum
+    typename Op::Data d{};
+    if (tid == 0) d = op.load(r0);
+    double s = 0.0;
+    for (int k = p0 + tid; k < p1; k += TPB)
+      s = dadd(s, dmul(ld_stream(val + k, pf), ld_gather(g + ld_stream(col + k, pf), pl)));
+    double tmp[1] = {s};
+    __shared__ double hscratch[1][WARPS];
+    block_sum<1>(tmp, hscratch);
+    if (tid == 0) op.row(r0, tmp[0], d, acc);
+    __syncthreads();
+  } else {
+    const int r = r0 + tid;
+    const bool mine = r < r1;
+    typename Op::Data d{};
+    int a = 0, b = 0;
+    if (mine) {
+      d = op.load(r);
+      a = A.row_ptr[r] - p0;
+      b = A.row_ptr[r + 1] - p0;
+    }
+    // phase (a): balanced gathers, rounded products into shared memory
+    for (int base = p0 + tid; base < p1; base += TPB * UNROLL) {
+      int cidx[UNROLL];
+      double v[UNROLL], xv[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int k = base + u * TPB;
+        cidx[u] = k < p1 ? ld_stream(col + k, pf) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int k = base + u * TPB;
+        v[u] = k < p1 ? ld_stream(val + k, pf) : 0.0;
+        xv[u] = k < p1 ? ld_gather(g + cidx[u], pl) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int k = base + u * TPB;
+        if (k < p1) prod[k - p0] = dmul(v[u], xv[u]);
+      }
+    }
+    __syncthreads();
+    // phase (b): sequential row sums (scipy csr_matvec order) + epilogue
+    if (mine) {
+      double s = 0.0;
+      for (int k = a; k < b; ++k) s = dadd(s, prod[k]);
+      op.row(r, s, d, acc);
+    }
+  }
+  store_partials<Op>(acc, partials);
+}
+
+// Row-wise epilogue over ascending-order sums of partial vectors.
+template <class Op>
+__global__ void __launch_bounds__(TPB) rows_kernel(gridlp_src_t src, int64_t n, Op op,
+                                                   double* __restrict__ partials) {
+  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+  op.prepare();
+  const int np = src.nparts;
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+    const typename Op::Data d = op.load(r);
+    double s = 0.0;
+    if (np > 0) {
+      s = src.parts[0][r];
+      for (int q = 1; q < np; ++q) s = dadd(s, src.parts[q][r]);
+    }
+    op.row(r, s, d, acc);
+  }
+  store_partials<Op>(acc, partials);
+}
+
+// Fixed-order final reduction of per-CTA slots.
+__global__ void __launch_bounds__(TPB) reduce_kernel(const double* __restrict__ partials,
+                                                     int64_t nslots, int nred,
+                                                     double* __restrict__ out) {
+  __shared__ double scratch[GRIDLP_MAX_RED][WARPS];
+  double acc[GRIDLP_MAX_RED];
+#pragma unroll
+  for (int q = 0; q < GRIDLP_MAX_RED; ++q) acc[q] = 0.0;
+  for (int64_t s = threadIdx.x; s < nslots; s += TPB) {
+#pragma unroll
+    for (int q = 0; q < GRIDLP_MAX_RED; ++q)
+      if (q < nred) acc[q] = dadd(acc[q], partials[s * GRIDLP_MAX_RED + q]);
+  }
+  block_sum<GRIDLP_MAX_RED>(acc, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < nred; ++q) out[q] = acc[q];
+}
+
+__global__ void step_advance_kernel(gridlp_step_t* st, int64_t delta) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) st->inner_k += delta;
+}
+
+// ------------------------------------------------------------------ host side
+int64_t rows_blocks(int64_t n) {
+  int64_t b = (n + TPB - 1) / TPB;
+  if (b < 1) b = 1;
+  return b < ROWS_MAX_BLOCKS ? b : ROWS_MAX_BLOCKS;
+}
+
+int check_csr(const gridlp_csr_t* A) {
+  if (!A) return fail(GRIDLP_ERR_ARG, "null matrix");
+  if (A->num_rows < 0 || A->num_cols < 0 || A->nnz < 0 || A->num_tiles < 0)
+    return fail(GRIDLP_ERR_ARG, "negative matrix dimension");
+  if (A->nnz >= (int64_t(1) << 31)) return fail(GRIDLP_ERR_ARG, "block nnz must be < 2^31");
+  if (A->exact_row_max < 0 || A->exact_row_max > CAP / 2)
+    return fail(GRIDLP_ERR_ARG, "exact_row_max must be in [0, TILE_NNZ_CAP/2]");
+  if (A->num_rows > 0 && (!A->row_ptr || !A->tile_ptr || A->num_tiles < 1))
+    return fail(GRIDLP_ERR_ARG, "missing row_ptr/tile_ptr");
+  if (A->nnz > 0 && (!A->col_idx || !A->values)) return fail(GRIDLP_ERR_ARG, "missing col_idx/values");
+  return GRIDLP_OK;
+}
+
+int64_t src_rows(const gridlp_src_t* src) { return src->A ? src->A->num_rows : src->num_rows; }
+
+template <class Op>
+int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* stream,
+              const char* name) {
+  if (!src) return fail(GRIDLP_ERR_ARG, std::string(name) + ": null source");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = src_rows(src);
+  int64_t slots;
+  if (src->A) {
+    int rc = check_csr(src->A);
+    if (rc) return rc;
+    if (src->A->num_rows > 0 && src->A->nnz > 0 && !src->gather)
+      return fail(GRIDLP_ERR_ARG, std::string(name) + ": missing gather vector");
+    slots = src->A->num_rows > 0 ? src->A->num_tiles : 0;
+  } else {
+    if (src->nparts < 0 || src->nparts > GRIDLP_MAX_PARTS)
+      return fail(GRIDLP_ERR_ARG, std::string(name) + ": nparts out of range");
+    for (int q = 0; q < src->nparts; ++q)
+      if (!src->parts[q] && n > 0) return fail(GRIDLP_ERR_ARG, std::string(name) + ": null part");
+    slots = n > 0 ? rows_blocks(n) : 0;
+  }
+  double* partials = nullptr;
+  if (Op::NRED > 0) {
+    if (!red || !red->out) return fail(GRIDLP_ERR_ARG, std::string(name) + ": reduction output required");
+    if (slots > 0) {
+      if (!red->partials || red->capacity < slots)
+        return fail(GRIDLP_ERR_WORKSPACE, std::string(name) + ": reduction workspace too small (need " +
+                                              std::to_string(slots) + " slots)");
+      partials = red->partials;
+    }
+  }
+  if (slots > 0) {
+    if (src->A) {
+      tile_kernel<Op><<<(unsigned)slots, TPB, CAP * sizeof(double), s>>>(*src->A, src->gather, op, partials);
+    } else {
+      rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials);
+    }
+    int rc = check_launch(name);
+    if (rc) return rc;
+  }
+  if (Op::NRED > 0) {
+    reduce_kernel<<<1, TPB, 0, s>>>(partials, slots, Op::NRED, red->out);
+    int rc = check_launch(name);
+    if (rc) return rc;
+  }
+  return GRIDLP_OK;
+}
+
+gridlp_src_t rows_src(int64_t n) {
+  gridlp_src_t s;
+  std::memset(&s, 0, sizeof(s));
+  s.num_rows = n;
+  return s;
+}
+
+struct KernelAttrInit {
+  KernelAttrInit() {}
+};
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int gridlp_abi_version(void) { return GRIDLP_ABI_VERSION; }
+
+const char* gridlp_last_error(void) { return g_err.c_str(); }
+
+int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes) {
+  int v = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("device_info: ") + cudaGetErrorString(e));
+  if (sm_count) *sm_count = v;
+  e = cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device);
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("device_info: ") + cudaGetErrorString(e));
+  if (l2_bytes) *l2_bytes = v;
+  return GRIDLP_OK;
+}
+
+int64_t gridlp_op_slots(const gridlp_src_t* src) {
+  if (!src) return 0;
+  if (src->A) return src->A->num_rows > 0 ? src->A->num_tiles : 0;
+  return src->num_rows > 0 ? rows_blocks(src->num_rows) : 0;
+}
+
+int gridlp_op_store(const gridlp_src_t* src, double* out, uint32_t flags, const gridlp_red_t* red,
+                    void* stream) {
+  if (!src) return fail(GRIDLP_ERR_ARG, "op_store: null source");
+  if (!out && src_rows(src) > 0) return fail(GRIDLP_ERR_ARG, "op_store: null output");
+  if (flags & GRIDLP_F_SUMSQ) return launch_op(src, OpStore<true>{out}, red, stream, "op_store");
+  return launch_op(src, OpStore<false>{out}, red, stream, "op_store");
+}
+
+int gridlp_op_primal(const gridlp_src_t* src, const gridlp_primal_t* pv, const gridlp_step_t* d_step,
+                     int32_t iter, uint32_t flags, void* stream) {
+  if (!pv || !d_step) return fail(GRIDLP_ERR_ARG, "op_primal: null argument");
+  if (src && src_rows(src) != pv->n) return fail(GRIDLP_ERR_ARG, "op_primal: length mismatch");
+  OpPrimal op{};
+  op.x = pv->x; op.xbar = pv->x_bar; op.x0 = pv->x_anchor; op.c = pv->c; op.lo = pv->lo; op.hi = pv->hi;
+  op.step = d_step; op.iter = iter; op.halpern = (flags & GRIDLP_F_HALPERN) != 0;
+  return launch_op(src, op, nullptr, stream, "op_primal");
+}
+
+int gridlp_op_dual(const gridlp_src_t* src, const gridlp_dual_t* dv, const gridlp_step_t* d_step,
+                   int32_t iter, uint32_t flags, void* stream) {
+  if (!dv || !d_step) return fail(GRIDLP_ERR_ARG, "op_dual: null argument");
+  if (src && src_rows(src) != dv->m) return fail(GRIDLP_ERR_ARG, "op_dual: length mismatch");
+  OpDual op{};
+  op.y = dv->y; op.y0 = dv->y_anchor; op.lo = dv->lo; op.hi = dv->hi;
+  op.step = d_step; op.iter = iter; op.halpern = (flags & GRIDLP_F_HALPERN) != 0;
+  return launch_op(src, op, nullptr, stream, "op_dual");
+}
+
+int gridlp_op_kkt_rows(const gridlp_src_t* src, const gridlp_dual_t* dv, double* ax,
+                       const gridlp_red_t* red, void* stream) {
+  if (!dv) return fail(GRIDLP_ERR_ARG, "op_kkt_rows: null argument");
+  if (src && src_rows(src) != dv->m) return fail(GRIDLP_ERR_ARG, "op_kkt_rows: length mismatch");
+  OpKktRows op{dv->y, dv->lo, dv->hi, ax};
+  return launch_op(src, op, red, stream, "op_kkt_rows");
+}
+
+int gridlp_op_kkt_cols(const gridlp_src_t* src, const gridlp_primal_t* pv, double* x_probe_bar,
+                       const gridlp_step_t* d_step, const gridlp_red_t* red, void* stream) {
+  if (!pv || !d_step) return fail(GRIDLP_ERR_ARG, "op_kkt_cols: null argument");
+  if (src && src_rows(src) != pv->n) return fail(GRIDLP_ERR_ARG, "op_kkt_cols: length mismatch");
+  OpKktCols op{};
+  op.x = pv->x; op.c = pv->c; op.lo = pv->lo; op.hi = pv->hi; op.xpb = x_probe_bar; op.step = d_step;
+  return launch_op(src, op, red, stream, "op_kkt_cols");
+}
+
+int gridlp_op_probe(const gridlp_src_t* src, const gridlp_dual_t* dv, const double* ax, double* dy_out,
+                    const gridlp_step_t* d_step, const gridlp_red_t* red, void* stream) {
+  if (!dv || !d_step) return fail(GRIDLP_ERR_ARG, "op_probe: null argument");
+  if (src && src_rows(src) != dv->m) return fail(GRIDLP_ERR_ARG, "op_probe: length mismatch");
+  OpProbe op{};
+  op.y = dv->y; op.lo = dv->lo; op.hi = dv->hi; op.ax = ax; op.dy_out = dy_out; op.step = d_step;
+  return launch_op(src, op, red, stream, "op_probe");
+}
+
+int gridlp_op_halfdiff_dot(const double* a, const double* b, const double* d, int64_t n,
+                           const gridlp_red_t* red, void* stream) {
+  if (n < 0 || (n > 0 && (!a || !b || !d))) return fail(GRIDLP_ERR_ARG, "op_halfdiff_dot: bad argument");
+  gridlp_src_t src = rows_src(n);
+  return launch_op(&src, OpHalfDiffDot{a, b, d}, red, stream, "op_halfdiff_dot");
+}
+
+int gridlp_op_anchor(double* v, double* anchor, int64_t n, const gridlp_red_t* red, void* stream) {
+  if (n < 0 || (n > 0 && (!v || !anchor))) return fail(GRIDLP_ERR_ARG, "op_anchor: bad argument");
+  gridlp_src_t src = rows_src(n);
+  return launch_op(&src, OpAnchor{v, anchor}, red, stream, "op_anchor");
+}
+
+int gridlp_op_dot(const double* a, const double* b, int64_t n, const gridlp_red_t* red, void* stream) {
+  if (n < 0 || (n > 0 && (!a || !b))) return fail(GRIDLP_ERR_ARG, "op_dot: bad argument");
+  gridlp_src_t src = rows_src(n);
+  return launch_op(&src, OpDot{a, b}, red, stream, "op_dot");
+}
+
+int gridlp_op_div(const double* in, double* out, int64_t n, double divisor, void* stream) {
+  if (n < 0 || (n > 0 && (!in || !out))) return fail(GRIDLP_ERR_ARG, "op_div: bad argument");
+  gridlp_src_t src = rows_src(n);
+  return launch_op(&src, OpDiv{in, out, divisor}, nullptr, stream, "op_div");
+}
+
+int gridlp_op_init_primal(const gridlp_primal_t* pv, void* stream) {
+  if (!pv) return fail(GRIDLP_ERR_ARG, "op_init_primal: null argument");
+  gridlp_src_t src = rows_src(pv->n);
+  return launch_op(&src, OpInitPrimal{pv->x, pv->x_anchor, pv->lo, pv->hi}, nullptr, stream,
+                   "op_init_primal");
+}
+
+int gridlp_op_step_advance(gridlp_step_t* d_step, int64_t delta, void* stream) {
+  if (!d_step) return fail(GRIDLP_ERR_ARG, "op_step_advance: null step");
+  step_advance_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(d_step, delta);
+  return check_launch("op_step_advance");
+}
+
+}  // extern "C"

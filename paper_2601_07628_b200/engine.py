@@ -1,0 +1,632 @@
+"""PDHG engine: restarted Halpern PDHG over an R x C grid of HBM-resident
+blocks, driving the sm_100a kernels of libgridlp_b200.so.
+
+Reference: iterate_epoch and its helpers (/root/reference/pkg/src/gridlp/
+pdhg_engine.py:223-476) and the step-size setup of solve()
+(solver_driver.py:211-234, sparse_kernels.py:61-93).
+
+Per main-loop iteration, per grid column j and row i:
+  primal:  [Aᵀy]_j -> x̂, x̄, Halpern x   (one fused kernel when R == 1)
+  dual:    [A x̄]_i -> ŷ, Halpern y        (one fused kernel when C == 1)
+When the reduced axis is longer than one, each block writes its partial
+product and the epilogue kernel consumes the axis sum (ascending-order sum of
+the resident partials on one GPU, or an NCCL allreduce across GPUs).
+A chunk of iterations up to the next KKT pass is captured once as a CUDA
+graph and replayed; the Halpern counter lives on the device and the graph
+advances it itself.
+
+Every restart / termination decision is taken on the host from scalars
+reduced in the reference's order (ascending device rank), exactly as
+pdhg_engine.py:405-462 does, with the same collective ledger.
+"""
+
+from __future__ import annotations
+
+import logging
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .blocks import DEFAULT_EXACT_ROW_MAX, DeviceCsr, permute_matrix, slice_blocks, transpose
+from .comm import Ledger, asc_sum
+from .ops import Fused, Parts
+
+log = logging.getLogger("gridlp.solver")
+
+OPTIMAL = "optimal"
+ITERATION_LIMIT = "iteration_limit"
+TIME_LIMIT = "time_limit"
+NUMERICAL_FAILURE = "numerical_failure"
+
+# per-coord scalar table fields of one KKT pass
+F_RP2, F_PEN, F_RD2, F_CX, F_RCX, F_DX2, F_DY2, F_CROSS, F_TIME = range(9)
+NFIELDS = 9
+
+
+@dataclass
+class EngineOptions:
+    """EngineConfig (pdhg_engine.py:138-154) plus device knobs."""
+
+    tolerance: float = 1e-4
+    max_iterations: int = 100_000
+    kkt_interval: int = 64
+    gamma: float = 0.0
+    halpern: bool = True
+    restarts: bool = True
+    beta_sufficient: float = 0.2
+    beta_necessary: float = 0.8
+    beta_artificial: float = 0.36
+    pid_kp: float = 0.6
+    pid_ki: float = 0.1
+    pid_kd: float = 0.1
+    omega_min: float = 1e-6
+    omega_max: float = 1e6
+    time_limit_seconds: float | None = None
+    exact_row_max: int = DEFAULT_EXACT_ROW_MAX
+    use_graphs: bool = True
+    graph_chunk: int = 128
+
+
+@dataclass
+class ColState:
+    j: int
+    n: int
+    c: torch.Tensor
+    lo: torch.Tensor
+    hi: torch.Tensor
+    x: torch.Tensor
+    xbar: torch.Tensor
+    x0: torch.Tensor
+    xpb: torch.Tensor
+    v: torch.Tensor
+    s: torch.Tensor
+
+
+@dataclass
+class RowState:
+    i: int
+    m: int
+    lo: torch.Tensor
+    hi: torch.Tensor
+    y: torch.Tensor
+    y0: torch.Tensor
+    ax: torch.Tensor
+    dy: torch.Tensor
+    u: torch.Tensor
+
+
+@dataclass
+class BlockState:
+    i: int
+    j: int
+    A: DeviceCsr
+    AT: DeviceCsr
+    bufs: dict = field(default_factory=dict)
+
+
+@dataclass
+class Report:
+    r_primal: float
+    r_dual: float
+    r_gap: float
+    obj_primal: float
+    obj_dual: float
+
+    @property
+    def overall(self) -> float:
+        return max(self.r_primal, self.r_dual, self.r_gap)
+
+
+def gap_residual(p: float, d: float) -> float:
+    """pdhg_engine.py:211-216."""
+    if not math.isfinite(d) or not math.isfinite(p):
+        return float("inf")
+    return abs(p - d) / (1.0 + max(abs(p), abs(d)))
+
+
+def restart_decision(base, r_current, r_prev, inner_k, total, bs, bn, ba) -> bool:
+    """pdhg_engine.py:262-282."""
+    if base is not None:
+        if r_current <= bs * base:
+            return True
+        if r_prev is not None and r_current <= bn * base and r_current > r_prev:
+            return True
+    return inner_k >= ba * total
+
+
+class Pid:
+    """pdhg_engine.py:97-103, :285-307."""
+
+    def __init__(self, kp, ki, kd):
+        self.kp, self.ki, self.kd = kp, ki, kd
+        self.integral = 0.0
+        self.last_error = 0.0
+
+    def update(self, d_x, d_y, omega, lo, hi) -> float:
+        if d_x <= 0.0 or d_y <= 0.0:
+            return omega
+        so = math.sqrt(omega)
+        err = math.log((so * d_x) / (d_y / so))
+        self.integral += err
+        lw = math.log(omega) - (self.kp * err + self.ki * self.integral + self.kd * (err - self.last_error))
+        self.last_error = err
+        return min(max(math.exp(lw), lo), hi)
+
+
+def _broken(rep: Report) -> bool:
+    """pdhg_engine.py:356-361."""
+    return (not math.isfinite(rep.r_primal)) or (not math.isfinite(rep.r_dual)) or math.isnan(rep.obj_primal)
+
+
+class PdhgEngine:
+    """Blocks, state and the main loop for the coords local to this process."""
+
+    def __init__(self, problem, layout, opts: EngineOptions, comm, ops_factory, device,
+                 objective_norm: float, bound_norm: float, objective_constant: float):
+        self.opts = opts
+        self.layout = layout
+        self.comm = comm
+        self.device = device
+        self.R, self.C = layout.topology.rows, layout.topology.cols
+        self.cnorm, self.bnorm, self.const = objective_norm, bound_norm, objective_constant
+        self.ledger = Ledger()
+        self.timings = {}
+        t0 = time.perf_counter()
+        self._build(problem)
+        self.timings["setup_blocks_s"] = time.perf_counter() - t0
+        cap = max([b.A.num_tiles for b in self.blocks.values()]
+                  + [b.AT.num_tiles for b in self.blocks.values()] + [1184])
+        self.nslots = self._assign_slots()
+        self.ops = ops_factory(device, cap, self.nslots)
+        self._plans()
+        self._graph = None
+        self._graph_launches = 0
+        self.iteration_events = None   # bench hook: list of (start, end, iterations)
+
+    # ------------------------------------------------------------ setup
+    def _build(self, problem):
+        lay, dev = self.layout, self.device
+        pa = permute_matrix(problem.matrix, lay)
+        host_blocks = slice_blocks(pa, lay)
+        self.per_device_nnz = [host_blocks[c].nnz for c in lay.topology.coords()]
+        cp, rp = lay.perm.col_perm, lay.perm.row_perm
+        f64 = dict(dtype=torch.float64, device=dev)
+        obj = np.asarray(problem.objective, np.float64)[cp]
+        vlo = np.asarray(problem.var_lower, np.float64)[cp]
+        vhi = np.asarray(problem.var_upper, np.float64)[cp]
+        clo = np.asarray(problem.con_lower, np.float64)[rp]
+        chi = np.asarray(problem.con_upper, np.float64)[rp]
+        local = self.comm.local
+        self.local_cols = sorted({j for _, j in local})
+        self.local_rows = sorted({i for i, _ in local})
+        self.cols, self.rows, self.blocks = {}, {}, {}
+        for j in self.local_cols:
+            c0, c1 = lay.col_range(j)
+            n = c1 - c0
+            t = lambda a: torch.as_tensor(np.ascontiguousarray(a[c0:c1]), **f64)  # noqa: E731
+            self.cols[j] = ColState(j, n, t(obj), t(vlo), t(vhi), torch.zeros(n, **f64),
+                                    torch.zeros(n, **f64), torch.zeros(n, **f64),
+                                    torch.zeros(n, **f64), torch.zeros(n, **f64),
+                                    torch.zeros(n, **f64))
+        for i in self.local_rows:
+            r0, r1 = lay.row_range(i)
+            m = r1 - r0
+            t = lambda a: torch.as_tensor(np.ascontiguousarray(a[r0:r1]), **f64)  # noqa: E731
+            self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
+                                    torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
+        for (i, j) in local:
+            hb = host_blocks[(i, j)]
+            self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, self.opts.exact_row_max),
+                                             DeviceCsr(transpose(hb), dev, self.opts.exact_row_max))
+        del host_blocks, pa
+        tensors = [t for b in self.blocks.values() for d in (b.A, b.AT)
+                   for t in (d.row_ptr, d.col_idx, d.values, d.tile_ptr)]
+        tensors += [t for c in self.cols.values() for t in (c.c, c.lo, c.hi)]
+        tensors += [t for r in self.rows.values() for t in (r.lo, r.hi)]
+        self.h2d_bytes = int(sum(t.numel() * t.element_size() for t in tensors))
+        self.passes = 0
+
+    def _assign_slots(self):
+        s = {}
+        k = 0
+        for i in self.local_rows:
+            for name in ("kkt_rows", "probe", "anchor_y", "u"):
+                s[(name, i)] = k
+                k += 1
+        for j in self.local_cols:
+            for name in ("kkt_cols", "anchor_x", "v", "s"):
+                s[(name, j)] = k
+                k += 1
+        for c in self.comm.local:
+            s[("cross", c)] = k
+            k += 1
+        self.slot = s
+        return k
+
+    def _buf(self, blk, name, length):
+        b = blk.bufs.get(name)
+        if b is None:
+            b = torch.zeros(length, dtype=torch.float64, device=self.device)
+            blk.bufs[name] = b
+        return b
+
+    def _axis_plan(self, axis, index, items, length, keep, scratch_name):
+        """items: [(block, orientation, gather)] of the local blocks on one grid
+        row (C) / column (R), ascending. Returns (pre, reduce_args, final)."""
+        single = (axis == "R" and self.R == 1) or (axis == "C" and self.C == 1)
+        if single:
+            (blk, orient, g), = items
+            return [], None, Fused(blk.A if orient == "A" else blk.AT, g)
+        pre = []
+        bufs = []
+        for blk, orient, g in items:
+            buf = self._buf(blk, f"{scratch_name}_{orient}", length)
+            pre.append((Fused(blk.A if orient == "A" else blk.AT, g), buf))
+            bufs.append(buf)
+        if self.comm.kind == "virtual":
+            return pre, None, Parts(bufs, length)
+        scratch = None
+        if keep:
+            scratch = self._buf(items[0][0], f"{scratch_name}_red", length)
+        target = scratch if keep else bufs[0]
+        return pre, (axis, index, bufs, scratch), Parts([target], length)
+
+    def _plans(self):
+        cols, rows, blocks = self.cols, self.rows, self.blocks
+        col_items = lambda j, vec: [(blocks[(i, j)], "T", vec(i)) for i in self.local_rows if (i, j) in blocks]  # noqa: E731
+        row_items = lambda i, vec: [(blocks[(i, j)], "A", vec(j)) for j in self.local_cols if (i, j) in blocks]  # noqa: E731
+        self.plan_primal = {j: self._axis_plan("R", j, col_items(j, lambda i: rows[i].y), cols[j].n, False, "pT")
+                            for j in self.local_cols}
+        self.plan_dual = {i: self._axis_plan("C", i, row_items(i, lambda j: cols[j].xbar), rows[i].m, False, "pA")
+                          for i in self.local_rows}
+        self.plan_kkt_ax = {i: self._axis_plan("C", i, row_items(i, lambda j: cols[j].x), rows[i].m, True, "pAx")
+                            for i in self.local_rows}
+        self.plan_kkt_aty = {j: self._axis_plan("R", j, col_items(j, lambda i: rows[i].y), cols[j].n, False, "pT")
+                             for j in self.local_cols}
+        self.plan_probe = {i: self._axis_plan("C", i, row_items(i, lambda j: cols[j].xpb), rows[i].m, True, "pPr")
+                           for i in self.local_rows}
+        self.plan_pow_u = {i: self._axis_plan("C", i, row_items(i, lambda j: cols[j].v), rows[i].m, False, "pA")
+                           for i in self.local_rows}
+        self.plan_pow_s = {j: self._axis_plan("R", j, col_items(j, lambda i: rows[i].u), cols[j].n, False, "pT")
+                           for j in self.local_cols}
+
+    def _run_plan(self, plan):
+        pre, red, final = plan
+        for src, buf in pre:
+            self.ops.store(src, buf)
+        if red is not None:
+            axis, index, bufs, scratch = red
+            self.comm.reduce(axis, index, bufs, scratch)
+        return final
+
+    # ------------------------------------------------------- scalar tables
+    def _table(self, local_vals: dict) -> dict:
+        return self.comm.table(local_vals)
+
+    def _axis_sum(self, table, field_, axis):
+        """R: over i down my grid column; C: over j along my grid row."""
+        i0, j0 = self.comm.local[0] if self.comm.local else (0, 0)
+        if axis == "R":
+            return asc_sum([table[(i, j0)][field_] for i in range(self.R)])
+        return asc_sum([table[(i0, j)][field_] for j in range(self.C)])
+
+    def _g_sum(self, table, field_, scale=1.0):
+        return asc_sum([table[(i, j)][field_] / scale for i in range(self.R) for j in range(self.C)])
+
+    # ---------------------------------------------------- power iteration
+    def power_estimate(self, iters: int, probe: np.ndarray) -> float:
+        """estimate_spectral_norm (sparse_kernels.py:61-93) on the grid."""
+        if iters < 1:
+            raise ValueError("iters must be >= 1")
+        ops, lay = self.ops, self.layout
+        R, C = float(self.R), float(self.C)
+        for j, col in self.cols.items():
+            c0, c1 = lay.col_range(j)
+            col.v.copy_(torch.as_tensor(np.ascontiguousarray(probe[c0:c1], dtype=np.float64)))
+        est = 0.0
+        for _ in range(iters):
+            for i, row in self.rows.items():
+                src = self._run_plan(self.plan_pow_u[i])
+                ops.store(src, row.u, self.slot[("u", i)])
+            for j, col in self.cols.items():
+                ops.dot(col.v, col.v, self.slot[("v", j)])
+            vals = ops.read_slots(self.nslots)
+            local = {}
+            for (i, j) in self.comm.local:
+                row = np.zeros(2)
+                row[0] = vals[self.slot[("u", i)], 0]
+                row[1] = vals[self.slot[("v", j)], 0]
+                local[(i, j)] = row
+            tab = self._table(local)
+            self.ledger.vec("C", "m")
+            self.ledger.scalar("G", 2)
+            u_sq = self._g_sum(tab, 0, C)
+            v_sq = self._g_sum(tab, 1, R)
+            if u_sq == 0.0 or v_sq == 0.0:
+                return 0.0
+            est = math.sqrt(u_sq / v_sq)
+            for j, col in self.cols.items():
+                src = self._run_plan(self.plan_pow_s[j])
+                ops.store(src, col.s, self.slot[("s", j)])
+            vals = ops.read_slots(self.nslots)
+            local = {(i, j): np.array([vals[self.slot[("s", j)], 0]]) for (i, j) in self.comm.local}
+            tab = self._table(local)
+            self.ledger.vec("R", "n")
+            self.ledger.scalar("G")
+            s_sq = self._g_sum(tab, 0, R)
+            if s_sq == 0.0:
+                return est
+            d = math.sqrt(s_sq)
+            for col in self.cols.values():
+                ops.div(col.s, col.v, d)
+        return est
+
+    # -------------------------------------------------------- main loop
+    def _launch_iterations(self, count: int):
+        ops, h = self.ops, self.opts.halpern
+        for t in range(count):
+            for j, col in self.cols.items():
+                ops.primal(self._run_plan(self.plan_primal[j]), col, t, h)
+            for i, row in self.rows.items():
+                ops.dual(self._run_plan(self.plan_dual[i]), row, t, h)
+        ops.step_advance(count)
+
+    def _graphable(self) -> bool:
+        return self.opts.use_graphs and self.comm.kind == "virtual" and self.device.type == "cuda"
+
+    def _run_iterations(self, count: int):
+        if count <= 0:
+            return
+        ev = self.iteration_events
+        if ev is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            self._run_iterations_inner(count)
+            e1.record()
+            ev.append((e0, e1, count))
+            return
+        self._run_iterations_inner(count)
+
+    def _run_iterations_inner(self, count: int):
+        g = max(1, min(self.opts.graph_chunk, self.opts.kkt_interval))
+        if not self._graphable() or count < g:
+            self._launch_iterations(count)
+            return
+        if self._graph is None:
+            # warm every kernel once outside capture (module loading), then capture
+            self._launch_iterations(g)
+            count -= g
+            stream = torch.cuda.Stream(self.device)
+            stream.wait_stream(torch.cuda.current_stream(self.device))
+            graph = torch.cuda.CUDAGraph()
+            before = getattr(self.ops, "launches", 0)
+            with torch.cuda.stream(stream):
+                with torch.cuda.graph(graph, stream=stream):
+                    self._launch_iterations(g)
+            torch.cuda.current_stream(self.device).wait_stream(stream)
+            self._graph_launches = getattr(self.ops, "launches", 0) - before
+            if hasattr(self.ops, "launches"):
+                self.ops.launches = before     # capture records, it does not launch
+            self._graph = graph
+        while count >= g:
+            self._graph.replay()
+            if hasattr(self.ops, "launches"):
+                self.ops.launches += self._graph_launches
+            count -= g
+        if count:
+            self._launch_iterations(count)
+
+    def _kkt(self, tau: float, restarts: bool):
+        """One evaluation pass (+ the speculative restart probe). Returns
+        (report, pieces) with host scalars reduced in the reference order."""
+        ops = self.ops
+        for i, row in self.rows.items():
+            src = self._run_plan(self.plan_kkt_ax[i])
+            fused = isinstance(src, Fused)
+            ops.kkt_rows(src, row, row.ax if fused else None, self.slot[("kkt_rows", i)])
+        for j, col in self.cols.items():
+            src = self._run_plan(self.plan_kkt_aty[j])
+            ops.kkt_cols(src, col, self.slot[("kkt_cols", j)])
+        if restarts:
+            for i, row in self.rows.items():
+                src = self._run_plan(self.plan_probe[i])
+                if isinstance(src, Fused):
+                    ops.probe(src, row, row.ax, None, self.slot[("probe", i)])
+                else:
+                    ops.probe(src, row, None, row.dy, self.slot[("probe", i)])
+                    for j in self.local_cols:
+                        blk = self.blocks.get((i, j))
+                        if blk is not None:
+                            ops.halfdiff_dot(blk.bufs["pAx_A"], blk.bufs["pPr_A"], row.dy,
+                                             self.slot[("cross", (i, j))])
+        vals = ops.read_slots(self.nslots)
+        local = {}
+        for (i, j) in self.comm.local:
+            r = np.zeros(NFIELDS)
+            kr = vals[self.slot[("kkt_rows", i)]]
+            kc = vals[self.slot[("kkt_cols", j)]]
+            r[F_RP2] = kr[0]
+            r[F_PEN] = float("inf") if kr[3] > 0 else kr[1] - kr[2]
+            r[F_RD2], r[F_CX], r[F_RCX], r[F_DX2] = kc[0], kc[1], kc[2], kc[3]
+            if restarts:
+                pr = vals[self.slot[("probe", i)]]
+                r[F_DY2] = pr[0]
+                r[F_CROSS] = pr[1] if self.C == 1 else vals[self.slot[("cross", (i, j))], 0]
+            r[F_TIME] = time.monotonic() - self._started if (i, j) == (0, 0) else 0.0
+            local[(i, j)] = r
+        tab = self._table(local)
+        rp_sq = self._axis_sum(tab, F_RP2, "R")
+        rd_sq = self._axis_sum(tab, F_RD2, "C")
+        obj_p = self._axis_sum(tab, F_CX, "C")
+        pen = self._axis_sum(tab, F_PEN, "R")
+        cdot = self._axis_sum(tab, F_RCX, "C")
+        obj_d = -pen + cdot
+        rep = Report(
+            r_primal=math.sqrt(rp_sq) / (1.0 + self.bnorm),
+            r_dual=math.sqrt(rd_sq) / (1.0 + self.cnorm),
+            r_gap=gap_residual(obj_p, obj_d),
+            obj_primal=obj_p + self.const,
+            obj_dual=obj_d + self.const,
+        )
+        # evaluate_kkt ledger: C vec + R scalar, R vec + C scalar x2 + R scalar + C scalar
+        self.ledger.vec("C", "m")
+        self.ledger.vec("R", "n")
+        self.ledger.scalar("R", 2)
+        self.ledger.scalar("C", 3)
+        return rep, tab
+
+    def _anchor_distances(self):
+        ops = self.ops
+        for j, col in self.cols.items():
+            ops.anchor(col.x, col.x0, self.slot[("anchor_x", j)])
+        for i, row in self.rows.items():
+            ops.anchor(row.y, row.y0, self.slot[("anchor_y", i)])
+        vals = ops.read_slots(self.nslots)
+        local = {(i, j): np.array([vals[self.slot[("anchor_x", j)], 0], vals[self.slot[("anchor_y", i)], 0]])
+                 for (i, j) in self.comm.local}
+        tab = self._table(local)
+        self.ledger.scalar("G", 2)
+        return self._g_sum(tab, 0, self.R), self._g_sum(tab, 1, self.C)
+
+    def _snapshot_xy(self):
+        xs = {j: c.x.detach().cpu().numpy().copy() for j, c in self.cols.items()}
+        ys = {i: r.y.detach().cpu().numpy().copy() for i, r in self.rows.items()}
+        return xs, ys
+
+    # The loop of iterate_epoch (pdhg_engine.py:364-476), split so a caller
+    # (bench.py) can time individual passes: start() -> step()* -> finish().
+    def start(self, eta: float, omega: float, trace=None, log_hook=None):
+        o = self.opts
+        for col in self.cols.values():
+            self.ops.init_primal(col)
+            col.xbar.zero_()
+        for row in self.rows.values():
+            row.y.zero_()
+            row.y0.zero_()
+        self._pid = Pid(o.pid_kp, o.pid_ki, o.pid_kd)
+        self._s = dict(eta=eta, omega=omega, base_fp=None, prev_fp=None, inner_k=0, epoch=0, total=0,
+                       status=None, report=None, report_at=-1, trace=trace, log_hook=log_hook,
+                       keep=getattr(trace, "keep", None) if trace is not None else None)
+        self._started = time.monotonic()
+        self._t_loop = time.perf_counter()
+
+    def step(self) -> bool:
+        """Iterations up to the next KKT pass, then the pass. True when the
+        loop terminated (status set)."""
+        o, ops, st = self.opts, self.ops, self._s
+        K = o.kkt_interval
+        if st["total"] >= o.max_iterations:
+            st["status"] = ITERATION_LIMIT
+            return True
+        eta, omega = st["eta"], st["omega"]
+        tau, sigma = eta / omega, eta * omega
+        total = st["total"]
+        target = min((total // K + 1) * K, o.max_iterations)
+        ops.set_step(tau, sigma, o.gamma, st["inner_k"])
+        self.count_iterations(target - total)
+        trace = st["trace"]
+        if trace is None:
+            self._run_iterations(target - total)
+            st["inner_k"] += target - total
+            total = target
+        else:
+            while total < target:
+                self._launch_iterations(1)
+                total += 1
+                st["inner_k"] += 1
+                if st["keep"] is None or total in st["keep"]:
+                    xs, ys = self._snapshot_xy()
+                    trace.append((total, np.concatenate([xs[j] for j in sorted(xs)]),
+                                  np.concatenate([ys[i] for i in sorted(ys)])))
+        st["total"] = total
+        if total % K != 0:
+            return False
+        report, tab = self._kkt(tau, o.restarts)
+        self.passes += 1
+        st["report"], st["report_at"] = report, total
+        if st["log_hook"] is not None:
+            st["log_hook"](total, report, omega, eta, st["epoch"])
+        if _broken(report):
+            st["status"] = NUMERICAL_FAILURE
+            return True
+        if report.overall <= o.tolerance:
+            st["status"] = OPTIMAL
+            return True
+        if o.restarts:
+            self.ledger.vec("C", "m")
+            self.ledger.scalar("G", 3)
+            dx_sq = self._g_sum(tab, F_DX2, self.R)
+            dy_sq = self._g_sum(tab, F_DY2, self.C)
+            cross = self._g_sum(tab, F_CROSS)
+            value = (omega / eta) * dx_sq + dy_sq / (eta * omega) + 2.0 * cross
+            fp = math.sqrt(max(value, 0.0))
+            if st["base_fp"] is None:
+                st["base_fp"] = fp
+            if restart_decision(st["base_fp"], fp, st["prev_fp"], st["inner_k"], total,
+                                o.beta_sufficient, o.beta_necessary, o.beta_artificial):
+                d_x_sq, d_y_sq = self._anchor_distances()
+                st["omega"] = self._pid.update(math.sqrt(d_x_sq), math.sqrt(d_y_sq), omega,
+                                               o.omega_min, o.omega_max)
+                st["inner_k"] = 0
+                st["epoch"] += 1
+                st["base_fp"] = fp
+                st["prev_fp"] = None
+            else:
+                st["prev_fp"] = fp
+        if o.time_limit_seconds is not None:
+            self.ledger.scalar("G")
+            if self._g_sum(tab, F_TIME) >= o.time_limit_seconds:
+                st["status"] = TIME_LIMIT
+                return True
+        return False
+
+    def finish(self):
+        o, ops, st = self.opts, self.ops, self._s
+        eta, omega = st["eta"], st["omega"]
+        report, status = st["report"], st["status"]
+        if st["report_at"] != st["total"]:
+            ops.set_step(eta / omega, eta * omega, o.gamma, st["inner_k"])
+            report, _ = self._kkt(eta / omega, False)
+            if status != NUMERICAL_FAILURE and _broken(report):
+                status = NUMERICAL_FAILURE
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
+        self.timings["main_loop_s"] = time.perf_counter() - self._t_loop
+        return {"status": status, "report": report, "iterations": st["total"],
+                "restarts": st["epoch"], "omega": omega, "eta": eta}
+
+    def run(self, eta: float, omega: float, trace=None, log_hook=None):
+        """iterate_epoch (pdhg_engine.py:364-476). Returns a dict outcome."""
+        self.start(eta, omega, trace, log_hook)
+        while not self.step():
+            pass
+        return self.finish()
+
+    def count_iterations(self, n: int):
+        self.ledger.vec("R", "n", n)
+        self.ledger.vec("C", "m", n)
+
+    def solution_blocks(self):
+        """x blocks of grid columns (from devices (0, j)) and y blocks of grid
+        rows (from (i, 0)) as host arrays (solver_driver.py:246-248)."""
+        if self.comm.kind == "virtual":
+            xs = [self.cols[j].x.cpu().numpy() for j in range(self.C)]
+            ys = [self.rows[i].y.cpu().numpy() for i in range(self.R)]
+            return xs, ys
+        lay = self.layout
+        lengths = {(i, j): max(int(lay.col_cuts[j + 1] - lay.col_cuts[j]), int(lay.row_cuts[i + 1] - lay.row_cuts[i]))
+                   for i in range(self.R) for j in range(self.C)}
+        xl = {c: self.cols[c[1]].x for c in self.comm.local}
+        yl = {c: self.rows[c[0]].y for c in self.comm.local}
+        xlen = {(i, j): int(lay.col_cuts[j + 1] - lay.col_cuts[j]) for i in range(self.R) for j in range(self.C)}
+        ylen = {(i, j): int(lay.row_cuts[i + 1] - lay.row_cuts[i]) for i in range(self.R) for j in range(self.C)}
+        del lengths
+        xa = self.comm.gather_vectors(xl, xlen, self.device)
+        ya = self.comm.gather_vectors(yl, ylen, self.device)
+        xs = [xa[(0, j)].cpu().numpy() for j in range(self.C)]
+        ys = [ya[(i, 0)].cpu().numpy() for i in range(self.R)]
+        return xs, ys

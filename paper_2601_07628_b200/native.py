@@ -1,0 +1,159 @@
+"""ctypes binding of libgridlp_b200.so (include/gridlp_b200.h) and its build.
+
+The library is the only compute path: if it is missing or no CUDA device is
+present, `load()` raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_uint32, c_void_p
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+LIB_DIR = PKG / "_lib"
+LIB_PATH = LIB_DIR / "libgridlp_b200.so"
+SOURCES = [PKG / "csrc" / "gridlp_b200.cu"]
+HEADER = ROOT / "include" / "gridlp_b200.h"
+
+MAX_RED = 8
+MAX_PARTS = 16
+TILE_NNZ_CAP = 4096
+TILE_ROWS = 256
+F_HALPERN = 1
+F_SUMSQ = 2
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-std=c++17", "-lineinfo",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+class Csr(ctypes.Structure):
+    _fields_ = [("num_rows", c_int64), ("num_cols", c_int64), ("nnz", c_int64),
+                ("row_ptr", c_void_p), ("col_idx", c_void_p), ("values", c_void_p),
+                ("tile_ptr", c_void_p), ("num_tiles", c_int64),
+                ("exact_row_max", c_int32), ("reserved", c_int32)]
+
+
+class Src(ctypes.Structure):
+    _fields_ = [("A", POINTER(Csr)), ("gather", c_void_p),
+                ("parts", c_void_p * MAX_PARTS), ("nparts", c_int32),
+                ("reserved", c_int32), ("num_rows", c_int64)]
+
+
+class Step(ctypes.Structure):
+    _fields_ = [("tau", c_double), ("sigma", c_double), ("gamma", c_double),
+                ("inner_k", c_int64)]
+
+
+class Primal(ctypes.Structure):
+    _fields_ = [("x", c_void_p), ("x_bar", c_void_p), ("x_anchor", c_void_p),
+                ("c", c_void_p), ("lo", c_void_p), ("hi", c_void_p), ("n", c_int64)]
+
+
+class Dual(ctypes.Structure):
+    _fields_ = [("y", c_void_p), ("y_anchor", c_void_p), ("lo", c_void_p),
+                ("hi", c_void_p), ("m", c_int64)]
+
+
+class Red(ctypes.Structure):
+    _fields_ = [("partials", c_void_p), ("capacity", c_int64), ("out", c_void_p)]
+
+
+_P = c_void_p
+SIGNATURES = {
+    "gridlp_abi_version": ([], c_int),
+    "gridlp_last_error": ([], ctypes.c_char_p),
+    "gridlp_device_info": ([c_int, POINTER(c_int32), POINTER(c_int64)], c_int),
+    "gridlp_op_slots": ([POINTER(Src)], c_int64),
+    "gridlp_op_store": ([POINTER(Src), _P, c_uint32, POINTER(Red), _P], c_int),
+    "gridlp_op_primal": ([POINTER(Src), POINTER(Primal), _P, c_int32, c_uint32, _P], c_int),
+    "gridlp_op_dual": ([POINTER(Src), POINTER(Dual), _P, c_int32, c_uint32, _P], c_int),
+    "gridlp_op_kkt_rows": ([POINTER(Src), POINTER(Dual), _P, POINTER(Red), _P], c_int),
+    "gridlp_op_kkt_cols": ([POINTER(Src), POINTER(Primal), _P, _P, POINTER(Red), _P], c_int),
+    "gridlp_op_probe": ([POINTER(Src), POINTER(Dual), _P, _P, _P, POINTER(Red), _P], c_int),
+    "gridlp_op_halfdiff_dot": ([_P, _P, _P, c_int64, POINTER(Red), _P], c_int),
+    "gridlp_op_anchor": ([_P, _P, c_int64, POINTER(Red), _P], c_int),
+    "gridlp_op_dot": ([_P, _P, c_int64, POINTER(Red), _P], c_int),
+    "gridlp_op_div": ([_P, _P, c_int64, c_double, _P], c_int),
+    "gridlp_op_init_primal": ([POINTER(Primal), _P], c_int),
+    "gridlp_op_step_advance": ([_P, c_int64, _P], c_int),
+}
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    """nvcc the library for sm_100a into the package (in-tree, so it ships
+    with the repo snapshot to the GPU box)."""
+    LIB_DIR.mkdir(exist_ok=True)
+    newest = max(p.stat().st_mtime for p in SOURCES + [HEADER])
+    if not force and LIB_PATH.exists() and LIB_PATH.stat().st_mtime >= newest:
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-Xptxas", "-v" if verbose else "-O3",
+           "-I", str(ROOT / "include"), "-o", str(LIB_PATH), *map(str, SOURCES)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
+    if verbose:
+        print(res.stderr)
+    return LIB_PATH
+
+
+class GridlpError(RuntimeError):
+    pass
+
+
+class Library:
+    """Loaded libgridlp_b200.so with typed entry points; every call checks
+    the returned status and raises GridlpError with gridlp_last_error()."""
+
+    def __init__(self, path: Path = LIB_PATH):
+        if not path.exists():
+            raise GridlpError(
+                f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(no CPU fallback exists)")
+        self.path = path
+        self._lib = ctypes.CDLL(str(path))
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(self._lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        ver = self._lib.gridlp_abi_version()
+        if ver != 1:
+            raise GridlpError(f"ABI version {ver} != 1")
+
+    def symbols(self):
+        return list(SIGNATURES)
+
+    def last_error(self) -> str:
+        return self._lib.gridlp_last_error().decode()
+
+    def call(self, name, *args):
+        rc = getattr(self._lib, name)(*args)
+        if rc != 0:
+            raise GridlpError(f"{name} failed ({rc}): {self.last_error()}")
+        return rc
+
+    def slots(self, src: Src) -> int:
+        return int(self._lib.gridlp_op_slots(ctypes.byref(src)))
+
+    def device_info(self, device: int = 0):
+        sm = c_int32(0)
+        l2 = c_int64(0)
+        self.call("gridlp_device_info", device, ctypes.byref(sm), ctypes.byref(l2))
+        return sm.value, l2.value
+
+
+_LIB: Library | None = None
+
+
+def load() -> Library:
+    global _LIB
+    if _LIB is None:
+        _LIB = Library()
+    return _LIB

@@ -1,0 +1,163 @@
+"""Device operations of the engine, bound to libgridlp_b200.so.
+
+`CudaOps` is the only implementation in the package: each method is one
+C-ABI call (include/gridlp_b200.h) on the current CUDA stream. ctypes
+argument structs are built once per engine object and cached, so a
+captured chunk of iterations is a plain sequence of kernel launches.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import native
+from .blocks import DeviceCsr, parts_src
+
+
+class Fused:
+    """Sums come from a product of one local block with a gather vector."""
+
+    def __init__(self, mat: DeviceCsr, gather: torch.Tensor):
+        self.mat = mat
+        self.gather = gather
+        self.num_rows = mat.num_rows
+
+
+class Parts:
+    """Sums come from an ascending-order sum of partial vectors."""
+
+    def __init__(self, parts, num_rows: int):
+        self.parts = list(parts)
+        self.num_rows = int(num_rows)
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None and t.numel() else None
+
+
+class CudaOps:
+    kind = "cuda"
+
+    def __init__(self, device: torch.device, capacity: int, num_slots: int):
+        self.lib = native.load()
+        self.device = device
+        self.capacity = max(int(capacity), 1)
+        self.partials = torch.zeros(self.capacity * native.MAX_RED, dtype=torch.float64, device=device)
+        self.slots = torch.zeros((max(num_slots, 1), native.MAX_RED), dtype=torch.float64, device=device)
+        self.slots_host = torch.zeros_like(self.slots, device="cpu").pin_memory()
+        self.step = torch.zeros(4, dtype=torch.float64, device=device)
+        self.step_host = torch.zeros(4, dtype=torch.float64).pin_memory()
+        self._red = {}
+        self._srcs = {}
+        self.launches = 0          # kernels launched through this object
+
+    # -- plumbing ------------------------------------------------------------
+    def stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def red(self, slot: int):
+        r = self._red.get(slot)
+        if r is None:
+            r = native.Red(self.partials.data_ptr(), self.capacity, self.slots[slot].data_ptr())
+            self._red[slot] = r
+        return ctypes.byref(r)
+
+    def src(self, s):
+        key = id(s)
+        hit = self._srcs.get(key)
+        if hit is not None and hit[0] is s:
+            return ctypes.byref(hit[1])
+        if isinstance(s, Fused):
+            c = s.mat.src(s.gather)
+        else:
+            c = parts_src(s.parts, s.num_rows)
+        self._srcs[key] = (s, c)
+        return ctypes.byref(c)
+
+    @staticmethod
+    def primal_struct(col):
+        c = getattr(col, "_cprimal", None)
+        if c is None:
+            c = native.Primal(_ptr(col.x), _ptr(col.xbar), _ptr(col.x0), _ptr(col.c),
+                              _ptr(col.lo), _ptr(col.hi), col.n)
+            col._cprimal = c
+        return ctypes.byref(c)
+
+    @staticmethod
+    def dual_struct(row):
+        c = getattr(row, "_cdual", None)
+        if c is None:
+            c = native.Dual(_ptr(row.y), _ptr(row.y0), _ptr(row.lo), _ptr(row.hi), row.m)
+            row._cdual = c
+        return ctypes.byref(c)
+
+    def set_step(self, tau: float, sigma: float, gamma: float, inner_k: int):
+        h = self.step_host
+        h[0], h[1], h[2] = tau, sigma, gamma
+        h.view(torch.int64)[3] = int(inner_k)
+        self.step.copy_(h, non_blocking=True)
+
+    def read_slots(self, n: int) -> np.ndarray:
+        self.slots_host[:n].copy_(self.slots[:n], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return self.slots_host[:n].numpy().copy()
+
+    # -- ops -----------------------------------------------------------------
+    def store(self, src, out, slot=None):
+        self.launches += 2 if slot is not None else 1
+        flags = native.F_SUMSQ if slot is not None else 0
+        self.lib.call("gridlp_op_store", self.src(src), _ptr(out), flags,
+                      self.red(slot) if slot is not None else None, self.stream())
+
+    def primal(self, src, col, it: int, halpern: bool):
+        self.launches += 1
+        self.lib.call("gridlp_op_primal", self.src(src), self.primal_struct(col),
+                      self.step.data_ptr(), it, native.F_HALPERN if halpern else 0, self.stream())
+
+    def dual(self, src, row, it: int, halpern: bool):
+        self.launches += 1
+        self.lib.call("gridlp_op_dual", self.src(src), self.dual_struct(row),
+                      self.step.data_ptr(), it, native.F_HALPERN if halpern else 0, self.stream())
+
+    def kkt_rows(self, src, row, ax, slot):
+        self.launches += 2
+        self.lib.call("gridlp_op_kkt_rows", self.src(src), self.dual_struct(row), _ptr(ax),
+                      self.red(slot), self.stream())
+
+    def kkt_cols(self, src, col, slot):
+        self.launches += 2
+        self.lib.call("gridlp_op_kkt_cols", self.src(src), self.primal_struct(col), _ptr(col.xpb),
+                      self.step.data_ptr(), self.red(slot), self.stream())
+
+    def probe(self, src, row, ax, dy_out, slot):
+        self.launches += 2
+        self.lib.call("gridlp_op_probe", self.src(src), self.dual_struct(row), _ptr(ax), _ptr(dy_out),
+                      self.step.data_ptr(), self.red(slot), self.stream())
+
+    def halfdiff_dot(self, a, b, d, slot):
+        self.launches += 2
+        self.lib.call("gridlp_op_halfdiff_dot", _ptr(a), _ptr(b), _ptr(d), a.numel(),
+                      self.red(slot), self.stream())
+
+    def anchor(self, v, anchor, slot):
+        self.launches += 2
+        self.lib.call("gridlp_op_anchor", _ptr(v), _ptr(anchor), v.numel(), self.red(slot), self.stream())
+
+    def dot(self, a, b, slot):
+        self.launches += 2
+        self.lib.call("gridlp_op_dot", _ptr(a), _ptr(b), a.numel(), self.red(slot), self.stream())
+
+    def div(self, inp, out, divisor: float):
+        self.launches += 1
+        self.lib.call("gridlp_op_div", _ptr(inp), _ptr(out), inp.numel(), float(divisor), self.stream())
+
+    def init_primal(self, col):
+        self.launches += 1
+        self.lib.call("gridlp_op_init_primal", self.primal_struct(col), self.stream())
+
+    def step_advance(self, delta: int):
+        self.launches += 1
+        self.lib.call("gridlp_op_step_advance", self.step.data_ptr(), int(delta), self.stream())

@@ -1,0 +1,241 @@
+"""Parity of the sm_100a path (through the C ABI) with the reference.
+
+Bars (stated per test):
+  * sparse products with rows <= exact_row_max: BIT-IDENTICAL to scipy's
+    csr_matvec (the reference kernel); longer rows: <= 1e-12 relative;
+  * every epilogue op: BIT-IDENTICAL to the reference's numpy expression,
+    including NaN / inf / signed-zero cases;
+  * fixed-step (eta given) restart-free trajectories: BIT-IDENTICAL iterates
+    at every checkpoint (the device reproduces every rounding);
+  * full solves: identical status / iterations / restarts; objective and KKT
+    residuals within 1e-6 relative (north-star bar) and iterates within
+    1e-9 relative in max-norm. Only the norm/dot reductions use a different
+    (deterministic, tree) summation order than numpy's ddot.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_problem, load_json, load_npz
+from host_ops import HostOps
+
+pytestmark = pytest.mark.gpu
+
+cuda = pytest.importorskip("torch").cuda
+if not cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2601_07628_b200 import SolverConfig, native, solve, reference_solve  # noqa: E402
+from paper_2601_07628_b200.blocks import DeviceCsr, HostCsr  # noqa: E402
+from paper_2601_07628_b200.engine import ColState, RowState  # noqa: E402
+from paper_2601_07628_b200.ops import CudaOps, Fused, Parts  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def ops():
+    return CudaOps(DEV, 1 << 16, 16)
+
+
+def host_csr(m, n, ptr, col, val):
+    return HostCsr(int(m), int(n), np.asarray(ptr, np.int64), np.asarray(col, np.int64),
+                   np.asarray(val, np.float64))
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=DEV)
+
+
+def test_library_is_loaded_from_tree():
+    lib = native.load()
+    assert lib.path == native.LIB_PATH
+    sm, l2 = lib.device_info(0)
+    assert sm >= 100 and l2 > 0
+
+
+class TestProducts:
+    def test_golden_spmv_bitwise(self, ops):
+        z = load_npz("spmv.npz")
+        for t in range(int(z["ncases"])):
+            for tag, vec, want in (("", "x", "ax"), ("t", "y", "aty")):
+                h = host_csr(z[f"c{t}_m"] if tag == "" else z[f"c{t}_n"],
+                             z[f"c{t}_n"] if tag == "" else z[f"c{t}_m"],
+                             z[f"c{t}_{tag}ptr"], z[f"c{t}_{tag}col"], z[f"c{t}_{tag}val"])
+                A = DeviceCsr(h, DEV)
+                out = torch.full((h.num_rows,), np.nan, dtype=torch.float64, device=DEV)
+                ops.store(Fused(A, dev(z[f"c{t}_{vec}"])), out)
+                np.testing.assert_array_equal(out.cpu().numpy(), z[f"c{t}_{want}"])
+
+    @pytest.mark.parametrize("seed", range(4))
+    def test_random_bitwise_and_heavy_rows(self, ops, seed):
+        import scipy.sparse as sp
+
+        rng = np.random.default_rng(seed)
+        m, n = 3000, 5000
+        lens = rng.integers(0, 60, m)
+        lens[rng.integers(0, m, 5)] = rng.integers(600, 5000, 5)   # heavy rows
+        lens[100:300] = 0
+        ptr = np.concatenate([[0], np.cumsum(lens)])
+        col = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int64)
+        val = rng.standard_normal(len(col)) * 10.0 ** rng.integers(-6, 6, len(col))
+        x = rng.standard_normal(n)
+        h = host_csr(m, n, ptr, col, val)
+        want = sp.csr_matrix((val, col, ptr), shape=(m, n)).dot(x)
+        A = DeviceCsr(h, DEV)
+        assert A.heavy_rows == 5
+        out = torch.empty(m, dtype=torch.float64, device=DEV)
+        ops.store(Fused(A, dev(x)), out)
+        got = out.cpu().numpy()
+        light = lens <= 512
+        np.testing.assert_array_equal(got[light], want[light])
+        scale = np.abs(val[None, :]).max() * np.abs(x).max()
+        assert np.max(np.abs(got[~light] - want[~light])) <= 1e-12 * scale * lens.max()
+        out2 = torch.empty_like(out)
+        ops.store(Fused(A, dev(x)), out2)
+        assert torch.equal(out, out2)          # deterministic
+
+    def test_parts_sum_ascending(self, ops):
+        rng = np.random.default_rng(3)
+        parts = [rng.standard_normal(777) * 10.0 ** rng.integers(-8, 8, 777) for _ in range(5)]
+        out = torch.empty(777, dtype=torch.float64, device=DEV)
+        ops.store(Parts([dev(p) for p in parts], 777), out)
+        want = parts[0].copy()
+        for p in parts[1:]:
+            want += p
+        np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+def _edge_vectors(rng, n):
+    v = rng.standard_normal(n) * 10.0 ** rng.integers(-3, 3, n)
+    special = [0.0, -0.0, np.inf, -np.inf, 1e-300, -1e308, 5.0]
+    v[: len(special)] = special
+    return v
+
+
+class TestEpilogueOps:
+    """Each op against the CPU double (numpy, reference order), bitwise."""
+
+    def _states(self, rng, n, m, host):
+        def mk(a):
+            return torch.as_tensor(a.copy()) if host else dev(a)
+        lo = rng.uniform(-2, 0, n)
+        hi = lo + rng.uniform(0, 3, n)
+        lo[:3], hi[3:6] = -np.inf, np.inf
+        lo[6], hi[6] = 1.0, 1.0
+        x = _edge_vectors(rng, n)
+        x[10] = np.nan
+        col = ColState(0, n, mk(rng.standard_normal(n)), mk(lo), mk(hi), mk(x), mk(np.zeros(n)),
+                       mk(rng.standard_normal(n)), mk(np.zeros(n)), mk(np.zeros(n)), mk(np.zeros(n)))
+        clo = rng.uniform(-2, 0, m)
+        chi = clo + rng.uniform(0, 1, m)
+        clo[:4], chi[2:7] = -np.inf, np.inf
+        y = _edge_vectors(rng, m)
+        y[9] = np.nan
+        row = RowState(0, m, mk(clo), mk(chi), mk(y), mk(rng.standard_normal(m)), mk(np.zeros(m)),
+                       mk(np.zeros(m)), mk(np.zeros(m)))
+        return col, row
+
+    @pytest.mark.parametrize("gamma,halpern", [(0.0, True), (0.5, True), (0.0, False)])
+    def test_primal_dual_kkt_probe(self, ops, gamma, halpern):
+        rng = np.random.default_rng(11)
+        n, m = 2000, 1500
+        sums_n = _edge_vectors(rng, n)
+        sums_m = _edge_vectors(rng, m)
+        hops = HostOps(None, 0, 16)
+        results = []
+        for host in (False, True):
+            r2 = np.random.default_rng(5)
+            col, row = self._states(r2, n, m, host)
+            o = hops if host else ops
+            mk = (lambda a: torch.as_tensor(a.copy())) if host else dev
+            sn, sm_ = Parts([mk(sums_n)], n), Parts([mk(sums_m)], m)
+            o.set_step(0.37, 1.9, gamma, 41)
+            o.primal(sn, col, 3, halpern)
+            o.dual(sm_, row, 3, halpern)
+            ax = mk(np.zeros(m))
+            o.kkt_rows(sm_, row, ax, 0)
+            o.kkt_cols(sn, col, 1)
+            dy = mk(np.zeros(m))
+            o.probe(sm_, row, mk(sums_m[::-1].copy()), dy, 2)
+            o.anchor(col.x, col.x0, 3)
+            res = [t.cpu().numpy().copy() for t in (col.x, col.xbar, col.xpb, col.x0, row.y, ax, dy)]
+            results.append((res, o.read_slots(4)))
+        (gpu, gs), (cpu, cs) = results
+        for a, b in zip(gpu, cpu):
+            np.testing.assert_array_equal(a, b)
+            np.testing.assert_array_equal(np.signbit(a), np.signbit(b))
+        # reductions: same value up to summation order (NaN where numpy has NaN)
+        for q, (a, b) in enumerate(zip(gs.ravel(), cs.ravel())):
+            if math.isnan(b):
+                assert math.isnan(a), q
+            elif math.isinf(b):
+                assert a == b, q
+            else:
+                assert abs(a - b) <= 1e-12 * max(1.0, abs(b)), (q, a, b)
+
+
+class TestSolves:
+    def test_fixed_eta_trajectory_bitwise(self, golden_cfg1):
+        z = golden_cfg1
+
+        class Keep(list):
+            keep = set(int(t) for t in z["fx_trace_iters"])
+
+        tr = Keep()
+        r = reference_solve(golden_problem(z), SolverConfig(tolerance=1e-300, seed=0, eta=0.05,
+                                                           restarts=False, max_iterations=512), trace=tr)
+        assert [t for t, _, _ in tr] == [int(t) for t in z["fx_trace_iters"]]
+        for k, (_, x, y) in enumerate(tr):
+            np.testing.assert_array_equal(x, z["fx_trace_x"][k])
+            np.testing.assert_array_equal(y, z["fx_trace_y"][k])
+        np.testing.assert_array_equal(r.x, z["fx_x"])
+        for a, b in zip([r.report.r_primal, r.report.r_dual, r.report.r_gap, r.report.obj_primal,
+                         r.report.obj_dual], z["fx_kkt"]):
+            assert abs(a - b) <= 1e-12 * max(1.0, abs(b))
+
+    def test_graph_replay_equals_eager(self, golden_cfg1):
+        from paper_2601_07628_b200.api import _solve
+
+        p = golden_problem(golden_cfg1)
+        cfg = SolverConfig(tolerance=1e-300, seed=0, eta=0.05, restarts=False, max_iterations=640)
+        a = _solve(p, cfg, engine_overrides={"use_graphs": True})
+        b = _solve(p, cfg, engine_overrides={"use_graphs": False})
+        np.testing.assert_array_equal(a.x, b.x)
+        np.testing.assert_array_equal(a.y, b.y)
+
+    def test_cfg1_to_tolerance(self, golden_cfg1):
+        z = golden_cfg1
+        r = solve(golden_problem(z), SolverConfig(tolerance=1e-4, seed=0))
+        assert (r.status, r.iterations, r.restarts) == ("optimal", int(z["iterations"]), int(z["restarts"]))
+        ref = float(z["result_objective"])
+        assert abs(r.objective - ref) <= 1e-6 * abs(ref)
+        for a, b in zip([r.report.r_primal, r.report.r_dual, r.report.r_gap], z["kkt"][:3]):
+            assert abs(a - b) <= 1e-6 * max(abs(b), 1e-12)
+        for got, want in ((r.x, z["x"]), (r.y, z["y"])):
+            assert np.max(np.abs(got - want)) <= 1e-9 * max(1.0, np.max(np.abs(want)))
+        again = solve(golden_problem(z), SolverConfig(tolerance=1e-4, seed=0))
+        np.testing.assert_array_equal(r.x, again.x)   # run-to-run deterministic
+
+    @pytest.mark.parametrize("chunk", range(4))
+    def test_golden_cases(self, golden_solves, chunk):
+        z, meta = golden_solves
+        for m in [m for m in meta if "result" in m][chunk::4]:
+            cfg = dict(m["cfg"])
+            if cfg.get("grid") is not None:
+                cfg["grid"] = tuple(cfg["grid"])
+            r = solve(golden_problem(z, m["problem"] + "_"), SolverConfig(**cfg))
+            exp = m["result"]
+            assert r.status == exp["status"], m["id"]
+            assert r.iterations == exp["iterations"], m["id"]
+            assert r.restarts == exp["restarts"], m["id"]
+            assert r.counters == exp["counters"], m["id"]
+            assert r.layout == exp["layout"], m["id"]
+            if r.status in ("optimal", "iteration_limit"):
+                want = exp["objective"]
+                assert abs(r.objective - want) <= 1e-6 * max(1.0, abs(want)), m["id"]
+                xr = z[f"S{m['id']}_x"]
+                assert np.max(np.abs(r.x - xr), initial=0.0) <= 1e-6 * max(1.0, np.max(np.abs(xr), initial=0.0))
