@@ -61,19 +61,28 @@ enum gridlp_status {
  * matrix_transpose (partition.py:93-122): int32 column indices (12 B/nnz
  * instead of the reference's 16) and a tile directory. Tiles are row
  * ranges [tile_ptr[t], tile_ptr[t+1]) that either hold at most
- * GRIDLP_TILE_ROWS rows and GRIDLP_TILE_NNZ_CAP nonzeros ("light"), or a
- * single row longer than exact_row_max ("heavy", tree-summed).
+ * GRIDLP_TILE_ROWS rows and tile_nnz_cap nonzeros ("light"), or a single
+ * row longer than exact_row_max ("heavy", tree-summed). light_tiles /
+ * heavy_tiles list the tile ids of each kind.
+ * col_idx and values must stay readable 4 elements past nnz (the staging
+ * copies move whole 16-byte granules).
  */
 typedef struct gridlp_csr {
   int64_t num_rows;
   int64_t num_cols;
   int64_t nnz;
-  const int32_t* row_ptr;   /* [num_rows+1], nnz < 2^31 */
-  const int32_t* col_idx;   /* [nnz] strictly increasing within a row */
-  const double* values;     /* [nnz] */
-  const int32_t* tile_ptr;  /* [num_tiles+1] */
+  const int32_t* row_ptr;     /* [num_rows+1], nnz < 2^31 */
+  const int32_t* col_idx;     /* [nnz(+4)] strictly increasing within a row */
+  const double* values;       /* [nnz(+4)] */
+  const int32_t* tile_ptr;    /* [num_tiles+1] */
   int64_t num_tiles;
-  int32_t exact_row_max;    /* <= GRIDLP_TILE_NNZ_CAP/2 */
+  const int32_t* light_tiles; /* [num_light] */
+  int64_t num_light;
+  const int32_t* heavy_tiles; /* [num_heavy] */
+  int64_t num_heavy;
+  int32_t exact_row_max;      /* <= tile_nnz_cap/2 */
+  int32_t tile_nnz_cap;       /* <= GRIDLP_TILE_NNZ_CAP */
+  int32_t variant;            /* 0: persistent TMA-pipelined (default); 1: one CTA per tile */
   int32_t reserved;
 } gridlp_csr_t;
 
@@ -142,7 +151,7 @@ int gridlp_abi_version(void);
 const char* gridlp_last_error(void);
 /* SM count and L2 size of `device` (host ints). */
 int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes);
-/* Number of CTAs (reduction slots) an op over `src` launches. */
+/* Upper bound on the CTAs (reduction slots) an op over `src` launches. */
 int64_t gridlp_op_slots(const gridlp_src_t* src);
 
 /* --- products ------------------------------------------------------------ */

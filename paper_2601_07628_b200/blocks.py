@@ -121,24 +121,50 @@ def build_tiles(ptr: np.ndarray, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
 
 
 class DeviceCsr:
-    """One tiled CSR block resident in HBM; `.struct` is the gridlp_csr_t."""
+    """One tiled CSR block resident in HBM; `.struct` is the gridlp_csr_t.
 
-    def __init__(self, host: HostCsr, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX):
-        if host.nnz >= 2 ** 31:
+    `variant` 0 selects the persistent TMA-pipelined product kernel, 1 the
+    one-CTA-per-tile kernel (kept for A/B measurement)."""
+
+    PAD = 4   # the TMA staging copies read whole 16-byte granules
+
+    def __init__(self, host: HostCsr, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
+                 tile_cap: int = native.DEFAULT_TILE_CAP, variant: int = 0):
+        if host.nnz >= 2 ** 31 - 16:
             raise ValueError("block nnz must be < 2^31 (int32 row pointers)")
         self.num_rows, self.num_cols, self.nnz = host.num_rows, host.num_cols, host.nnz
-        tiles = build_tiles(host.ptr, exact_row_max)
+        tiles = build_tiles(host.ptr, exact_row_max, cap=tile_cap)
         self.num_tiles = max(len(tiles) - 1, 0)
+        lens = np.diff(host.ptr)
+        t_rows = np.diff(tiles.astype(np.int64))
+        first = tiles[:-1].astype(np.int64)
+        heavy = (t_rows == 1) & (lens[first] > exact_row_max) if self.num_tiles else np.zeros(0, bool)
+        light_ids = np.flatnonzero(~heavy).astype(np.int32)
+        heavy_ids = np.flatnonzero(heavy).astype(np.int32)
+        col = np.zeros(host.nnz + self.PAD, dtype=np.int32)
+        col[: host.nnz] = host.col
+        val = np.zeros(host.nnz + self.PAD, dtype=np.float64)
+        val[: host.nnz] = host.val
         self.row_ptr = torch.from_numpy(host.ptr.astype(np.int32)).to(device)
-        self.col_idx = torch.from_numpy(host.col.astype(np.int32)).to(device)
-        self.values = torch.from_numpy(np.ascontiguousarray(host.val)).to(device)
+        self.col_idx = torch.from_numpy(col).to(device)
+        self.values = torch.from_numpy(val).to(device)
         self.tile_ptr = torch.from_numpy(tiles).to(device)
+        self.light_tiles = torch.from_numpy(light_ids).to(device)
+        self.heavy_tiles = torch.from_numpy(heavy_ids).to(device)
         self.exact_row_max = exact_row_max
-        self.heavy_rows = int(np.count_nonzero(np.diff(host.ptr) > exact_row_max))
+        self.tile_cap = tile_cap
+        self.variant = variant
+        self.heavy_rows = int(len(heavy_ids))
         self.struct = native.Csr(
             self.num_rows, self.num_cols, self.nnz,
             self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.values.data_ptr(),
-            self.tile_ptr.data_ptr(), self.num_tiles, exact_row_max, 0)
+            self.tile_ptr.data_ptr(), self.num_tiles,
+            self.light_tiles.data_ptr() if len(light_ids) else None, len(light_ids),
+            self.heavy_tiles.data_ptr() if len(heavy_ids) else None, len(heavy_ids),
+            exact_row_max, tile_cap, variant, 0)
+
+    def tensors(self):
+        return (self.row_ptr, self.col_idx, self.values, self.tile_ptr, self.light_tiles, self.heavy_tiles)
 
     def src(self, gather: torch.Tensor | None) -> native.Src:
         s = native.Src()

@@ -109,6 +109,46 @@ __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
   return v;
 }
 
+// ------------------------------------------------ async copies (TMA, LDGSTS)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  }
+}
+// 1D bulk copy global -> shared through the TMA unit (SASS UBLKCP), completion
+// signalled on `bar`, L2 evict-first policy for the streamed matrix.
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                             uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// 8-byte LDGSTS gather with an L2 evict-last policy (the dense vector stays
+// resident in L2 across iterations).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;"
+               ::"r"(smem_u32(dst)), "l"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ------------------------------------------------------- deterministic sums
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -455,6 +495,125 @@ __global__ void __launch_bounds__(TPB) tile_kernel(gridlp_csr_t A, const double*
   store_partials<Op>(acc, partials);
 }
 
+// Persistent, TMA-pipelined product + epilogue kernel (variant 0).
+// Each CTA walks its light tiles (round-robin over light_tiles) with a
+// two-slot pipeline: while tile i is gathered and summed, the TMA unit
+// streams tile i+1's values and column indices into the other slot. The
+// gathers of the dense vector are 8-byte LDGSTS (cp.async) straight into
+// shared memory, so every gather of a tile is in flight at once without
+// holding registers. Row sums are the same sequential +0.0-seeded sums as
+// the one-CTA-per-tile kernel (bit-identical to scipy). Heavy tiles follow,
+// tree-summed by the whole CTA. Reduction partials are per CTA, in a fixed
+// tile order, hence deterministic.
+struct PipeLayout {
+  int cap;
+  __host__ __device__ size_t vals_bytes() const { return (size_t)(cap + 4) * 8; }
+  __host__ __device__ size_t cols_bytes() const { return (size_t)(cap + 8) * 4; }
+  __host__ __device__ size_t slot_bytes() const { return vals_bytes() + cols_bytes(); }
+  __host__ __device__ size_t total() const { return 2 * slot_bytes() + (size_t)cap * 8 + 64; }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(TPB) tile_kernel_pipe(gridlp_csr_t A, const double* __restrict__ g,
+                                                        Op op, double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const PipeLayout L{A.tile_nnz_cap};
+  double* xbuf = reinterpret_cast<double*>(smem_raw + 2 * L.slot_bytes());
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 2 * L.slot_bytes() + (size_t)L.cap * 8);
+  auto slot_vals = [&](int s) { return reinterpret_cast<double*>(smem_raw + s * L.slot_bytes()); };
+  auto slot_cols = [&](int s) {
+    return reinterpret_cast<int*>(smem_raw + s * L.slot_bytes() + L.vals_bytes());
+  };
+
+  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+  const int tid = threadIdx.x;
+  op.prepare();
+  const uint64_t pf = policy_evict_first();
+  const uint64_t pl = policy_evict_last();
+  const int* __restrict__ rp = A.row_ptr;
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // stage the streams of light tile #idx (in this CTA's sequence) into slot s
+  auto issue = [&](int64_t idx, int s) {
+    const int t = A.light_tiles[idx];
+    const int p0 = rp[A.tile_ptr[t]];
+    const int p1 = rp[A.tile_ptr[t + 1]];
+    const int va = p0 & ~1, vb = (p1 + 1) & ~1;
+    const int ca = p0 & ~3, cb = (p1 + 3) & ~3;
+    const uint32_t vbytes = (uint32_t)(vb - va) * 8u, cbytes = (uint32_t)(cb - ca) * 4u;
+    fence_proxy_async();
+    mbar_expect_tx(&bars[s], vbytes + cbytes);
+    if (vbytes) tma_bulk_g2s(slot_vals(s), A.values + va, vbytes, &bars[s], pf);
+    if (cbytes) tma_bulk_g2s(slot_cols(s), A.col_idx + ca, cbytes, &bars[s], pf);
+  };
+
+  const int64_t stride = gridDim.x;
+  int64_t i = blockIdx.x;
+  uint32_t phase[2] = {0u, 0u};
+  if (i < A.num_light && tid == 0) issue(i, 0);
+  for (int it = 0; i < A.num_light; ++it, i += stride) {
+    const int s = it & 1;
+    const int t = A.light_tiles[i];
+    const int r0 = A.tile_ptr[t];
+    const int r1 = A.tile_ptr[t + 1];
+    const int p0 = rp[r0];
+    const int p1 = rp[r1];
+    const int nnz = p1 - p0;
+    const int r = r0 + tid;
+    const bool mine = r < r1;
+    typename Op::Data d{};
+    int a = 0, b = 0;
+    if (mine) {
+      d = op.load(r);                   // epilogue operands: in flight during the gathers
+      a = rp[r] - p0;
+      b = rp[r + 1] - p0;
+    }
+    if (tid == 0 && i + stride < A.num_light) issue(i + stride, s ^ 1);
+    mbar_wait(&bars[s], phase[s]);
+    phase[s] ^= 1u;
+    const double* sv = slot_vals(s) + (p0 & 1);
+    const int* sc = slot_cols(s) + (p0 & 3);
+    for (int k = tid; k < nnz; k += TPB) cp_async8(&xbuf[k], g + sc[k], pl);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    for (int k = tid; k < nnz; k += TPB) xbuf[k] = dmul(sv[k], xbuf[k]);
+    __syncthreads();
+    if (mine) {
+      double sum = 0.0;
+      for (int k = a; k < b; ++k) sum = dadd(sum, xbuf[k]);
+      op.row(r, sum, d, acc);
+    }
+    __syncthreads();
+  }
+
+  for (int64_t h = blockIdx.x; h < A.num_heavy; h += stride) {
+    const int t = A.heavy_tiles[h];
+    const int row = A.tile_ptr[t];
+    const int p0 = rp[row], p1 = rp[row + 1];
+    typename Op::Data d{};
+    if (tid == 0) d = op.load(row);
+    double sum = 0.0;
+    for (int k = p0 + tid; k < p1; k += TPB)
+      sum = dadd(sum, dmul(ld_stream(A.values + k, pf), ld_gather(g + ld_stream(A.col_idx + k, pf), pl)));
+    double tmp[1] = {sum};
+    __shared__ double hscratch[1][WARPS];
+    block_sum<1>(tmp, hscratch);
+    if (tid == 0) op.row(row, tmp[0], d, acc);
+    __syncthreads();
+  }
+  store_partials<Op>(acc, partials);
+}
+
 // Row-wise epilogue over ascending-order sums of partial vectors.
 template <class Op>
 __global__ void __launch_bounds__(TPB) rows_kernel(gridlp_src_t src, int64_t n, Op op,
@@ -511,8 +670,15 @@ int check_csr(const gridlp_csr_t* A) {
   if (A->num_rows < 0 || A->num_cols < 0 || A->nnz < 0 || A->num_tiles < 0)
     return fail(GRIDLP_ERR_ARG, "negative matrix dimension");
   if (A->nnz >= (int64_t(1) << 31)) return fail(GRIDLP_ERR_ARG, "block nnz must be < 2^31");
-  if (A->exact_row_max < 0 || A->exact_row_max > CAP / 2)
-    return fail(GRIDLP_ERR_ARG, "exact_row_max must be in [0, TILE_NNZ_CAP/2]");
+  if (A->tile_nnz_cap < 64 || A->tile_nnz_cap > CAP || (A->tile_nnz_cap & 7))
+    return fail(GRIDLP_ERR_ARG, "tile_nnz_cap must be a multiple of 8 in [64, TILE_NNZ_CAP]");
+  if (A->exact_row_max < 0 || A->exact_row_max > A->tile_nnz_cap / 2)
+    return fail(GRIDLP_ERR_ARG, "exact_row_max must be in [0, tile_nnz_cap/2]");
+  if (A->variant != 0 && A->variant != 1) return fail(GRIDLP_ERR_ARG, "unknown kernel variant");
+  if (A->num_light + A->num_heavy != A->num_tiles)
+    return fail(GRIDLP_ERR_ARG, "light + heavy tiles must cover the tile directory");
+  if (A->num_tiles > 0 && ((A->num_light > 0 && !A->light_tiles) || (A->num_heavy > 0 && !A->heavy_tiles)))
+    return fail(GRIDLP_ERR_ARG, "missing light/heavy tile lists");
   if (A->num_rows > 0 && (!A->row_ptr || !A->tile_ptr || A->num_tiles < 1))
     return fail(GRIDLP_ERR_ARG, "missing row_ptr/tile_ptr");
   if (A->nnz > 0 && (!A->col_idx || !A->values)) return fail(GRIDLP_ERR_ARG, "missing col_idx/values");
@@ -520,6 +686,29 @@ int check_csr(const gridlp_csr_t* A) {
 }
 
 int64_t src_rows(const gridlp_src_t* src) { return src->A ? src->A->num_rows : src->num_rows; }
+
+// CTAs of the persistent kernel: SMs x resident CTAs (cached per op type and
+// shared-memory size).
+template <class Op>
+int pipe_grid(size_t smem) {
+  static size_t cached_smem = 0;
+  static int cached = 0;
+  if (cached > 0 && cached_smem == smem) return cached;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(tile_kernel_pipe<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return -1;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel_pipe<Op>, TPB, smem) != cudaSuccess)
+    return -1;
+  if (per_sm < 1) per_sm = 1;
+  cached = sms * per_sm;
+  cached_smem = smem;
+  return cached;
+}
 
 template <class Op>
 int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* stream,
@@ -552,8 +741,16 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
     }
   }
   if (slots > 0) {
-    if (src->A) {
-      tile_kernel<Op><<<(unsigned)slots, TPB, CAP * sizeof(double), s>>>(*src->A, src->gather, op, partials);
+    if (src->A && src->A->variant == 0) {
+      const size_t smem = PipeLayout{src->A->tile_nnz_cap}.total();
+      int grid = pipe_grid<Op>(smem);
+      if (grid <= 0) return fail(GRIDLP_ERR_CUDA, std::string(name) + ": occupancy query failed");
+      if (grid > slots) grid = (int)slots;
+      slots = grid;
+      tile_kernel_pipe<Op><<<(unsigned)grid, TPB, smem, s>>>(*src->A, src->gather, op, partials);
+    } else if (src->A) {
+      tile_kernel<Op><<<(unsigned)slots, TPB, src->A->tile_nnz_cap * sizeof(double), s>>>(
+          *src->A, src->gather, op, partials);
     } else {
       rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials);
     }

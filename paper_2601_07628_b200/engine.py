@@ -66,6 +66,8 @@ class EngineOptions:
     omega_max: float = 1e6
     time_limit_seconds: float | None = None
     exact_row_max: int = DEFAULT_EXACT_ROW_MAX
+    tile_cap: int = 2048
+    kernel_variant: int = 1
     use_graphs: bool = True
     graph_chunk: int = 128
 
@@ -219,11 +221,11 @@ class PdhgEngine:
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
         for (i, j) in local:
             hb = host_blocks[(i, j)]
-            self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, self.opts.exact_row_max),
-                                             DeviceCsr(transpose(hb), dev, self.opts.exact_row_max))
+            kw = dict(exact_row_max=self.opts.exact_row_max, tile_cap=self.opts.tile_cap,
+                      variant=self.opts.kernel_variant)
+            self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(transpose(hb), dev, **kw))
         del host_blocks, pa
-        tensors = [t for b in self.blocks.values() for d in (b.A, b.AT)
-                   for t in (d.row_ptr, d.col_idx, d.values, d.tile_ptr)]
+        tensors = [t for b in self.blocks.values() for d in (b.A, b.AT) for t in d.tensors()]
         tensors += [t for c in self.cols.values() for t in (c.c, c.lo, c.hi)]
         tensors += [t for r in self.rows.values() for t in (r.lo, r.hi)]
         self.h2d_bytes = int(sum(t.numel() * t.element_size() for t in tensors))

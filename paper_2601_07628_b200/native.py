@@ -22,6 +22,7 @@ HEADER = ROOT / "include" / "gridlp_b200.h"
 MAX_RED = 8
 MAX_PARTS = 16
 TILE_NNZ_CAP = 4096
+DEFAULT_TILE_CAP = 2048
 TILE_ROWS = 256
 F_HALPERN = 1
 F_SUMSQ = 2
@@ -37,7 +38,10 @@ class Csr(ctypes.Structure):
     _fields_ = [("num_rows", c_int64), ("num_cols", c_int64), ("nnz", c_int64),
                 ("row_ptr", c_void_p), ("col_idx", c_void_p), ("values", c_void_p),
                 ("tile_ptr", c_void_p), ("num_tiles", c_int64),
-                ("exact_row_max", c_int32), ("reserved", c_int32)]
+                ("light_tiles", c_void_p), ("num_light", c_int64),
+                ("heavy_tiles", c_void_p), ("num_heavy", c_int64),
+                ("exact_row_max", c_int32), ("tile_nnz_cap", c_int32),
+                ("variant", c_int32), ("reserved", c_int32)]
 
 
 class Src(ctypes.Structure):
