@@ -80,9 +80,31 @@ typedef struct gridlp_csr {
   int64_t num_light;
   const int32_t* heavy_tiles; /* [num_heavy] */
   int64_t num_heavy;
+  /* SELL-32 windows (variant 6): rows are taken in windows of 256; the
+   * light rows of a window are sorted by length (descending, stable) into 8
+   * slices of 32 lanes; slice s stores its entry j of lane l at
+   * sell_*[slice_off[s] + 32 j + l] (column-major inside the slice, so a
+   * warp reads 32 consecutive values per step), in the row's original entry
+   * order. lane_info[32 s + l] = (row length << 8) | (row & 255), or -1 for
+   * an empty lane. Rows longer than exact_row_max are kept as a compact CSR
+   * (heavy_rows / heavy_ptr / heavy_cols / heavy_vals) and tree-summed. */
+  const double* sell_vals;    /* [slice_off[num_slices]] */
+  const int32_t* sell_cols;
+  const int32_t* slice_off;   /* [8 * num_windows + 1] */
+  const int32_t* lane_info;   /* [256 * num_windows] */
+  int64_t num_windows;
+  const int32_t* heavy_rows;  /* [num_heavy_rows] */
+  const int32_t* heavy_ptr;   /* [num_heavy_rows + 1] */
+  const int32_t* heavy_cols;
+  const double* heavy_vals;
+  int64_t num_heavy_rows;
   int32_t exact_row_max;      /* <= tile_nnz_cap/2 */
   int32_t tile_nnz_cap;       /* <= GRIDLP_TILE_NNZ_CAP */
-  int32_t variant;            /* 0: persistent TMA-pipelined (default); 1: one CTA per tile */
+  int32_t variant;            /* product kernel: 0 persistent TMA-pipelined; 1/2/5 one CTA
+                                 per tile (register-staged, 5/8/6 CTAs per SM); 3/4 one CTA
+                                 per tile with TMA-staged matrix stream (8/5 CTAs per SM);
+                                 6/7/8 SELL-32 windows, register row sums, no shared staging
+                                 (8/6/5 CTAs per SM) */
   int32_t reserved;
 } gridlp_csr_t;
 

@@ -19,6 +19,7 @@ import torch
 from . import native
 
 DEFAULT_EXACT_ROW_MAX = 512
+DEFAULT_VARIANT = 6
 
 
 @dataclass
@@ -120,51 +121,122 @@ def build_tiles(ptr: np.ndarray, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
     return tiles.astype(np.int32)
 
 
-class DeviceCsr:
-    """One tiled CSR block resident in HBM; `.struct` is the gridlp_csr_t.
+SELL_WINDOW = 256
 
-    `variant` 0 selects the persistent TMA-pipelined product kernel, 1 the
-    one-CTA-per-tile kernel (kept for A/B measurement)."""
+
+def build_sell(host: HostCsr, exact_row_max: int, window: int = SELL_WINDOW):
+    """SELL-32 layout of include/gridlp_b200.h (variant 6): per 256-row
+    window the light rows sorted by length (descending, stable) into 32-lane
+    slices stored column-major; heavy rows as a compact CSR."""
+    ptr, m = host.ptr, host.num_rows
+    lens = np.diff(ptr)
+    heavy = lens > exact_row_max
+    nw = -(-m // window) if m else 0
+    eff = np.where(heavy, -1, lens)
+    win = np.arange(m, dtype=np.int64) // window
+    order = np.lexsort((-eff, win))             # window-major, longest first, heavy last
+    info = np.full(nw * window, -1, dtype=np.int64)
+    slen = eff[order]
+    light = slen >= 0
+    pos = np.flatnonzero(light)
+    info[pos] = (slen[pos] << 8) | (order[pos] & 255)
+    lane_len = np.zeros(nw * window, dtype=np.int64)
+    lane_len[pos] = slen[pos]
+    slice_len = lane_len.reshape(-1, 32).max(axis=1) if nw else np.zeros(0, np.int64)
+    slice_off = np.concatenate([[0], np.cumsum(32 * slice_len)]).astype(np.int64)
+    total = int(slice_off[-1])
+    if total >= 2 ** 31 - 64:
+        raise ValueError("SELL block too large for int32 offsets")
+    vals = np.zeros(total + 8, dtype=np.float64)
+    cols = np.zeros(total + 8, dtype=np.int32)
+    rows_l = order[pos]
+    cnt = lens[rows_l]
+    base = slice_off[pos // 32] + (pos % 32)
+    nl = int(cnt.sum())
+    if nl:
+        first = np.repeat(np.cumsum(cnt) - cnt, cnt)
+        j = np.arange(nl, dtype=np.int64) - first
+        dest = np.repeat(base, cnt) + 32 * j
+        src = np.repeat(ptr[rows_l], cnt) + j
+        vals[dest] = host.val[src]
+        cols[dest] = host.col[src]
+    hrows = np.flatnonzero(heavy).astype(np.int64)
+    hlen = lens[hrows]
+    hptr = np.concatenate([[0], np.cumsum(hlen)]).astype(np.int64)
+    if len(hrows):
+        hsrc = np.repeat(ptr[hrows] - hptr[:-1], hlen) + np.arange(int(hptr[-1]), dtype=np.int64)
+        hcols = np.concatenate([host.col[hsrc].astype(np.int32), np.zeros(4, np.int32)])
+        hvals = np.concatenate([host.val[hsrc], np.zeros(4)])
+    else:
+        hcols, hvals = np.zeros(4, np.int32), np.zeros(4)
+    return dict(vals=vals, cols=cols, slice_off=slice_off.astype(np.int32),
+                lane_info=info.astype(np.int32), num_windows=nw, heavy_rows=hrows.astype(np.int32),
+                heavy_ptr=hptr.astype(np.int32), heavy_cols=hcols, heavy_vals=hvals)
+
+
+class DeviceCsr:
+    """One block resident in HBM; `.struct` is its gridlp_csr_t.
+
+    variant >= 6 (default 6): SELL-32 windows (build_sell) — only the SELL
+    arrays and the heavy-row CSR are uploaded. variants 0-5: tiled CSR
+    (tile directory + int32 CSR), kept for A/B measurement."""
 
     PAD = 4   # the TMA staging copies read whole 16-byte granules
 
     def __init__(self, host: HostCsr, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
-                 tile_cap: int = native.DEFAULT_TILE_CAP, variant: int = 0):
-        if host.nnz >= 2 ** 31 - 16:
-            raise ValueError("block nnz must be < 2^31 (int32 row pointers)")
+                 tile_cap: int = native.DEFAULT_TILE_CAP, variant: int = DEFAULT_VARIANT):
+        if host.nnz >= 2 ** 31 - 64:
+            raise ValueError("block nnz must be < 2^31 (int32 offsets)")
         self.num_rows, self.num_cols, self.nnz = host.num_rows, host.num_cols, host.nnz
-        tiles = build_tiles(host.ptr, exact_row_max, cap=tile_cap)
-        self.num_tiles = max(len(tiles) - 1, 0)
+        self.exact_row_max, self.tile_cap, self.variant = exact_row_max, tile_cap, variant
+        # the host copy is kept only for CPU-resident blocks (the CPU test double)
+        self.host = host if torch.device(device).type == "cpu" else None
+        self.dev = {}
+        up = lambda k, a: self.dev.__setitem__(k, torch.from_numpy(np.ascontiguousarray(a)).to(device))  # noqa: E731
+        ptr = lambda k: self.dev[k].data_ptr() if k in self.dev and self.dev[k].numel() else None  # noqa: E731
         lens = np.diff(host.ptr)
-        t_rows = np.diff(tiles.astype(np.int64))
-        first = tiles[:-1].astype(np.int64)
-        heavy = (t_rows == 1) & (lens[first] > exact_row_max) if self.num_tiles else np.zeros(0, bool)
-        light_ids = np.flatnonzero(~heavy).astype(np.int32)
-        heavy_ids = np.flatnonzero(heavy).astype(np.int32)
-        col = np.zeros(host.nnz + self.PAD, dtype=np.int32)
-        col[: host.nnz] = host.col
-        val = np.zeros(host.nnz + self.PAD, dtype=np.float64)
-        val[: host.nnz] = host.val
-        self.row_ptr = torch.from_numpy(host.ptr.astype(np.int32)).to(device)
-        self.col_idx = torch.from_numpy(col).to(device)
-        self.values = torch.from_numpy(val).to(device)
-        self.tile_ptr = torch.from_numpy(tiles).to(device)
-        self.light_tiles = torch.from_numpy(light_ids).to(device)
-        self.heavy_tiles = torch.from_numpy(heavy_ids).to(device)
-        self.exact_row_max = exact_row_max
-        self.tile_cap = tile_cap
-        self.variant = variant
-        self.heavy_rows = int(len(heavy_ids))
-        self.struct = native.Csr(
-            self.num_rows, self.num_cols, self.nnz,
-            self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.values.data_ptr(),
-            self.tile_ptr.data_ptr(), self.num_tiles,
-            self.light_tiles.data_ptr() if len(light_ids) else None, len(light_ids),
-            self.heavy_tiles.data_ptr() if len(heavy_ids) else None, len(heavy_ids),
-            exact_row_max, tile_cap, variant, 0)
+        self.heavy_rows = int(np.count_nonzero(lens > exact_row_max))
+        csr_args = [None, None, None, None, 0, None, 0, None, 0]
+        sell_args = [None] * 4 + [0] + [None] * 4 + [0]
+        self.num_tiles = 0
+        if variant >= 6:
+            sd = build_sell(host, exact_row_max)
+            for k in ("vals", "cols", "slice_off", "lane_info", "heavy_rows", "heavy_ptr", "heavy_cols",
+                      "heavy_vals"):
+                up("sell_" + k, sd[k])
+            sell_args = [ptr("sell_vals"), ptr("sell_cols"), ptr("sell_slice_off"), ptr("sell_lane_info"),
+                         sd["num_windows"], ptr("sell_heavy_rows"), ptr("sell_heavy_ptr"),
+                         ptr("sell_heavy_cols"), ptr("sell_heavy_vals"), len(sd["heavy_rows"])]
+            self.num_windows = sd["num_windows"]
+        else:
+            tiles = build_tiles(host.ptr, exact_row_max, cap=tile_cap)
+            self.num_tiles = max(len(tiles) - 1, 0)
+            t_rows = np.diff(tiles.astype(np.int64))
+            first = tiles[:-1].astype(np.int64)
+            heavy = (t_rows == 1) & (lens[first] > exact_row_max) if self.num_tiles else np.zeros(0, bool)
+            col = np.zeros(host.nnz + self.PAD, dtype=np.int32)
+            col[: host.nnz] = host.col
+            val = np.zeros(host.nnz + self.PAD, dtype=np.float64)
+            val[: host.nnz] = host.val
+            up("row_ptr", host.ptr.astype(np.int32))
+            up("col_idx", col)
+            up("values", val)
+            up("tile_ptr", tiles)
+            up("light_tiles", np.flatnonzero(~heavy).astype(np.int32))
+            up("heavy_tiles", np.flatnonzero(heavy).astype(np.int32))
+            csr_args = [ptr("row_ptr"), ptr("col_idx"), ptr("values"), ptr("tile_ptr"), self.num_tiles,
+                        ptr("light_tiles"), int(np.count_nonzero(~heavy)), ptr("heavy_tiles"),
+                        int(np.count_nonzero(heavy))]
+        self.struct = native.Csr(self.num_rows, self.num_cols, self.nnz, *csr_args, *sell_args,
+                                 exact_row_max, tile_cap, variant, 0)
 
     def tensors(self):
-        return (self.row_ptr, self.col_idx, self.values, self.tile_ptr, self.light_tiles, self.heavy_tiles)
+        return tuple(self.dev.values())
+
+    def slots(self) -> int:
+        if self.variant >= 6:
+            return self.num_windows + self.heavy_rows
+        return self.num_tiles
 
     def src(self, gather: torch.Tensor | None) -> native.Src:
         s = native.Src()

@@ -419,10 +419,13 @@ __device__ __forceinline__ void store_partials(double (&acc)[Op::NRED > 0 ? Op::
   }
 }
 
-// Sparse-product + fused-epilogue kernel over a tile directory.
-template <class Op>
-__global__ void __launch_bounds__(TPB) tile_kernel(gridlp_csr_t A, const double* __restrict__ g,
-                                                   Op op, double* __restrict__ partials) {
+// Sparse-product + fused-epilogue kernel over a tile directory, one CTA per
+// tile. LEAN (variant 2) trades the early epilogue prefetch and the 8-deep
+// unroll for <= 32 registers, so 8 CTAs (64 warps) stay resident per SM and
+// keep the gather stream saturated.
+template <class Op, int U, int MINB, bool LEAN>
+__global__ void __launch_bounds__(TPB, MINB) tile_kernel(gridlp_csr_t A, const double* __restrict__ g,
+                                                         Op op, double* __restrict__ partials) {
   extern __shared__ double prod[];
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   double acc[NR];
@@ -458,31 +461,36 @@ __global__ void __launch_bounds__(TPB) tile_kernel(gridlp_csr_t A, const double*
     const bool mine = r < r1;
     typename Op::Data d{};
     int a = 0, b = 0;
-    if (mine) {
+    if (mine && !LEAN) {
       d = op.load(r);
       a = A.row_ptr[r] - p0;
       b = A.row_ptr[r + 1] - p0;
     }
     // phase (a): balanced gathers, rounded products into shared memory
-    for (int base = p0 + tid; base < p1; base += TPB * UNROLL) {
-      int cidx[UNROLL];
-      double v[UNROLL], xv[UNROLL];
+    for (int base = p0 + tid; base < p1; base += TPB * U) {
+      int cidx[U];
+      double v[U], xv[U];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int k = base + u * TPB;
         cidx[u] = k < p1 ? ld_stream(col + k, pf) : 0;
       }
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int k = base + u * TPB;
         v[u] = k < p1 ? ld_stream(val + k, pf) : 0.0;
         xv[u] = k < p1 ? ld_gather(g + cidx[u], pl) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int k = base + u * TPB;
         if (k < p1) prod[k - p0] = dmul(v[u], xv[u]);
       }
+    }
+    if (mine && LEAN) {
+      d = op.load(r);
+      a = A.row_ptr[r] - p0;
+      b = A.row_ptr[r + 1] - p0;
     }
     __syncthreads();
     // phase (b): sequential row sums (scipy csr_matvec order) + epilogue
@@ -491,6 +499,170 @@ __global__ void __launch_bounds__(TPB) tile_kernel(gridlp_csr_t A, const double*
       for (int k = a; k < b; ++k) s = dadd(s, prod[k]);
       op.row(r, s, d, acc);
     }
+  }
+  store_partials<Op>(acc, partials);
+}
+
+// One CTA per tile with the matrix stream staged by the TMA unit
+// (variants 3/4): thread 0 issues two 1D bulk copies (values, column
+// indices) into shared memory, so the LSU/L1 path carries only the gathers
+// and the epilogue vectors. Gathers read the staged column indices and the
+// rounded products overwrite the staged values in place; row sums as above.
+template <class Op, int U, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) tile_kernel_tma(gridlp_csr_t A, const double* __restrict__ g,
+                                                             Op op, double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int cap = A.tile_nnz_cap;
+  double* sv = reinterpret_cast<double*>(smem_raw);
+  int* sc = reinterpret_cast<int*>(smem_raw + (size_t)(cap + 4) * 8);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + (size_t)(cap + 4) * 8 + (size_t)(cap + 8) * 4);
+  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+  const int tid = threadIdx.x;
+  const int64_t t = blockIdx.x;
+  const int r0 = A.tile_ptr[t];
+  const int r1 = A.tile_ptr[t + 1];
+  const int p0 = A.row_ptr[r0];
+  const int p1 = A.row_ptr[r1];
+  op.prepare();
+  const uint64_t pf = policy_evict_first();
+  const uint64_t pl = policy_evict_last();
+
+  if (r1 - r0 == 1 && p1 - p0 > A.exact_row_max) {
+    typename Op::Data d{};
+    if (tid == 0) d = op.load(r0);
+    double s = 0.0;
+    for (int k = p0 + tid; k < p1; k += TPB)
+      s = dadd(s, dmul(ld_stream(A.values + k, pf), ld_gather(g + ld_stream(A.col_idx + k, pf), pl)));
+    double tmp[1] = {s};
+    __shared__ double hscratch[1][WARPS];
+    block_sum<1>(tmp, hscratch);
+    if (tid == 0) op.row(r0, tmp[0], d, acc);
+    __syncthreads();
+  } else {
+    const int nnz = p1 - p0;
+    if (tid == 0) {
+      const int va = p0 & ~1, vb = (p1 + 1) & ~1;
+      const int ca = p0 & ~3, cb = (p1 + 3) & ~3;
+      const uint32_t vbytes = (uint32_t)(vb - va) * 8u, cbytes = (uint32_t)(cb - ca) * 4u;
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(bar, vbytes + cbytes);
+      if (vbytes) tma_bulk_g2s(sv, A.values + va, vbytes, bar, pf);
+      if (cbytes) tma_bulk_g2s(sc, A.col_idx + ca, cbytes, bar, pf);
+    }
+    const int r = r0 + tid;
+    const bool mine = r < r1;
+    typename Op::Data d{};
+    int a = 0, b = 0;
+    if (mine) {
+      d = op.load(r);
+      a = A.row_ptr[r] - p0;
+      b = A.row_ptr[r + 1] - p0;
+    }
+    __syncthreads();            // barrier initialised before anyone waits on it
+    mbar_wait(bar, 0);
+    double* v = sv + (p0 & 1);
+    const int* c = sc + (p0 & 3);
+    for (int base = tid; base < nnz; base += TPB * U) {
+      double xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = base + u * TPB;
+        xv[u] = k < nnz ? ld_gather(g + c[k], pl) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = base + u * TPB;
+        if (k < nnz) v[k] = dmul(v[k], xv[u]);
+      }
+    }
+    __syncthreads();
+    if (mine) {
+      double sum = 0.0;
+      for (int k = a; k < b; ++k) sum = dadd(sum, v[k]);
+      op.row(r, sum, d, acc);
+    }
+  }
+  store_partials<Op>(acc, partials);
+}
+
+// SELL-32 window kernel (variant 6). One CTA = one window of 256 rows =
+// 8 warps = 8 slices. Each lane owns one light row of its slice and walks
+// the row's entries in their original order: the column index and value of
+// step j are 32 consecutive elements across the warp (fully coalesced), the
+// gather of x is one 8-byte load, and the sum lives in a register — no
+// shared-memory staging of products, no bank conflicts, no phase barrier.
+// Sums are parked in shared memory by window-local row and the epilogue
+// then runs in natural row order (coalesced vector traffic). Blocks past the
+// windows tree-sum one heavy row each (compact CSR).
+template <class Op, int U, int MINB, bool EARLY>
+__global__ void __launch_bounds__(TPB, MINB) sell_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
+                                                         double* __restrict__ partials) {
+  __shared__ double sums[TPB];
+  __shared__ int have[TPB];
+  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+  const int tid = threadIdx.x;
+  op.prepare();
+  const uint64_t pf = policy_evict_first();
+  const uint64_t pl = policy_evict_last();
+  const int64_t w = blockIdx.x;
+  if (w >= A.num_windows) {
+    const int64_t h = w - A.num_windows;
+    const int row = A.heavy_rows[h];
+    const int p0 = A.heavy_ptr[h], p1 = A.heavy_ptr[h + 1];
+    typename Op::Data d{};
+    if (tid == 0) d = op.load(row);
+    double s = 0.0;
+    for (int k = p0 + tid; k < p1; k += TPB)
+      s = dadd(s, dmul(ld_stream(A.heavy_vals + k, pf), ld_gather(g + ld_stream(A.heavy_cols + k, pf), pl)));
+    double tmp[1] = {s};
+    __shared__ double hscratch[1][WARPS];
+    block_sum<1>(tmp, hscratch);
+    if (tid == 0) op.row(row, tmp[0], d, acc);
+    __syncthreads();
+  } else {
+    const int64_t r = w * TPB + tid;
+    const bool in_range = r < A.num_rows;
+    typename Op::Data d{};
+    if (EARLY && in_range) d = op.load(r);   // natural-order epilogue operands, issued first
+    have[tid] = 0;
+    const int lane = tid & 31;
+    const int64_t slice = w * WARPS + (tid >> 5);
+    const int info = A.lane_info[slice * 32 + lane];
+    __syncthreads();
+    if (info >= 0) {
+      const int len = info >> 8;
+      const int64_t base = (int64_t)A.slice_off[slice] + lane;
+      const int* __restrict__ cp = A.sell_cols + base;
+      const double* __restrict__ vp = A.sell_vals + base;
+      double s = 0.0;
+      for (int j = 0; j < len; j += U) {
+        int c[U];
+        double v[U], x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = j + u < len;
+          c[u] = ok ? ld_stream(cp + 32 * (j + u), pf) : 0;
+          v[u] = ok ? ld_stream(vp + 32 * (j + u), pf) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = (j + u < len) ? ld_gather(g + c[u], pl) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
+      }
+      sums[info & 255] = s;
+      have[info & 255] = 1;
+    }
+    if (!EARLY && in_range) d = op.load(r);
+    __syncthreads();
+    if (in_range && have[tid]) op.row(r, sums[tid], d, acc);
   }
   store_partials<Op>(acc, partials);
 }
@@ -674,7 +846,16 @@ int check_csr(const gridlp_csr_t* A) {
     return fail(GRIDLP_ERR_ARG, "tile_nnz_cap must be a multiple of 8 in [64, TILE_NNZ_CAP]");
   if (A->exact_row_max < 0 || A->exact_row_max > A->tile_nnz_cap / 2)
     return fail(GRIDLP_ERR_ARG, "exact_row_max must be in [0, tile_nnz_cap/2]");
-  if (A->variant != 0 && A->variant != 1) return fail(GRIDLP_ERR_ARG, "unknown kernel variant");
+  if (A->variant < 0 || A->variant > 8) return fail(GRIDLP_ERR_ARG, "unknown kernel variant");
+  if (A->variant >= 6) {
+    if (A->num_rows > 0 &&
+        (!A->slice_off || !A->lane_info || A->num_windows != (A->num_rows + TPB - 1) / TPB))
+      return fail(GRIDLP_ERR_ARG, "SELL layout missing or inconsistent");
+    if (A->num_heavy_rows > 0 && (!A->heavy_rows || !A->heavy_ptr || !A->heavy_cols || !A->heavy_vals))
+      return fail(GRIDLP_ERR_ARG, "missing heavy-row CSR");
+    if (A->nnz > 0 && (!A->sell_cols || !A->sell_vals)) return fail(GRIDLP_ERR_ARG, "missing SELL arrays");
+    return GRIDLP_OK;
+  }
   if (A->num_light + A->num_heavy != A->num_tiles)
     return fail(GRIDLP_ERR_ARG, "light + heavy tiles must cover the tile directory");
   if (A->num_tiles > 0 && ((A->num_light > 0 && !A->light_tiles) || (A->num_heavy > 0 && !A->heavy_tiles)))
@@ -722,7 +903,8 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
     if (rc) return rc;
     if (src->A->num_rows > 0 && src->A->nnz > 0 && !src->gather)
       return fail(GRIDLP_ERR_ARG, std::string(name) + ": missing gather vector");
-    slots = src->A->num_rows > 0 ? src->A->num_tiles : 0;
+    slots = src->A->num_rows <= 0 ? 0
+            : (src->A->variant >= 6 ? src->A->num_windows + src->A->num_heavy_rows : src->A->num_tiles);
   } else {
     if (src->nparts < 0 || src->nparts > GRIDLP_MAX_PARTS)
       return fail(GRIDLP_ERR_ARG, std::string(name) + ": nparts out of range");
@@ -749,8 +931,26 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
       slots = grid;
       tile_kernel_pipe<Op><<<(unsigned)grid, TPB, smem, s>>>(*src->A, src->gather, op, partials);
     } else if (src->A) {
-      tile_kernel<Op><<<(unsigned)slots, TPB, src->A->tile_nnz_cap * sizeof(double), s>>>(
-          *src->A, src->gather, op, partials);
+      const gridlp_csr_t& M = *src->A;
+      const size_t sm_prod = M.tile_nnz_cap * sizeof(double);
+      const size_t sm_tma = (size_t)(M.tile_nnz_cap + 4) * 8 + (size_t)(M.tile_nnz_cap + 8) * 4 + 16;
+      const unsigned nb = (unsigned)slots;
+      switch (M.variant) {
+        case 2: tile_kernel<Op, 4, 8, true><<<nb, TPB, sm_prod, s>>>(M, src->gather, op, partials); break;
+        case 3: tile_kernel_tma<Op, 4, 8><<<nb, TPB, sm_tma, s>>>(M, src->gather, op, partials); break;
+        case 4: tile_kernel_tma<Op, 8, 5><<<nb, TPB, sm_tma, s>>>(M, src->gather, op, partials); break;
+        case 5: tile_kernel<Op, 4, 6, false><<<nb, TPB, sm_prod, s>>>(M, src->gather, op, partials); break;
+        case 6: case 7: case 8: {
+          const unsigned nsell = (unsigned)(M.num_windows + M.num_heavy_rows);
+          slots = nsell;
+          if (!nsell) break;
+          if (M.variant == 6) sell_kernel<Op, 4, 8, false><<<nsell, TPB, 0, s>>>(M, src->gather, op, partials);
+          else if (M.variant == 7) sell_kernel<Op, 8, 6, false><<<nsell, TPB, 0, s>>>(M, src->gather, op, partials);
+          else sell_kernel<Op, 4, 5, true><<<nsell, TPB, 0, s>>>(M, src->gather, op, partials);
+          break;
+        }
+        default: tile_kernel<Op, UNROLL, 5, false><<<nb, TPB, sm_prod, s>>>(M, src->gather, op, partials); break;
+      }
     } else {
       rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials);
     }
@@ -798,6 +998,7 @@ int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes) {
 
 int64_t gridlp_op_slots(const gridlp_src_t* src) {
   if (!src) return 0;
+  if (src->A && src->A->variant >= 6) return src->A->num_windows + src->A->num_heavy_rows;
   if (src->A) return src->A->num_rows > 0 ? src->A->num_tiles : 0;
   return src->num_rows > 0 ? rows_blocks(src->num_rows) : 0;
 }

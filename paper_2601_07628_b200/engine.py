@@ -67,7 +67,7 @@ class EngineOptions:
     time_limit_seconds: float | None = None
     exact_row_max: int = DEFAULT_EXACT_ROW_MAX
     tile_cap: int = 2048
-    kernel_variant: int = 1
+    kernel_variant: int = 6
     use_graphs: bool = True
     graph_chunk: int = 128
 
@@ -179,8 +179,8 @@ class PdhgEngine:
         t0 = time.perf_counter()
         self._build(problem)
         self.timings["setup_blocks_s"] = time.perf_counter() - t0
-        cap = max([b.A.num_tiles for b in self.blocks.values()]
-                  + [b.AT.num_tiles for b in self.blocks.values()] + [1184])
+        cap = max([b.A.slots() for b in self.blocks.values()]
+                  + [b.AT.slots() for b in self.blocks.values()] + [1184])
         self.nslots = self._assign_slots()
         self.ops = ops_factory(device, cap, self.nslots)
         self._plans()

@@ -40,6 +40,10 @@ class Csr(ctypes.Structure):
                 ("tile_ptr", c_void_p), ("num_tiles", c_int64),
                 ("light_tiles", c_void_p), ("num_light", c_int64),
                 ("heavy_tiles", c_void_p), ("num_heavy", c_int64),
+                ("sell_vals", c_void_p), ("sell_cols", c_void_p), ("slice_off", c_void_p),
+                ("lane_info", c_void_p), ("num_windows", c_int64),
+                ("heavy_rows", c_void_p), ("heavy_ptr", c_void_p), ("heavy_cols", c_void_p),
+                ("heavy_vals", c_void_p), ("num_heavy_rows", c_int64),
                 ("exact_row_max", c_int32), ("tile_nnz_cap", c_int32),
                 ("variant", c_int32), ("reserved", c_int32)]
 

@@ -35,9 +35,8 @@ class HostOps:
         key = id(dc)
         hit = self._mats.get(key)
         if hit is None or hit[0] is not dc:
-            nnz = dc.nnz
-            a = sp.csr_matrix((dc.values.numpy()[:nnz], dc.col_idx.numpy()[:nnz].astype(np.int64),
-                               dc.row_ptr.numpy().astype(np.int64)), shape=(dc.num_rows, dc.num_cols))
+            h = dc.host
+            a = sp.csr_matrix((h.val, h.col, h.ptr), shape=(h.num_rows, h.num_cols))
             hit = (dc, a)
             self._mats[key] = hit
         return hit[1]

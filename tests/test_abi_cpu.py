@@ -97,3 +97,40 @@ def test_tile_directory_invariants():
         assert b - a <= native.TILE_ROWS
         assert nnz <= native.TILE_NNZ_CAP
         assert np.all(lens[a:b] <= 512)
+
+
+def test_sell_layout_roundtrip():
+    """The SELL-32 window layout (variant 6) holds every light row's entries
+    in their original order and every heavy row in the compact CSR."""
+    from paper_2601_07628_b200.blocks import HostCsr, build_sell
+
+    rng = np.random.default_rng(1)
+    m, n = 1300, 900
+    lens = rng.integers(0, 50, m)
+    lens[[3, 700, 1299]] = [600, 2000, 513]
+    lens[10:300] = 0
+    ptr = np.concatenate([[0], np.cumsum(lens)])
+    col = rng.integers(0, n, int(ptr[-1]))
+    val = rng.standard_normal(int(ptr[-1]))
+    sd = build_sell(HostCsr(m, n, ptr, col, val), 512)
+    assert sd["num_windows"] == -(-m // 256)
+    seen = np.zeros(m, dtype=bool)
+    off, info = sd["slice_off"], sd["lane_info"]
+    for s in range(len(off) - 1):
+        for lane in range(32):
+            inf = int(info[32 * s + lane])
+            if inf < 0:
+                continue
+            length, local = inf >> 8, inf & 255
+            row = (s // 8) * 256 + local
+            assert length == lens[row] and not seen[row]
+            seen[row] = True
+            idx = off[s] + lane + 32 * np.arange(length)
+            np.testing.assert_array_equal(sd["cols"][idx], col[ptr[row]:ptr[row + 1]])
+            np.testing.assert_array_equal(sd["vals"][idx], val[ptr[row]:ptr[row + 1]])
+    heavy = np.flatnonzero(lens > 512)
+    np.testing.assert_array_equal(sd["heavy_rows"], heavy)
+    assert np.all(seen == (lens <= 512))
+    for h, row in enumerate(heavy):
+        a, b = sd["heavy_ptr"][h], sd["heavy_ptr"][h + 1]
+        np.testing.assert_array_equal(sd["heavy_cols"][a:b], col[ptr[row]:ptr[row + 1]])

@@ -78,7 +78,7 @@ def test_adjoint_identity_full_size(cfg2):
     A = cfg2.matrix
     h = HostCsr(A.num_rows, A.num_cols, A.row_offsets, A.col_indices, A.values)
     dA, dAT = DeviceCsr(h, dev), DeviceCsr(transpose(h), dev)
-    ops = CudaOps(dev, max(dA.num_tiles, dAT.num_tiles), 2)
+    ops = CudaOps(dev, max(dA.slots(), dAT.slots()), 2)
     rng = np.random.default_rng(0)
     x = torch.as_tensor(rng.standard_normal(A.num_cols), device=dev)
     y = torch.as_tensor(rng.standard_normal(A.num_rows), device=dev)

@@ -57,21 +57,26 @@ def test_library_is_loaded_from_tree():
     assert sm >= 100 and l2 > 0
 
 
+VARIANTS = [0, 1, 2, 3, 4, 5, 6]
+
+
 class TestProducts:
-    def test_golden_spmv_bitwise(self, ops):
+    @pytest.mark.parametrize("variant", VARIANTS)
+    def test_golden_spmv_bitwise(self, ops, variant):
         z = load_npz("spmv.npz")
         for t in range(int(z["ncases"])):
             for tag, vec, want in (("", "x", "ax"), ("t", "y", "aty")):
                 h = host_csr(z[f"c{t}_m"] if tag == "" else z[f"c{t}_n"],
                              z[f"c{t}_n"] if tag == "" else z[f"c{t}_m"],
                              z[f"c{t}_{tag}ptr"], z[f"c{t}_{tag}col"], z[f"c{t}_{tag}val"])
-                A = DeviceCsr(h, DEV)
+                A = DeviceCsr(h, DEV, variant=variant)
                 out = torch.full((h.num_rows,), np.nan, dtype=torch.float64, device=DEV)
                 ops.store(Fused(A, dev(z[f"c{t}_{vec}"])), out)
                 np.testing.assert_array_equal(out.cpu().numpy(), z[f"c{t}_{want}"])
 
-    @pytest.mark.parametrize("seed", range(4))
-    def test_random_bitwise_and_heavy_rows(self, ops, seed):
+    @pytest.mark.parametrize("variant", VARIANTS)
+    @pytest.mark.parametrize("seed", range(3))
+    def test_random_bitwise_and_heavy_rows(self, ops, seed, variant):
         import scipy.sparse as sp
 
         rng = np.random.default_rng(seed)
@@ -85,7 +90,7 @@ class TestProducts:
         x = rng.standard_normal(n)
         h = host_csr(m, n, ptr, col, val)
         want = sp.csr_matrix((val, col, ptr), shape=(m, n)).dot(x)
-        A = DeviceCsr(h, DEV)
+        A = DeviceCsr(h, DEV, variant=variant)
         assert A.heavy_rows == 5
         out = torch.empty(m, dtype=torch.float64, device=DEV)
         ops.store(Fused(A, dev(x)), out)

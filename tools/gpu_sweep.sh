@@ -1,12 +1,6 @@
 mkdir -p gpurun_out
-set -x
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
-tail -3 gpurun_out/smoke.log
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -15 gpurun_out/pytest_gpu.log
-for cfg in "0 2048" "0 1024" "0 4096" "1 2048" "1 4096"; do
-  set -- $cfg
-  timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --variant $1 --tile-cap $2 > gpurun_out/bench_v$1_c$2.log 2>&1
-  echo "variant $1 cap $2 rc=$?"
-  python -c "import json,sys; d=json.loads(open('gpurun_out/bench_v$1_c$2.log').read().strip().splitlines()[-1]); print('v$1 c$2', round(d['value']), 'it/s', d['roofline']['seconds_per_launch']*1e6, 'us/iter frac', round(d['roofline']['frac'],3), d['kernels'])" || tail -20 gpurun_out/bench_v$1_c$2.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "Products" > gpurun_out/pytest_products.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_products.log
+for V in ${@:-6 7 8 5}; do
+  timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --variant $V > gpurun_out/bench_v$V.log 2>&1
+  python -c "import json,sys; d=json.loads(open('gpurun_out/bench_v$V.log').read().strip().splitlines()[-1]); k=d['kernels']; print('v$V', round(d['value']), 'it/s', round(d['roofline']['seconds_per_launch']*1e6,1), 'us/iter frac', round(d['roofline']['frac'],3), 'K1', round(k['K1']['seconds']*1e6,1), 'K2', round(k['K2']['seconds']*1e6,1))" || tail -5 gpurun_out/bench_v$V.log
 done
