@@ -369,7 +369,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)
     ap.add_argument("--ref-sample-iters", type=int, default=4)
-    ap.add_argument("--variant", type=int, default=6, help="product kernel variant (0 pipelined, 1 per-tile)")
+    ap.add_argument("--variant", type=int, default=9, help="product kernel variant (0 pipelined, 1 per-tile)")
     ap.add_argument("--tile-cap", type=int, default=2048)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -31,6 +31,7 @@
 #ifndef GRIDLP_B200_H
 #define GRIDLP_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -85,7 +86,7 @@ typedef struct gridlp_csr {
    * slices of 32 lanes; slice s stores its entry j of lane l at
    * sell_*[slice_off[s] + 32 j + l] (column-major inside the slice, so a
    * warp reads 32 consecutive values per step), in the row's original entry
-   * order. lane_info[32 s + l] = (row length << 8) | (row & 255), or -1 for
+   * order. lane_info[32 s + l] = (row length << 8) | (row & (window-1)), or -1 for
    * an empty lane. Rows longer than exact_row_max are kept as a compact CSR
    * (heavy_rows / heavy_ptr / heavy_cols / heavy_vals) and tree-summed. */
   const double* sell_vals;    /* [slice_off[num_slices]] */
@@ -103,8 +104,9 @@ typedef struct gridlp_csr {
   int32_t variant;            /* product kernel: 0 persistent TMA-pipelined; 1/2/5 one CTA
                                  per tile (register-staged, 5/8/6 CTAs per SM); 3/4 one CTA
                                  per tile with TMA-staged matrix stream (8/5 CTAs per SM);
-                                 6/7/8 SELL-32 windows, register row sums, no shared staging
-                                 (8/6/5 CTAs per SM) */
+                                 6/7/8 SELL-32 windows of 256 rows, register row sums, no shared
+                                 staging (8/6/5 CTAs per SM); 9/10 SELL-32 windows of one warp
+                                 (32 rows), warp-synchronous, 64-thread CTAs */
   int32_t reserved;
 } gridlp_csr_t;
 
@@ -260,6 +262,48 @@ int gridlp_op_init_primal(const gridlp_primal_t* pv, void* stream);
 /* d_step->inner_k += delta on the device (a captured chunk of `delta`
  * iterations advances the Halpern counter itself, pdhg_engine.py:400). */
 int gridlp_op_step_advance(gridlp_step_t* d_step, int64_t delta, void* stream);
+
+/* --- one-off device preprocessing (csrc/gridlp_setup.cu) -----------------
+ * Replaces permute_problem / distribute / slice_block / transpose
+ * (partition.py:262-319, sparse_kernels.py:27-58; the from_coo lexsort of
+ * lp_model.py:121-141 is the reference's setup hot spot). All outputs are
+ * deterministic. `ws` is caller-allocated scratch of at least
+ * gridlp_setup_workspace_bytes(items, segments) bytes. */
+size_t gridlp_setup_workspace_bytes(int64_t max_items, int64_t max_segments);
+
+/* Row counts of one grid block: band row lr is source row band_rows[lr]; an
+ * entry belongs to the block when inv_col[col] is in [c0, c1). Writes the
+ * block's row pointers (exclusive scan, out_ptr[nrows] = block nnz). */
+int gridlp_block_count(const int64_t* src_ptr, const int32_t* src_col, const int64_t* band_rows,
+                       int64_t nrows, const int32_t* inv_col, int32_t c0, int32_t c1,
+                       int32_t* out_ptr, void* ws, size_t ws_bytes, void* stream);
+
+/* Entries of the block with local columns inv_col[col] - c0, each row sorted
+ * by column (== the reference's from_coo order after permutation). */
+int gridlp_block_fill(const int64_t* src_ptr, const int32_t* src_col, const double* src_val,
+                      const int64_t* band_rows, int64_t nrows, const int32_t* inv_col, int32_t c0,
+                      int32_t c1, const int32_t* out_ptr, int64_t nnz, int32_t* out_col,
+                      double* out_val, void* ws, size_t ws_bytes, void* stream);
+
+/* Explicit CSR transpose with sorted columns (sparse_kernels.py:27-36). */
+int gridlp_csr_transpose(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows,
+                         int64_t ncols, int64_t nnz, int32_t* t_ptr, int32_t* t_col, double* t_val,
+                         void* ws, size_t ws_bytes, void* stream);
+
+/* SELL-32 warp-window plan (variants 9/10): lane_info [32*ceil(nrows/32)],
+ * slice_off [ceil(nrows/32)+1], rank_of [nrows], heavy_rows [nrows],
+ * heavy_ptr [nrows+1]; sizes (device int64[3]) = {SELL elements, heavy rows,
+ * heavy nonzeros}. */
+int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t exact_row_max, int32_t* lane_info,
+                     int32_t* slice_off, int32_t* rank_of, int32_t* heavy_rows, int32_t* heavy_ptr,
+                     int64_t* sizes, void* ws, size_t ws_bytes, void* stream);
+
+/* SELL-32 fill from a CSR and its plan (padding zeroed). */
+int gridlp_sell_fill(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows,
+                     int32_t exact_row_max, const int32_t* slice_off, const int32_t* rank_of,
+                     const int32_t* heavy_rows, const int32_t* heavy_ptr, int64_t num_heavy,
+                     int32_t* sell_col, double* sell_val, int64_t sell_elems, int32_t* heavy_col,
+                     double* heavy_val, void* stream);
 
 #ifdef __cplusplus
 }

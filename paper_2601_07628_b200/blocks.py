@@ -19,7 +19,7 @@ import torch
 from . import native
 
 DEFAULT_EXACT_ROW_MAX = 512
-DEFAULT_VARIANT = 6
+DEFAULT_VARIANT = 9
 
 
 @dataclass
@@ -139,7 +139,7 @@ def build_sell(host: HostCsr, exact_row_max: int, window: int = SELL_WINDOW):
     slen = eff[order]
     light = slen >= 0
     pos = np.flatnonzero(light)
-    info[pos] = (slen[pos] << 8) | (order[pos] & 255)
+    info[pos] = (slen[pos] << 8) | (order[pos] & (window - 1))
     lane_len = np.zeros(nw * window, dtype=np.int64)
     lane_len[pos] = slen[pos]
     slice_len = lane_len.reshape(-1, 32).max(axis=1) if nw else np.zeros(0, np.int64)
@@ -177,33 +177,48 @@ def build_sell(host: HostCsr, exact_row_max: int, window: int = SELL_WINDOW):
 class DeviceCsr:
     """One block resident in HBM; `.struct` is its gridlp_csr_t.
 
-    variant >= 6 (default 6): SELL-32 windows (build_sell) — only the SELL
-    arrays and the heavy-row CSR are uploaded. variants 0-5: tiled CSR
-    (tile directory + int32 CSR), kept for A/B measurement."""
+    variant 9 (default; 10 = early epilogue loads): SELL-32 with one-warp
+    windows; variants 6-8: SELL-32 with 256-row windows — only the SELL
+    arrays and the heavy-row CSR live in HBM, built either on the host
+    (build_sell, from a HostCsr) or on the device (DeviceSetup.sell, passed
+    as a dict). Variants 0-5: tiled CSR (tile directory + int32 CSR), kept
+    for A/B measurement."""
 
     PAD = 4   # the TMA staging copies read whole 16-byte granules
 
     def __init__(self, host: HostCsr, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
                  tile_cap: int = native.DEFAULT_TILE_CAP, variant: int = DEFAULT_VARIANT):
-        if host.nnz >= 2 ** 31 - 64:
-            raise ValueError("block nnz must be < 2^31 (int32 offsets)")
-        self.num_rows, self.num_cols, self.nnz = host.num_rows, host.num_cols, host.nnz
+        if isinstance(host, dict):
+            shape = host["shape"]
+            self.num_rows, self.num_cols, self.nnz = shape
+            lens = np.zeros(0, dtype=np.int64)
+            self.heavy_rows = int(len(host["heavy_rows"]))
+        else:
+            if host.nnz >= 2 ** 31 - 64:
+                raise ValueError("block nnz must be < 2^31 (int32 offsets)")
+            self.num_rows, self.num_cols, self.nnz = host.num_rows, host.num_cols, host.nnz
+            lens = np.diff(host.ptr)
+            self.heavy_rows = int(np.count_nonzero(lens > exact_row_max))
         self.exact_row_max, self.tile_cap, self.variant = exact_row_max, tile_cap, variant
         # the host copy is kept only for CPU-resident blocks (the CPU test double)
         self.host = host if torch.device(device).type == "cpu" else None
         self.dev = {}
         up = lambda k, a: self.dev.__setitem__(k, torch.from_numpy(np.ascontiguousarray(a)).to(device))  # noqa: E731
         ptr = lambda k: self.dev[k].data_ptr() if k in self.dev and self.dev[k].numel() else None  # noqa: E731
-        lens = np.diff(host.ptr)
-        self.heavy_rows = int(np.count_nonzero(lens > exact_row_max))
         csr_args = [None, None, None, None, 0, None, 0, None, 0]
         sell_args = [None] * 4 + [0] + [None] * 4 + [0]
         self.num_tiles = 0
         if variant >= 6:
-            sd = build_sell(host, exact_row_max)
-            for k in ("vals", "cols", "slice_off", "lane_info", "heavy_rows", "heavy_ptr", "heavy_cols",
-                      "heavy_vals"):
-                up("sell_" + k, sd[k])
+            if isinstance(host, dict):      # SELL arrays already built on the device (DeviceSetup.sell)
+                sd = host
+                for k in ("vals", "cols", "slice_off", "lane_info", "heavy_rows", "heavy_ptr", "heavy_cols",
+                          "heavy_vals"):
+                    self.dev["sell_" + k] = sd[k]
+            else:
+                sd = build_sell(host, exact_row_max, window=32 if variant >= 9 else SELL_WINDOW)
+                for k in ("vals", "cols", "slice_off", "lane_info", "heavy_rows", "heavy_ptr", "heavy_cols",
+                          "heavy_vals"):
+                    up("sell_" + k, sd[k])
             sell_args = [ptr("sell_vals"), ptr("sell_cols"), ptr("sell_slice_off"), ptr("sell_lane_info"),
                          sd["num_windows"], ptr("sell_heavy_rows"), ptr("sell_heavy_ptr"),
                          ptr("sell_heavy_cols"), ptr("sell_heavy_vals"), len(sd["heavy_rows"])]
@@ -234,6 +249,8 @@ class DeviceCsr:
         return tuple(self.dev.values())
 
     def slots(self) -> int:
+        if self.variant >= 9:
+            return (self.num_windows + 1) // 2 + self.heavy_rows
         if self.variant >= 6:
             return self.num_windows + self.heavy_rows
         return self.num_tiles
@@ -264,3 +281,114 @@ def parts_src(parts, num_rows: int) -> native.Src:
     s.nparts = len(parts)
     s.num_rows = num_rows
     return s
+
+
+@dataclass
+class DeviceCsrArrays:
+    """A block (or its transpose) as int32 CSR in HBM — the output of the
+    device setup, input of the SELL build."""
+
+    num_rows: int
+    num_cols: int
+    nnz: int
+    ptr: torch.Tensor
+    col: torch.Tensor
+    val: torch.Tensor
+
+
+class DeviceSetup:
+    """One-off device preprocessing through the C ABI (csrc/gridlp_setup.cu):
+    the original CSR is uploaded once; every local block is then extracted
+    (permuted, column-banded, rows sorted by column), transposed and laid
+    out as SELL-32 on the device. Replaces the host permute/slice/transpose
+    (partition.py:262-319, sparse_kernels.py:27-58)."""
+
+    def __init__(self, problem, layout, device):
+        self.lib = native.load()
+        self.device = device
+        self.layout = layout
+        A = problem.matrix
+        m, n = int(A.num_rows), int(A.num_cols)
+        if n >= 2 ** 31 - 1 or m >= 2 ** 31 - 1:
+            raise ValueError("device setup needs < 2^31 rows and columns per matrix")
+        nnz = int(len(A.values))
+
+        def t(a, dt):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
+
+        self.src_ptr = t(A.row_offsets, np.int64)
+        self.src_col = t(A.col_indices, np.int32) if nnz else torch.zeros(1, dtype=torch.int32, device=device)
+        self.src_val = t(A.values, np.float64) if nnz else torch.zeros(1, dtype=torch.float64, device=device)
+        self.inv_col = t(layout.perm.inverse_cols(), np.int32) if n else torch.zeros(1, dtype=torch.int32,
+                                                                                      device=device)
+        self.row_perm = t(layout.perm.row_perm, np.int64) if m else torch.zeros(1, dtype=torch.int64,
+                                                                                 device=device)
+        items = max(nnz, m + n) + 64
+        segs = (m + n) + (m + n) // 32 + 64
+        wsb = int(self.lib._lib.gridlp_setup_workspace_bytes(items, segs))
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+        self.ws_bytes = wsb
+        self.h2d_bytes = sum(x.numel() * x.element_size()
+                             for x in (self.src_ptr, self.src_col, self.src_val, self.inv_col, self.row_perm))
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def block(self, i: int, j: int) -> DeviceCsrArrays:
+        lay = self.layout
+        r0, r1 = lay.row_range(i)
+        c0, c1 = lay.col_range(j)
+        nrows = r1 - r0
+        band = self.row_perm[r0:r1]
+        ptr = torch.empty(nrows + 1, dtype=torch.int32, device=self.device)
+        self.lib.call("gridlp_block_count", self.src_ptr.data_ptr(), self.src_col.data_ptr(),
+                      band.data_ptr() if nrows else None, nrows, self.inv_col.data_ptr(), c0, c1,
+                      ptr.data_ptr(), self.ws.data_ptr(), self.ws_bytes, self._stream())
+        nnz = int(ptr[-1].item())
+        col = torch.empty(nnz + 8, dtype=torch.int32, device=self.device)
+        val = torch.empty(nnz + 8, dtype=torch.float64, device=self.device)
+        self.lib.call("gridlp_block_fill", self.src_ptr.data_ptr(), self.src_col.data_ptr(),
+                      self.src_val.data_ptr(), band.data_ptr() if nrows else None, nrows,
+                      self.inv_col.data_ptr(), c0, c1, ptr.data_ptr(), nnz, col.data_ptr(), val.data_ptr(),
+                      self.ws.data_ptr(), self.ws_bytes, self._stream())
+        return DeviceCsrArrays(nrows, c1 - c0, nnz, ptr, col, val)
+
+    def transpose(self, a: DeviceCsrArrays) -> DeviceCsrArrays:
+        ptr = torch.empty(a.num_cols + 1, dtype=torch.int32, device=self.device)
+        col = torch.empty(a.nnz + 8, dtype=torch.int32, device=self.device)
+        val = torch.empty(a.nnz + 8, dtype=torch.float64, device=self.device)
+        self.lib.call("gridlp_csr_transpose", a.ptr.data_ptr(), a.col.data_ptr(), a.val.data_ptr(), a.num_rows,
+                      a.num_cols, a.nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), self.ws.data_ptr(),
+                      self.ws_bytes, self._stream())
+        return DeviceCsrArrays(a.num_cols, a.num_rows, a.nnz, ptr, col, val)
+
+    def sell(self, a: DeviceCsrArrays, exact_row_max: int) -> dict:
+        """SELL-32 warp-window arrays (variants 9/10) built on the device."""
+        dev, m = self.device, a.num_rows
+        ns = (m + 31) // 32
+        i32 = dict(dtype=torch.int32, device=dev)
+        lane_info = torch.empty(max(ns * 32, 1), **i32)
+        slice_off = torch.empty(ns + 1, **i32)
+        rank_of = torch.empty(max(m, 1), **i32)
+        heavy_rows = torch.empty(max(m, 1), **i32)
+        heavy_ptr = torch.empty(m + 1, **i32)
+        sizes = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.lib.call("gridlp_sell_plan", a.ptr.data_ptr(), m, exact_row_max, lane_info.data_ptr(),
+                      slice_off.data_ptr(), rank_of.data_ptr(), heavy_rows.data_ptr(), heavy_ptr.data_ptr(),
+                      sizes.data_ptr(), self.ws.data_ptr(), self.ws_bytes, self._stream())
+        total, nh, hnnz = (int(v) for v in sizes.cpu().tolist())
+        sell_col = torch.empty(total + 8, **i32)
+        sell_val = torch.empty(total + 8, dtype=torch.float64, device=dev)
+        hcol = torch.empty(hnnz + 8, **i32)
+        hval = torch.empty(hnnz + 8, dtype=torch.float64, device=dev)
+        self.lib.call("gridlp_sell_fill", a.ptr.data_ptr(), a.col.data_ptr(), a.val.data_ptr(), m, exact_row_max,
+                      slice_off.data_ptr(), rank_of.data_ptr(), heavy_rows.data_ptr(), heavy_ptr.data_ptr(), nh,
+                      sell_col.data_ptr(), sell_val.data_ptr(), total, hcol.data_ptr(), hval.data_ptr(),
+                      self._stream())
+        return dict(vals=sell_val, cols=sell_col, slice_off=slice_off, lane_info=lane_info,
+                    num_windows=ns, heavy_rows=heavy_rows[:nh].clone() if nh else heavy_rows[:0],
+                    heavy_ptr=heavy_ptr[: nh + 1].clone(), heavy_cols=hcol, heavy_vals=hval)
+
+    def release(self):
+        for name in ("src_ptr", "src_col", "src_val", "inv_col", "row_perm", "ws"):
+            setattr(self, name, None)

@@ -152,9 +152,9 @@ class NcclGrid:
         (coord, row), = local_rows.items()
         row = np.asarray(row, dtype=np.float64)
         t = torch.as_tensor(row, device=self.device)
-        out = torch.empty((self.rows * self.cols, len(row)), dtype=torch.float64, device=self.device)
-        self.dist.all_gather_into_tensor(out, t, group=self.active_group)
-        full = out.cpu().numpy()
+        outs = [torch.empty_like(t) for _ in range(self.rows * self.cols)]
+        self.dist.all_gather(outs, t, group=self.active_group)
+        full = torch.stack(outs).cpu().numpy()
         return {(r // self.cols, r % self.cols): full[r] for r in range(self.rows * self.cols)}
 
     def gather_vectors(self, local: dict, lengths: dict, device) -> dict:
@@ -163,9 +163,9 @@ class NcclGrid:
         width = max(lengths.values()) if lengths else 0
         buf = torch.zeros(width, dtype=torch.float64, device=self.device)
         buf[: vec.numel()] = vec
-        out = torch.empty((self.rows * self.cols, width), dtype=torch.float64, device=self.device)
-        self.dist.all_gather_into_tensor(out, buf, group=self.active_group)
-        return {(r // self.cols, r % self.cols): out[r, : lengths[(r // self.cols, r % self.cols)]]
+        outs = [torch.empty_like(buf) for _ in range(self.rows * self.cols)]
+        self.dist.all_gather(outs, buf, group=self.active_group)
+        return {(r // self.cols, r % self.cols): outs[r][: lengths[(r // self.cols, r % self.cols)]]
                 for r in range(self.rows * self.cols)}
 
     def barrier(self):

@@ -667,6 +667,104 @@ __global__ void __launch_bounds__(TPB, MINB) sell_kernel(gridlp_csr_t A, const d
   store_partials<Op>(acc, partials);
 }
 
+// Warp-window SELL kernel (variant 9): the window is ONE warp (32 rows,
+// sorted by length inside the slice), so there is no CTA-wide barrier — each
+// warp parks its 32 sums in shared memory, __syncwarp()s and runs the
+// natural-order epilogue of its own 32 rows. CTAs are WPB warps; heavy rows
+// (compact CSR) are tree-summed by the blocks past the windows.
+template <class Op, int U, int WPB, bool EARLY, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) sell32_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
+                                                          double* __restrict__ partials) {
+  __shared__ double sums[WPB][32];
+  __shared__ int have[WPB][32];
+  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  constexpr int NT = WPB * 32;
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  op.prepare();
+  const uint64_t pf = policy_evict_first();
+  const uint64_t pl = policy_evict_last();
+  const int64_t nblk_win = (A.num_windows + WPB - 1) / WPB;
+  if ((int64_t)blockIdx.x >= nblk_win) {
+    const int64_t h = blockIdx.x - nblk_win;
+    const int row = A.heavy_rows[h];
+    const int p0 = A.heavy_ptr[h], p1 = A.heavy_ptr[h + 1];
+    typename Op::Data d{};
+    if (tid == 0) d = op.load(row);
+    double s = 0.0;
+    for (int k = p0 + tid; k < p1; k += NT)
+      s = dadd(s, dmul(ld_stream(A.heavy_vals + k, pf), ld_gather(g + ld_stream(A.heavy_cols + k, pf), pl)));
+    s = warp_sum(s);
+    __shared__ double hs[WPB];
+    if (lane == 0) hs[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = hs[0];
+      for (int w = 1; w < WPB; ++w) t = dadd(t, hs[w]);
+      op.row(row, t, d, acc);
+    }
+  } else {
+    const int64_t slice = (int64_t)blockIdx.x * WPB + warp;
+    if (slice < A.num_windows) {
+      const int64_t r = slice * 32 + lane;
+      const bool in_range = r < A.num_rows;
+      typename Op::Data d{};
+      if (EARLY && in_range) d = op.load(r);
+      have[warp][lane] = 0;
+      const int info = A.lane_info[slice * 32 + lane];
+      __syncwarp();
+      if (info >= 0) {
+        const int len = info >> 8;
+        const int64_t base = (int64_t)A.slice_off[slice] + lane;
+        const int* __restrict__ cp = A.sell_cols + base;
+        const double* __restrict__ vp = A.sell_vals + base;
+        double s = 0.0;
+        for (int j = 0; j < len; j += U) {
+          int c[U];
+          double v[U], x[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool ok = j + u < len;
+            c[u] = ok ? ld_stream(cp + 32 * (j + u), pf) : 0;
+            v[u] = ok ? ld_stream(vp + 32 * (j + u), pf) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) x[u] = (j + u < len) ? ld_gather(g + c[u], pl) : 0.0;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
+        }
+        sums[warp][info & 31] = s;
+        have[warp][info & 31] = 1;
+      }
+      if (!EARLY && in_range) d = op.load(r);
+      __syncwarp();
+      if (in_range && have[warp][lane]) op.row(r, sums[warp][lane], d, acc);
+    }
+  }
+  if constexpr (Op::NRED > 0) {
+    // deterministic: warp tree, then warps in order
+    __shared__ double rs[Op::NRED][WPB];
+#pragma unroll
+    for (int q = 0; q < Op::NRED; ++q) {
+      const double v = warp_sum(acc[q]);
+      if (lane == 0) rs[q][warp] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < Op::NRED; ++q) {
+        double t = rs[q][0];
+        for (int w = 1; w < WPB; ++w) t = dadd(t, rs[q][w]);
+        partials[(int64_t)blockIdx.x * GRIDLP_MAX_RED + q] = t;
+      }
+    }
+  }
+}
+
 // Persistent, TMA-pipelined product + epilogue kernel (variant 0).
 // Each CTA walks its light tiles (round-robin over light_tiles) with a
 // two-slot pipeline: while tile i is gathered and summed, the TMA unit
@@ -846,10 +944,11 @@ int check_csr(const gridlp_csr_t* A) {
     return fail(GRIDLP_ERR_ARG, "tile_nnz_cap must be a multiple of 8 in [64, TILE_NNZ_CAP]");
   if (A->exact_row_max < 0 || A->exact_row_max > A->tile_nnz_cap / 2)
     return fail(GRIDLP_ERR_ARG, "exact_row_max must be in [0, tile_nnz_cap/2]");
-  if (A->variant < 0 || A->variant > 8) return fail(GRIDLP_ERR_ARG, "unknown kernel variant");
+  if (A->variant < 0 || A->variant > 10) return fail(GRIDLP_ERR_ARG, "unknown kernel variant");
   if (A->variant >= 6) {
+    const int win = A->variant >= 9 ? 32 : TPB;
     if (A->num_rows > 0 &&
-        (!A->slice_off || !A->lane_info || A->num_windows != (A->num_rows + TPB - 1) / TPB))
+        (!A->slice_off || !A->lane_info || A->num_windows != (A->num_rows + win - 1) / win))
       return fail(GRIDLP_ERR_ARG, "SELL layout missing or inconsistent");
     if (A->num_heavy_rows > 0 && (!A->heavy_rows || !A->heavy_ptr || !A->heavy_cols || !A->heavy_vals))
       return fail(GRIDLP_ERR_ARG, "missing heavy-row CSR");
@@ -904,7 +1003,8 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
     if (src->A->num_rows > 0 && src->A->nnz > 0 && !src->gather)
       return fail(GRIDLP_ERR_ARG, std::string(name) + ": missing gather vector");
     slots = src->A->num_rows <= 0 ? 0
-            : (src->A->variant >= 6 ? src->A->num_windows + src->A->num_heavy_rows : src->A->num_tiles);
+            : (src->A->variant >= 9 ? (src->A->num_windows + 1) / 2 + src->A->num_heavy_rows
+               : src->A->variant >= 6 ? src->A->num_windows + src->A->num_heavy_rows : src->A->num_tiles);
   } else {
     if (src->nparts < 0 || src->nparts > GRIDLP_MAX_PARTS)
       return fail(GRIDLP_ERR_ARG, std::string(name) + ": nparts out of range");
@@ -940,6 +1040,15 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
         case 3: tile_kernel_tma<Op, 4, 8><<<nb, TPB, sm_tma, s>>>(M, src->gather, op, partials); break;
         case 4: tile_kernel_tma<Op, 8, 5><<<nb, TPB, sm_tma, s>>>(M, src->gather, op, partials); break;
         case 5: tile_kernel<Op, 4, 6, false><<<nb, TPB, sm_prod, s>>>(M, src->gather, op, partials); break;
+        case 9: case 10: {
+          const int64_t nwb = (M.num_windows + 1) / 2;
+          const unsigned nb9 = (unsigned)(nwb + M.num_heavy_rows);
+          slots = nb9;
+          if (!nb9) break;
+          if (M.variant == 9) sell32_kernel<Op, 4, 2, false, 32><<<nb9, 64, 0, s>>>(M, src->gather, op, partials);
+          else sell32_kernel<Op, 4, 2, true, 21><<<nb9, 64, 0, s>>>(M, src->gather, op, partials);
+          break;
+        }
         case 6: case 7: case 8: {
           const unsigned nsell = (unsigned)(M.num_windows + M.num_heavy_rows);
           slots = nsell;
@@ -985,6 +1094,9 @@ int gridlp_abi_version(void) { return GRIDLP_ABI_VERSION; }
 
 const char* gridlp_last_error(void) { return g_err.c_str(); }
 
+// not part of the header: lets the setup translation unit share the error slot
+void gridlp_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
+
 int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes) {
   int v = 0;
   cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -998,6 +1110,7 @@ int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes) {
 
 int64_t gridlp_op_slots(const gridlp_src_t* src) {
   if (!src) return 0;
+  if (src->A && src->A->variant >= 9) return (src->A->num_windows + 1) / 2 + src->A->num_heavy_rows;
   if (src->A && src->A->variant >= 6) return src->A->num_windows + src->A->num_heavy_rows;
   if (src->A) return src->A->num_rows > 0 ? src->A->num_tiles : 0;
   return src->num_rows > 0 ? rows_blocks(src->num_rows) : 0;

@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .blocks import DEFAULT_EXACT_ROW_MAX, DeviceCsr, permute_matrix, slice_blocks, transpose
+from .blocks import DEFAULT_EXACT_ROW_MAX, DeviceCsr, DeviceSetup, permute_matrix, slice_blocks, transpose
 from .comm import Ledger, asc_sum
 from .ops import Fused, Parts
 
@@ -67,7 +67,8 @@ class EngineOptions:
     time_limit_seconds: float | None = None
     exact_row_max: int = DEFAULT_EXACT_ROW_MAX
     tile_cap: int = 2048
-    kernel_variant: int = 6
+    kernel_variant: int = 9
+    device_setup: bool = True
     use_graphs: bool = True
     graph_chunk: int = 128
 
@@ -191,9 +192,20 @@ class PdhgEngine:
     # ------------------------------------------------------------ setup
     def _build(self, problem):
         lay, dev = self.layout, self.device
-        pa = permute_matrix(problem.matrix, lay)
-        host_blocks = slice_blocks(pa, lay)
-        self.per_device_nnz = [host_blocks[c].nnz for c in lay.topology.coords()]
+        on_device = dev.type == "cuda" and self.opts.kernel_variant >= 9 and self.opts.device_setup
+        tm = self.timings
+        if on_device:
+            t0 = time.perf_counter()
+            setup = DeviceSetup(problem, lay, dev)
+            torch.cuda.synchronize(dev)
+            tm["setup_upload_s"] = time.perf_counter() - t0
+            self.setup_h2d_bytes = setup.h2d_bytes
+            host_blocks = None
+        else:
+            pa = permute_matrix(problem.matrix, lay)
+            host_blocks = slice_blocks(pa, lay)
+            self.per_device_nnz = [host_blocks[c].nnz for c in lay.topology.coords()]
+            self.setup_h2d_bytes = 0
         cp, rp = lay.perm.col_perm, lay.perm.row_perm
         f64 = dict(dtype=torch.float64, device=dev)
         obj = np.asarray(problem.objective, np.float64)[cp]
@@ -219,16 +231,48 @@ class PdhgEngine:
             t = lambda a: torch.as_tensor(np.ascontiguousarray(a[r0:r1]), **f64)  # noqa: E731
             self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
+        kw = dict(exact_row_max=self.opts.exact_row_max, tile_cap=self.opts.tile_cap,
+                  variant=self.opts.kernel_variant)
+        nnz_of = {}
         for (i, j) in local:
-            hb = host_blocks[(i, j)]
-            kw = dict(exact_row_max=self.opts.exact_row_max, tile_cap=self.opts.tile_cap,
-                      variant=self.opts.kernel_variant)
-            self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(transpose(hb), dev, **kw))
-        del host_blocks, pa
+            if on_device:
+                t0 = time.perf_counter()
+                a = setup.block(i, j)
+                torch.cuda.synchronize(dev)
+                t1 = time.perf_counter()
+                at = setup.transpose(a)
+                torch.cuda.synchronize(dev)
+                t2 = time.perf_counter()
+                sa = setup.sell(a, self.opts.exact_row_max)
+                sa["shape"] = (a.num_rows, a.num_cols, a.nnz)
+                st = setup.sell(at, self.opts.exact_row_max)
+                st["shape"] = (at.num_rows, at.num_cols, at.nnz)
+                torch.cuda.synchronize(dev)
+                t3 = time.perf_counter()
+                tm["setup_extract_s"] = tm.get("setup_extract_s", 0.0) + t1 - t0
+                tm["setup_transpose_s"] = tm.get("setup_transpose_s", 0.0) + t2 - t1
+                tm["setup_sell_s"] = tm.get("setup_sell_s", 0.0) + t3 - t2
+                del a, at
+                self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(sa, dev, **kw), DeviceCsr(st, dev, **kw))
+                nnz_of[(i, j)] = self.blocks[(i, j)].A.nnz
+            else:
+                hb = host_blocks[(i, j)]
+                self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(transpose(hb), dev, **kw))
+        if on_device:
+            setup.release()
+            del setup
+            torch.cuda.empty_cache()
+            coords = lay.topology.coords()
+            self.per_device_nnz = [nnz_of.get(c, -1) for c in coords] if self.comm.kind == "virtual" else None
+        del host_blocks
         tensors = [t for b in self.blocks.values() for d in (b.A, b.AT) for t in d.tensors()]
         tensors += [t for c in self.cols.values() for t in (c.c, c.lo, c.hi)]
         tensors += [t for r in self.rows.values() for t in (r.lo, r.hi)]
         self.h2d_bytes = int(sum(t.numel() * t.element_size() for t in tensors))
+        if self.setup_h2d_bytes:      # blocks were built on the device from the uploaded CSR
+            self.h2d_bytes = int(self.setup_h2d_bytes + sum(
+                t.numel() * t.element_size() for c in self.cols.values() for t in (c.c, c.lo, c.hi))
+                + sum(t.numel() * t.element_size() for r in self.rows.values() for t in (r.lo, r.hi)))
         self.passes = 0
 
     def _assign_slots(self):

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libgridlp_b200.so"
-SOURCES = [PKG / "csrc" / "gridlp_b200.cu"]
+SOURCES = [PKG / "csrc" / "gridlp_b200.cu", PKG / "csrc" / "gridlp_setup.cu"]
 HEADER = ROOT / "include" / "gridlp_b200.h"
 
 MAX_RED = 8
@@ -91,6 +91,14 @@ SIGNATURES = {
     "gridlp_op_div": ([_P, _P, c_int64, c_double, _P], c_int),
     "gridlp_op_init_primal": ([POINTER(Primal), _P], c_int),
     "gridlp_op_step_advance": ([_P, c_int64, _P], c_int),
+    "gridlp_setup_workspace_bytes": ([c_int64, c_int64], ctypes.c_size_t),
+    "gridlp_block_count": ([_P, _P, _P, c_int64, _P, c_int32, c_int32, _P, _P, ctypes.c_size_t, _P], c_int),
+    "gridlp_block_fill": ([_P, _P, _P, _P, c_int64, _P, c_int32, c_int32, _P, c_int64, _P, _P, _P,
+                           ctypes.c_size_t, _P], c_int),
+    "gridlp_csr_transpose": ([_P, _P, _P, c_int64, c_int64, c_int64, _P, _P, _P, _P, ctypes.c_size_t, _P], c_int),
+    "gridlp_sell_plan": ([_P, c_int64, c_int32, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], c_int),
+    "gridlp_sell_fill": ([_P, _P, _P, c_int64, c_int32, _P, _P, _P, _P, c_int64, _P, _P, c_int64, _P, _P, _P],
+                         c_int),
 }
 
 

@@ -57,7 +57,7 @@ def test_library_is_loaded_from_tree():
     assert sm >= 100 and l2 > 0
 
 
-VARIANTS = [0, 1, 2, 3, 4, 5, 6]
+VARIANTS = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10]
 
 
 class TestProducts:
