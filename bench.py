@@ -146,6 +146,72 @@ def iteration_bytes(engine) -> dict:
         out["K1"] += 12 * nnz + 4 * (n + 1) + 8 * m + 56 * n
         out["K2"] += 12 * nnz + 4 * (m + 1) + 8 * n + 40 * m
     out["iteration"] = out["K1"] + out["K2"]
+    # L1->L2 requests: one 32-byte sector request per gathered element (random
+    # columns: no two lanes of a warp share a 128-byte line) plus one request
+    # per 128-byte line of every streamed array
+    gathers = sum(2 * blk.A.nnz for blk in engine.blocks.values())
+    vec_once = sum(8 * (blk.A.num_rows + blk.A.num_cols) for blk in engine.blocks.values())
+    out["requests"] = gathers + (out["iteration"] - vec_once) // 128
+    return out
+
+
+# Random 8-byte gathers from an L2-resident vector on this B200: 255 G/s
+# (tools/microbench.cu, profiles/r1/microbench_gather.log) — one L1->L2
+# sector request per gather, the port ncu shows 77-81 % busy in K1/K2
+# (profiles/r1/ncu_sell32_full.md).
+GATHER_CEILING_PER_S = 255e9
+
+
+def spmv_compare(problem, device, reps=20) -> dict:
+    """SpMV-only HBM GB/s: y = A·x over the instance's own CSR,
+    our SELL-32 product (gridlp_op_store, bit-identical to scipy) against
+    cuSPARSE csrmv through torch.sparse (FP64, int32 indices) on the same
+    matrix and vector; CUDA events on the launching stream, L2 not flushed
+    (A is 240 MB, > L2). Bytes per product: 12 nnz + 4(rows+1) + 8 cols +
+    8 rows."""
+    import numpy as np
+    import torch
+
+    from paper_2601_07628_b200.blocks import DeviceCsr, HostCsr
+    from paper_2601_07628_b200.ops import CudaOps, Fused
+
+    M = problem.matrix
+    m, n = int(M.num_rows), int(M.num_cols)
+    h = HostCsr(m, n, np.asarray(M.row_offsets, np.int64), np.asarray(M.col_indices, np.int64),
+                np.asarray(M.values, np.float64))
+    A = DeviceCsr(h, device)
+    ops = CudaOps(device, A.slots() + 8, 1)
+    x = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).to(device)
+    ours = torch.empty(m, dtype=torch.float64, device=device)
+    T = torch.sparse_csr_tensor(torch.from_numpy(h.ptr.astype(np.int32)), torch.from_numpy(h.col.astype(np.int32)),
+                                torch.from_numpy(h.val), size=(m, n)).to(device)
+    xs = x.reshape(n, 1)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        evs = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return sorted(a.elapsed_time(b) for a, b in evs)[reps // 2] * 1e-3
+
+    t_ours = timed(lambda: ops.store(Fused(A, x), ours))
+    lib = {}
+    t_lib = timed(lambda: lib.__setitem__("y", torch.mm(T, xs)))
+    same = bool(torch.equal(lib["y"].reshape(m), ours))
+    bytes_ = 12 * h.nnz + 4 * (m + 1) + 8 * n + 8 * m
+    out = {"rows": m, "cols": n, "nnz": h.nnz, "bytes_per_product": bytes_,
+           "ours_us": t_ours * 1e6, "ours_GBs": bytes_ / t_ours / 1e9,
+           "cusparse_us": t_lib * 1e6, "cusparse_GBs": bytes_ / t_lib / 1e9,
+           "speedup_vs_cusparse": t_lib / t_ours, "cusparse_bitwise_equal_ours": same,
+           "median_of": reps}
+    del A, ops, T
+    torch.cuda.empty_cache()
     return out
 
 
@@ -297,10 +363,12 @@ def run_ours(args, rank, world, local_rank):
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(args.config)
+        tr = json.loads(tf.read_text()).get(args.config)
+        traffic = tr["bytes_per_iteration"] if isinstance(tr, dict) else tr
     restarts = engine._s["epoch"]
     del engine
     torch.cuda.empty_cache()
+    spmv = spmv_compare(p, dev) if world == 1 and not args.no_spmv else None
 
     # e2e through the public API, host arrays in, host arrays out
     e2e = None
@@ -347,9 +415,17 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": "fused PDHG iteration (K1 A^T y+primal/Halpern, K2 A x_bar+dual/Halpern)",
                      "bytes_per_launch": bytes_["iteration"], "seconds_per_launch": t_iter,
                      "peak_source": peak_src,
-                     "frac_of_8TBs": achieved / 8000.0},
+                     "frac_of_8TBs": achieved / 8000.0,
+                     "request_bound": {
+                         "requests_per_iteration": bytes_["requests"],
+                         "ceiling_requests_per_s": GATHER_CEILING_PER_S,
+                         "seconds_at_ceiling": bytes_["requests"] / GATHER_CEILING_PER_S,
+                         "frac": bytes_["requests"] / GATHER_CEILING_PER_S / t_iter,
+                         "note": "random FP64 gathers (2 nnz per iteration) cost one L1->L2 request each; "
+                                 "ceiling measured by tools/microbench.cu"}},
         "kernels": {k: {"seconds": ktimes[k], "bytes": bytes_[k], "GB/s": bytes_[k] / ktimes[k] / 1e9}
                     for k in ktimes},
+        "spmv": spmv,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -367,6 +443,7 @@ def main():
     ap.add_argument("--config", choices=tuple(CONFIGS), default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-spmv", action="store_true", help="skip the SpMV-only comparison with cuSPARSE")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)
     ap.add_argument("--ref-sample-iters", type=int, default=4)
     ap.add_argument("--variant", type=int, default=9, help="product kernel variant (0 pipelined, 1 per-tile)")
