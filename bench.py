@@ -319,8 +319,7 @@ def run_ours(args, rank, world, local_rank):
         base = dict(n_procs=1)
     cfg = SolverConfig(tolerance=1e-300, max_iterations=10**12, seed=0, **base)
     t0 = time.perf_counter()
-    engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides={
-        "kernel_variant": args.variant, "tile_cap": args.tile_cap})
+    engine, layout, eta, omega, tim = prepare(p, cfg, device=dev)
     log(f"[bench] rank {rank}: setup {time.perf_counter() - t0:.1f}s {tim}")
     R, C = layout.topology.rows, layout.topology.cols
     engine.start(eta, omega)
@@ -446,8 +445,6 @@ def main():
     ap.add_argument("--no-spmv", action="store_true", help="skip the SpMV-only comparison with cuSPARSE")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)
     ap.add_argument("--ref-sample-iters", type=int, default=4)
-    ap.add_argument("--variant", type=int, default=9, help="product kernel variant (0 pipelined, 1 per-tile)")
-    ap.add_argument("--tile-cap", type=int, default=2048)
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")

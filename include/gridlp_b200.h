@@ -51,62 +51,54 @@ enum gridlp_status {
 #define GRIDLP_MAX_RED 8
 /* Max partial products summed by an unfused epilogue (grid rows/cols). */
 #define GRIDLP_MAX_PARTS 16
-/* Nonzeros a light tile may hold (shared-memory product buffer). */
-#define GRIDLP_TILE_NNZ_CAP 4096
-/* Rows a light tile may hold (one thread per row in the row-sum phase). */
-#define GRIDLP_TILE_ROWS 256
+/* Entries per chunk of a heavy row (one CTA sums one chunk). */
+#define GRIDLP_HEAVY_CHUNK 2048
+/* Largest exact_row_max accepted (rows up to this length are summed
+ * sequentially, bit-identical to the reference). */
+#define GRIDLP_EXACT_ROW_MAX_LIMIT 4096
 
 /*
- * One device-resident block A_ij (or its stored transpose) in tiled CSR.
+ * One device-resident block A_ij (or its stored transpose) in SELL-32.
  * Replaces SparseMatrix (lp_model.py:40-150) for a LocalBlock matrix /
- * matrix_transpose (partition.py:93-122): int32 column indices (12 B/nnz
- * instead of the reference's 16) and a tile directory. Tiles are row
- * ranges [tile_ptr[t], tile_ptr[t+1]) that either hold at most
- * GRIDLP_TILE_ROWS rows and tile_nnz_cap nonzeros ("light"), or a single
- * row longer than exact_row_max ("heavy", tree-summed). light_tiles /
- * heavy_tiles list the tile ids of each kind.
- * col_idx and values must stay readable 4 elements past nnz (the staging
- * copies move whole 16-byte granules).
+ * matrix_transpose (partition.py:93-122): int32 column indices, FP64
+ * values — 12 B/nnz instead of the reference's 16.
+ *
+ * Light rows (length <= exact_row_max): rows are cut into slices of 32
+ * consecutive rows; inside a slice the lanes are ordered by row length
+ * (descending, stable) and entry j of lane l is stored at
+ * sell_*[slice_off[s] + 32 j + l] in the row's original entry order, so a
+ * warp step reads 32 consecutive values and column indices.
+ * lane_info[32 s + l] = (row length << 8) | (row & 31), or -1 for an empty
+ * lane (heavy row or past the end).
+ *
+ * Heavy rows (length > exact_row_max): a compact CSR (heavy_rows /
+ * heavy_ptr / heavy_cols / heavy_vals) cut into chunks of
+ * GRIDLP_HEAVY_CHUNK entries: chunks chunk_first[h] .. chunk_first[h+1]-1
+ * belong to heavy row h and chunk_row[c] = h. chunk_sums (one double per
+ * chunk) and chunk_done (one int per heavy row, zero before the first
+ * launch, left zero by every launch) are caller-owned scratch; products
+ * over the same block must be stream-ordered.
  */
 typedef struct gridlp_csr {
   int64_t num_rows;
   int64_t num_cols;
-  int64_t nnz;
-  const int32_t* row_ptr;     /* [num_rows+1], nnz < 2^31 */
-  const int32_t* col_idx;     /* [nnz(+4)] strictly increasing within a row */
-  const double* values;       /* [nnz(+4)] */
-  const int32_t* tile_ptr;    /* [num_tiles+1] */
-  int64_t num_tiles;
-  const int32_t* light_tiles; /* [num_light] */
-  int64_t num_light;
-  const int32_t* heavy_tiles; /* [num_heavy] */
-  int64_t num_heavy;
-  /* SELL-32 windows (variant 6): rows are taken in windows of 256; the
-   * light rows of a window are sorted by length (descending, stable) into 8
-   * slices of 32 lanes; slice s stores its entry j of lane l at
-   * sell_*[slice_off[s] + 32 j + l] (column-major inside the slice, so a
-   * warp reads 32 consecutive values per step), in the row's original entry
-   * order. lane_info[32 s + l] = (row length << 8) | (row & (window-1)), or -1 for
-   * an empty lane. Rows longer than exact_row_max are kept as a compact CSR
-   * (heavy_rows / heavy_ptr / heavy_cols / heavy_vals) and tree-summed. */
+  int64_t nnz;                /* < 2^31 per block */
   const double* sell_vals;    /* [slice_off[num_slices]] */
   const int32_t* sell_cols;
-  const int32_t* slice_off;   /* [8 * num_windows + 1] */
-  const int32_t* lane_info;   /* [256 * num_windows] */
-  int64_t num_windows;
-  const int32_t* heavy_rows;  /* [num_heavy_rows] */
+  const int32_t* slice_off;   /* [num_slices + 1] */
+  const int32_t* lane_info;   /* [32 * num_slices] */
+  int64_t num_slices;         /* ceil(num_rows / 32) */
+  const int32_t* heavy_rows;  /* [num_heavy_rows] ascending */
   const int32_t* heavy_ptr;   /* [num_heavy_rows + 1] */
   const int32_t* heavy_cols;
   const double* heavy_vals;
   int64_t num_heavy_rows;
-  int32_t exact_row_max;      /* <= tile_nnz_cap/2 */
-  int32_t tile_nnz_cap;       /* <= GRIDLP_TILE_NNZ_CAP */
-  int32_t variant;            /* product kernel: 0 persistent TMA-pipelined; 1/2/5 one CTA
-                                 per tile (register-staged, 5/8/6 CTAs per SM); 3/4 one CTA
-                                 per tile with TMA-staged matrix stream (8/5 CTAs per SM);
-                                 6/7/8 SELL-32 windows of 256 rows, register row sums, no shared
-                                 staging (8/6/5 CTAs per SM); 9/10 SELL-32 windows of one warp
-                                 (32 rows), warp-synchronous, 64-thread CTAs */
+  const int32_t* chunk_first; /* [num_heavy_rows + 1] */
+  const int32_t* chunk_row;   /* [num_chunks] */
+  int64_t num_chunks;
+  double* chunk_sums;         /* [num_chunks] scratch */
+  int32_t* chunk_done;        /* [num_heavy_rows] scratch, zero-initialised */
+  int32_t exact_row_max;      /* <= GRIDLP_EXACT_ROW_MAX_LIMIT */
   int32_t reserved;
 } gridlp_csr_t;
 

@@ -1,11 +1,11 @@
-"""Per-device blocks: permutation, 2D slicing, stored transpose, tiling, and
-upload into HBM.
+"""Per-device blocks: permutation, 2D slicing, stored transpose, SELL-32
+layout, and upload into HBM.
 
 Reference: permute_problem / distribute (partition.py:262-319), slice_block
 and transpose (sparse_kernels.py:27-58). The reference builds CSR with int64
-indices (16 B/nnz); a device block here stores int32 row pointers and column
-indices with FP64 values (12 B/nnz per orientation) plus a tile directory
-(include/gridlp_b200.h, gridlp_csr_t).
+indices (16 B/nnz); a device block here is SELL-32 with int32 column indices
+and FP64 values (12 B/nnz per orientation) plus a chunked CSR of its heavy
+rows (include/gridlp_b200.h, gridlp_csr_t).
 """
 
 from __future__ import annotations
@@ -19,7 +19,6 @@ import torch
 from . import native
 
 DEFAULT_EXACT_ROW_MAX = 512
-DEFAULT_VARIANT = 9
 
 
 @dataclass
@@ -87,62 +86,26 @@ def transpose(a: HostCsr) -> HostCsr:
     return HostCsr(a.num_cols, a.num_rows, ptr, rows[order], a.val[order])
 
 
-def build_tiles(ptr: np.ndarray, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
-                cap: int = native.TILE_NNZ_CAP, max_rows: int = native.TILE_ROWS) -> np.ndarray:
-    """Tile directory for the product kernel.
-
-    Light tiles group the rows whose first nonzero falls in the same window
-    of (cap - exact_row_max) nonzeros, so a light tile never exceeds `cap`
-    nonzeros, and are split further to at most `max_rows` rows. Every row
-    longer than exact_row_max is isolated in its own (heavy) tile.
-    """
-    ptr = np.asarray(ptr, dtype=np.int64)
-    m = len(ptr) - 1
-    if m <= 0:
-        return np.zeros(1, dtype=np.int32)
-    if not (0 <= exact_row_max <= cap // 2):
-        raise ValueError("exact_row_max must be in [0, cap/2]")
-    seg = cap - exact_row_max
-    lens = np.diff(ptr)
-    heavy = lens > exact_row_max
-    win = ptr[:-1] // seg
-    start = np.zeros(m, dtype=bool)
-    start[0] = True
-    start[1:] = win[1:] != win[:-1]
-    start |= heavy
-    start[1:] |= heavy[:-1]
-    run = np.cumsum(start) - 1
-    first = np.flatnonzero(start)
-    pos = np.arange(m, dtype=np.int64) - first[run]
-    start |= (pos % max_rows) == 0
-    tiles = np.concatenate([np.flatnonzero(start), [m]]).astype(np.int64)
-    if tiles[-1] >= 2 ** 31:
-        raise ValueError("too many rows for int32 tiles")
-    return tiles.astype(np.int32)
-
-
-SELL_WINDOW = 256
-
-
-def build_sell(host: HostCsr, exact_row_max: int, window: int = SELL_WINDOW):
-    """SELL-32 layout of include/gridlp_b200.h (variant 6): per 256-row
-    window the light rows sorted by length (descending, stable) into 32-lane
-    slices stored column-major; heavy rows as a compact CSR."""
+def build_sell(host: HostCsr, exact_row_max: int):
+    """SELL-32 layout of include/gridlp_b200.h on the host (the device build,
+    DeviceSetup.sell, must produce the same arrays): per 32-row slice the
+    light rows sorted by length (descending, stable), stored column-major;
+    heavy rows as a compact CSR."""
     ptr, m = host.ptr, host.num_rows
     lens = np.diff(ptr)
     heavy = lens > exact_row_max
-    nw = -(-m // window) if m else 0
+    ns = -(-m // 32) if m else 0
     eff = np.where(heavy, -1, lens)
-    win = np.arange(m, dtype=np.int64) // window
-    order = np.lexsort((-eff, win))             # window-major, longest first, heavy last
-    info = np.full(nw * window, -1, dtype=np.int64)
+    sl = np.arange(m, dtype=np.int64) // 32
+    order = np.lexsort((-eff, sl))             # slice-major, longest first, heavy last
+    info = np.full(ns * 32, -1, dtype=np.int64)
     slen = eff[order]
     light = slen >= 0
     pos = np.flatnonzero(light)
-    info[pos] = (slen[pos] << 8) | (order[pos] & (window - 1))
-    lane_len = np.zeros(nw * window, dtype=np.int64)
+    info[pos] = (slen[pos] << 8) | (order[pos] & 31)
+    lane_len = np.zeros(ns * 32, dtype=np.int64)
     lane_len[pos] = slen[pos]
-    slice_len = lane_len.reshape(-1, 32).max(axis=1) if nw else np.zeros(0, np.int64)
+    slice_len = lane_len.reshape(-1, 32).max(axis=1) if ns else np.zeros(0, np.int64)
     slice_off = np.concatenate([[0], np.cumsum(32 * slice_len)]).astype(np.int64)
     total = int(slice_off[-1])
     if total >= 2 ** 31 - 64:
@@ -170,90 +133,71 @@ def build_sell(host: HostCsr, exact_row_max: int, window: int = SELL_WINDOW):
     else:
         hcols, hvals = np.zeros(4, np.int32), np.zeros(4)
     return dict(vals=vals, cols=cols, slice_off=slice_off.astype(np.int32),
-                lane_info=info.astype(np.int32), num_windows=nw, heavy_rows=hrows.astype(np.int32),
+                lane_info=info.astype(np.int32), num_slices=ns, heavy_rows=hrows.astype(np.int32),
                 heavy_ptr=hptr.astype(np.int32), heavy_cols=hcols, heavy_vals=hvals)
+
+
+def chunk_directory(heavy_ptr: torch.Tensor):
+    """Cut each heavy row into GRIDLP_HEAVY_CHUNK-entry chunks: returns
+    (chunk_first [nh+1], chunk_row [num_chunks]) as int32 tensors on the
+    heavy_ptr's device."""
+    hp = heavy_ptr.to(torch.int64)
+    nh = hp.numel() - 1
+    lens = hp[1:] - hp[:-1]
+    nch = (lens + native.HEAVY_CHUNK - 1) // native.HEAVY_CHUNK
+    first = torch.zeros(nh + 1, dtype=torch.int64, device=hp.device)
+    if nh:
+        first[1:] = torch.cumsum(nch, 0)
+    rows = torch.repeat_interleave(torch.arange(nh, device=hp.device), nch) if nh else first[:0]
+    if int(first[-1]) >= 2 ** 31:
+        raise ValueError("too many heavy-row chunks for int32")
+    return first.to(torch.int32), rows.to(torch.int32)
 
 
 class DeviceCsr:
     """One block resident in HBM; `.struct` is its gridlp_csr_t.
 
-    variant 9 (default; 10 = early epilogue loads): SELL-32 with one-warp
-    windows; variants 6-8: SELL-32 with 256-row windows — only the SELL
-    arrays and the heavy-row CSR live in HBM, built either on the host
-    (build_sell, from a HostCsr) or on the device (DeviceSetup.sell, passed
-    as a dict). Variants 0-5: tiled CSR (tile directory + int32 CSR), kept
-    for A/B measurement."""
+    Built from a HostCsr (host SELL build, build_sell) or from the dict the
+    device setup returns (DeviceSetup.sell). Only the SELL arrays, the heavy
+    rows' chunked CSR and the chunk scratch live in HBM."""
 
-    PAD = 4   # the TMA staging copies read whole 16-byte granules
-
-    def __init__(self, host: HostCsr, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
-                 tile_cap: int = native.DEFAULT_TILE_CAP, variant: int = DEFAULT_VARIANT):
-        if isinstance(host, dict):
-            shape = host["shape"]
-            self.num_rows, self.num_cols, self.nnz = shape
-            lens = np.zeros(0, dtype=np.int64)
-            self.heavy_rows = int(len(host["heavy_rows"]))
+    def __init__(self, host, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX):
+        if not 0 <= exact_row_max <= native.EXACT_ROW_MAX_LIMIT:
+            raise ValueError(f"exact_row_max must be in [0, {native.EXACT_ROW_MAX_LIMIT}]")
+        if isinstance(host, dict):      # SELL arrays already built on the device (DeviceSetup.sell)
+            self.num_rows, self.num_cols, self.nnz = host["shape"]
+            sd = host
         else:
             if host.nnz >= 2 ** 31 - 64:
                 raise ValueError("block nnz must be < 2^31 (int32 offsets)")
             self.num_rows, self.num_cols, self.nnz = host.num_rows, host.num_cols, host.nnz
-            lens = np.diff(host.ptr)
-            self.heavy_rows = int(np.count_nonzero(lens > exact_row_max))
-        self.exact_row_max, self.tile_cap, self.variant = exact_row_max, tile_cap, variant
+            sd = build_sell(host, exact_row_max)
+        self.exact_row_max = exact_row_max
         # the host copy is kept only for CPU-resident blocks (the CPU test double)
-        self.host = host if torch.device(device).type == "cpu" else None
+        self.host = host if torch.device(device).type == "cpu" and not isinstance(host, dict) else None
         self.dev = {}
-        up = lambda k, a: self.dev.__setitem__(k, torch.from_numpy(np.ascontiguousarray(a)).to(device))  # noqa: E731
-        ptr = lambda k: self.dev[k].data_ptr() if k in self.dev and self.dev[k].numel() else None  # noqa: E731
-        csr_args = [None, None, None, None, 0, None, 0, None, 0]
-        sell_args = [None] * 4 + [0] + [None] * 4 + [0]
-        self.num_tiles = 0
-        if variant >= 6:
-            if isinstance(host, dict):      # SELL arrays already built on the device (DeviceSetup.sell)
-                sd = host
-                for k in ("vals", "cols", "slice_off", "lane_info", "heavy_rows", "heavy_ptr", "heavy_cols",
-                          "heavy_vals"):
-                    self.dev["sell_" + k] = sd[k]
-            else:
-                sd = build_sell(host, exact_row_max, window=32 if variant >= 9 else SELL_WINDOW)
-                for k in ("vals", "cols", "slice_off", "lane_info", "heavy_rows", "heavy_ptr", "heavy_cols",
-                          "heavy_vals"):
-                    up("sell_" + k, sd[k])
-            sell_args = [ptr("sell_vals"), ptr("sell_cols"), ptr("sell_slice_off"), ptr("sell_lane_info"),
-                         sd["num_windows"], ptr("sell_heavy_rows"), ptr("sell_heavy_ptr"),
-                         ptr("sell_heavy_cols"), ptr("sell_heavy_vals"), len(sd["heavy_rows"])]
-            self.num_windows = sd["num_windows"]
-        else:
-            tiles = build_tiles(host.ptr, exact_row_max, cap=tile_cap)
-            self.num_tiles = max(len(tiles) - 1, 0)
-            t_rows = np.diff(tiles.astype(np.int64))
-            first = tiles[:-1].astype(np.int64)
-            heavy = (t_rows == 1) & (lens[first] > exact_row_max) if self.num_tiles else np.zeros(0, bool)
-            col = np.zeros(host.nnz + self.PAD, dtype=np.int32)
-            col[: host.nnz] = host.col
-            val = np.zeros(host.nnz + self.PAD, dtype=np.float64)
-            val[: host.nnz] = host.val
-            up("row_ptr", host.ptr.astype(np.int32))
-            up("col_idx", col)
-            up("values", val)
-            up("tile_ptr", tiles)
-            up("light_tiles", np.flatnonzero(~heavy).astype(np.int32))
-            up("heavy_tiles", np.flatnonzero(heavy).astype(np.int32))
-            csr_args = [ptr("row_ptr"), ptr("col_idx"), ptr("values"), ptr("tile_ptr"), self.num_tiles,
-                        ptr("light_tiles"), int(np.count_nonzero(~heavy)), ptr("heavy_tiles"),
-                        int(np.count_nonzero(heavy))]
-        self.struct = native.Csr(self.num_rows, self.num_cols, self.nnz, *csr_args, *sell_args,
-                                 exact_row_max, tile_cap, variant, 0)
+        for k in ("vals", "cols", "slice_off", "lane_info", "heavy_rows", "heavy_ptr", "heavy_cols", "heavy_vals"):
+            a = sd[k]
+            self.dev[k] = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        self.heavy_rows = int(self.dev["heavy_rows"].numel())
+        self.dev["chunk_first"], self.dev["chunk_row"] = chunk_directory(self.dev["heavy_ptr"])
+        self.num_chunks = int(self.dev["chunk_row"].numel())
+        self.dev["chunk_sums"] = torch.zeros(max(self.num_chunks, 1), dtype=torch.float64, device=device)
+        self.dev["chunk_done"] = torch.zeros(max(self.heavy_rows, 1), dtype=torch.int32, device=device)
+        self.num_slices = int(sd["num_slices"])
+        ptr = lambda k: self.dev[k].data_ptr() if self.dev[k].numel() else None  # noqa: E731
+        self.struct = native.Csr(self.num_rows, self.num_cols, self.nnz,
+                                 ptr("vals"), ptr("cols"), ptr("slice_off"), ptr("lane_info"), self.num_slices,
+                                 ptr("heavy_rows"), ptr("heavy_ptr"), ptr("heavy_cols"), ptr("heavy_vals"),
+                                 self.heavy_rows, ptr("chunk_first"), ptr("chunk_row") if self.num_chunks else None,
+                                 self.num_chunks, ptr("chunk_sums"), ptr("chunk_done"), exact_row_max, 0)
 
     def tensors(self):
         return tuple(self.dev.values())
 
     def slots(self) -> int:
-        if self.variant >= 9:
-            return (self.num_windows + 1) // 2 + self.heavy_rows
-        if self.variant >= 6:
-            return self.num_windows + self.heavy_rows
-        return self.num_tiles
+        """CTAs of one product (= reduction slots): heavy chunks + slice pairs."""
+        return self.num_chunks + (self.num_slices + 1) // 2 if self.num_rows else 0
 
     def src(self, gather: torch.Tensor | None) -> native.Src:
         s = native.Src()
@@ -363,7 +307,7 @@ class DeviceSetup:
         return DeviceCsrArrays(a.num_cols, a.num_rows, a.nnz, ptr, col, val)
 
     def sell(self, a: DeviceCsrArrays, exact_row_max: int) -> dict:
-        """SELL-32 warp-window arrays (variants 9/10) built on the device."""
+        """SELL-32 arrays built on the device (same as build_sell)."""
         dev, m = self.device, a.num_rows
         ns = (m + 31) // 32
         i32 = dict(dtype=torch.int32, device=dev)
@@ -386,7 +330,7 @@ class DeviceSetup:
                       sell_col.data_ptr(), sell_val.data_ptr(), total, hcol.data_ptr(), hval.data_ptr(),
                       self._stream())
         return dict(vals=sell_val, cols=sell_col, slice_off=slice_off, lane_info=lane_info,
-                    num_windows=ns, heavy_rows=heavy_rows[:nh].clone() if nh else heavy_rows[:0],
+                    num_slices=ns, heavy_rows=heavy_rows[:nh].clone() if nh else heavy_rows[:0],
                     heavy_ptr=heavy_ptr[: nh + 1].clone(), heavy_cols=hcol, heavy_vals=hval)
 
     def release(self):

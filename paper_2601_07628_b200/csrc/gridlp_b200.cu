@@ -1,19 +1,20 @@
 // gridlp_b200.cu — sm_100a kernels + C ABI for the distributed-PDHG hot path.
 //
 // Design:
-//  * Sparse products run over a tile directory of each CSR block. A light
-//    tile (<= 256 rows, <= 4096 nnz) is processed by one 256-thread CTA in
-//    two phases: (a) all threads stream values/column indices (coalesced,
-//    L2 evict-first) and gather the dense vector (L2 evict-last), writing
-//    the rounded products val*x into shared memory — this balances the
-//    gathers over the CTA regardless of row lengths; (b) one thread per row
-//    adds its products left to right from +0.0 and applies the fused PDHG
-//    epilogue. Because each product is rounded and then added in index
-//    order, the row sum is bit-identical to scipy's csr_matvec — the
-//    reference's kernel (sparse_kernels.py:18-24). A heavy tile (one row
-//    longer than exact_row_max) is tree-summed by the whole CTA.
-//  * The epilogue's per-row vector reads (x, c, bounds, anchor) are issued
-//    before phase (a) so their DRAM latency overlaps the gathers.
+//  * Sparse products run over a SELL-32 layout of each CSR block: 32
+//    consecutive rows form a slice owned by one warp, lanes ordered by row
+//    length; entry j of lane l sits at slice_off[s] + 32 j + l in the row's
+//    original order. A warp step therefore reads 32 consecutive column
+//    indices and values (coalesced, L2 evict-first), gathers 32 entries of
+//    the dense vector (L2 evict-last) and each lane adds its product to a
+//    register sum left to right from +0.0 — bit-identical to scipy's
+//    csr_matvec, the reference's kernel (sparse_kernels.py:18-24). The
+//    fused PDHG epilogue then runs in natural row order.
+//  * Rows longer than exact_row_max live in a compact CSR, cut into chunks
+//    of GRIDLP_HEAVY_CHUNK entries; one CTA per chunk tree-sums its part and
+//    the last chunk CTA of a row to arrive adds the chunk sums in chunk order
+//    (deterministic) and applies the epilogue. Chunk CTAs are launched first
+//    so long rows do not form a tail.
 //  * No FMA contraction anywhere: every multiply/add/divide is an explicit
 //    __d*_rn so each numpy expression of the reference is reproduced
 //    operation for operation.
@@ -32,8 +33,6 @@ namespace {
 
 constexpr int TPB = 256;
 constexpr int WARPS = TPB / 32;
-constexpr int CAP = GRIDLP_TILE_NNZ_CAP;
-constexpr int UNROLL = 8;
 constexpr int64_t ROWS_MAX_BLOCKS = 1184;  // 8 x 148 SMs
 
 thread_local std::string g_err;
@@ -108,46 +107,6 @@ __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
-
-// ------------------------------------------------ async copies (TMA, LDGSTS)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-  }
-}
-// 1D bulk copy global -> shared through the TMA unit (SASS UBLKCP), completion
-// signalled on `bar`, L2 evict-first policy for the streamed matrix.
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                             uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-// 8-byte LDGSTS gather with an L2 evict-last policy (the dense vector stays
-// resident in L2 across iterations).
-__device__ __forceinline__ void cp_async8(void* dst, const void* src, uint64_t pol) {
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;"
-               ::"r"(smem_u32(dst)), "l"(src), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // ------------------------------------------------------- deterministic sums
 __device__ __forceinline__ double warp_sum(double v) {
@@ -403,9 +362,6 @@ struct OpInitPrimal {
 };
 
 // ------------------------------------------------------------------ kernels
-template <int NR>
-struct AccN { double v[NR > 0 ? NR : 1]; };
-
 template <class Op>
 __device__ __forceinline__ void store_partials(double (&acc)[Op::NRED > 0 ? Op::NRED : 1],
                                                double* partials) {
@@ -419,266 +375,118 @@ __device__ __forceinline__ void store_partials(double (&acc)[Op::NRED > 0 ? Op::
   }
 }
 
-// Sparse-product + fused-epilogue kernel over a tile directory, one CTA per
-// tile. LEAN (variant 2) trades the early epilogue prefetch and the 8-deep
-// unroll for <= 32 registers, so 8 CTAs (64 warps) stay resident per SM and
-// keep the gather stream saturated.
-template <class Op, int U, int MINB, bool LEAN>
-__global__ void __launch_bounds__(TPB, MINB) tile_kernel(gridlp_csr_t A, const double* __restrict__ g,
-                                                         Op op, double* __restrict__ partials) {
-  extern __shared__ double prod[];
+constexpr int SELL_WPB = 2;          // warps (slices) per CTA
+constexpr int SELL_NT = SELL_WPB * 32;
+constexpr int SELL_U = 4;            // steps in flight per lane
+constexpr int SELL_MINB = 32;        // 64 warps per SM at <= 32 registers
+
+// Deterministic per-CTA reduction of a SELL_NT-thread CTA: warp tree, then
+// warps in order, one slot per CTA.
+template <class Op>
+__device__ __forceinline__ void cta_partials(double (&acc)[Op::NRED > 0 ? Op::NRED : 1], double* partials) {
+  if constexpr (Op::NRED > 0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double rs[Op::NRED][SELL_WPB];
+#pragma unroll
+    for (int q = 0; q < Op::NRED; ++q) {
+      const double v = warp_sum(acc[q]);
+      if (lane == 0) rs[q][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < Op::NRED; ++q) {
+        double t = rs[q][0];
+        for (int w = 1; w < SELL_WPB; ++w) t = dadd(t, rs[q][w]);
+        partials[(int64_t)blockIdx.x * GRIDLP_MAX_RED + q] = t;
+      }
+    }
+  }
+}
+
+// Heavy rows, one CTA per chunk of GRIDLP_HEAVY_CHUNK entries: strided
+// per-thread sums, warp tree, warps in order; the last-arriving chunk CTA of
+// a row adds the chunk sums in chunk order (deterministic) and applies the
+// fused epilogue. Launched before the slice kernel of the same product; its
+// reduction partials occupy slots [0, num_chunks).
+template <class Op>
+__global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
+                                                              double* __restrict__ partials) {
+  constexpr int U = SELL_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   double acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
-
-  const int tid = threadIdx.x;
-  const int64_t t = blockIdx.x;
-  const int r0 = A.tile_ptr[t];
-  const int r1 = A.tile_ptr[t + 1];
-  const int p0 = A.row_ptr[r0];
-  const int p1 = A.row_ptr[r1];
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
-  const int* __restrict__ col = A.col_idx;
-  const double* __restrict__ val = A.values;
-
-  if (r1 - r0 == 1 && p1 - p0 > A.exact_row_max) {
-    // heavy row: CTA-wide strided products, deterministic tree sum
-    typename Op::Data d{};
-    if (tid == 0) d = op.load(r0);
-    double s = 0.0;
-    for (int k = p0 + tid; k < p1; k += TPB)
-      s = dadd(s, dmul(ld_stream(val + k, pf), ld_gather(g + ld_stream(col + k, pf), pl)));
-    double tmp[1] = {s};
-    __shared__ double hscratch[1][WARPS];
-    block_sum<1>(tmp, hscratch);
-    if (tid == 0) op.row(r0, tmp[0], d, acc);
-    __syncthreads();
-  } else {
-    const int r = r0 + tid;
-    const bool mine = r < r1;
-    typename Op::Data d{};
-    int a = 0, b = 0;
-    if (mine && !LEAN) {
-      d = op.load(r);
-      a = A.row_ptr[r] - p0;
-      b = A.row_ptr[r + 1] - p0;
-    }
-    // phase (a): balanced gathers, rounded products into shared memory
-    for (int base = p0 + tid; base < p1; base += TPB * U) {
-      int cidx[U];
-      double v[U], xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = base + u * TPB;
-        cidx[u] = k < p1 ? ld_stream(col + k, pf) : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = base + u * TPB;
-        v[u] = k < p1 ? ld_stream(val + k, pf) : 0.0;
-        xv[u] = k < p1 ? ld_gather(g + cidx[u], pl) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = base + u * TPB;
-        if (k < p1) prod[k - p0] = dmul(v[u], xv[u]);
-      }
-    }
-    if (mine && LEAN) {
-      d = op.load(r);
-      a = A.row_ptr[r] - p0;
-      b = A.row_ptr[r + 1] - p0;
-    }
-    __syncthreads();
-    // phase (b): sequential row sums (scipy csr_matvec order) + epilogue
-    if (mine) {
-      double s = 0.0;
-      for (int k = a; k < b; ++k) s = dadd(s, prod[k]);
-      op.row(r, s, d, acc);
-    }
-  }
-  store_partials<Op>(acc, partials);
-}
-
-// One CTA per tile with the matrix stream staged by the TMA unit
-// (variants 3/4): thread 0 issues two 1D bulk copies (values, column
-// indices) into shared memory, so the LSU/L1 path carries only the gathers
-// and the epilogue vectors. Gathers read the staged column indices and the
-// rounded products overwrite the staged values in place; row sums as above.
-template <class Op, int U, int MINB>
-__global__ void __launch_bounds__(TPB, MINB) tile_kernel_tma(gridlp_csr_t A, const double* __restrict__ g,
-                                                             Op op, double* __restrict__ partials) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int cap = A.tile_nnz_cap;
-  double* sv = reinterpret_cast<double*>(smem_raw);
-  int* sc = reinterpret_cast<int*>(smem_raw + (size_t)(cap + 4) * 8);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + (size_t)(cap + 4) * 8 + (size_t)(cap + 8) * 4);
-  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
-  double acc[NR];
-#pragma unroll
-  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
   const int tid = threadIdx.x;
-  const int64_t t = blockIdx.x;
-  const int r0 = A.tile_ptr[t];
-  const int r1 = A.tile_ptr[t + 1];
-  const int p0 = A.row_ptr[r0];
-  const int p1 = A.row_ptr[r1];
-  op.prepare();
-  const uint64_t pf = policy_evict_first();
-  const uint64_t pl = policy_evict_last();
-
-  if (r1 - r0 == 1 && p1 - p0 > A.exact_row_max) {
-    typename Op::Data d{};
-    if (tid == 0) d = op.load(r0);
-    double s = 0.0;
-    for (int k = p0 + tid; k < p1; k += TPB)
-      s = dadd(s, dmul(ld_stream(A.values + k, pf), ld_gather(g + ld_stream(A.col_idx + k, pf), pl)));
-    double tmp[1] = {s};
-    __shared__ double hscratch[1][WARPS];
-    block_sum<1>(tmp, hscratch);
-    if (tid == 0) op.row(r0, tmp[0], d, acc);
-    __syncthreads();
-  } else {
-    const int nnz = p1 - p0;
-    if (tid == 0) {
-      const int va = p0 & ~1, vb = (p1 + 1) & ~1;
-      const int ca = p0 & ~3, cb = (p1 + 3) & ~3;
-      const uint32_t vbytes = (uint32_t)(vb - va) * 8u, cbytes = (uint32_t)(cb - ca) * 4u;
-      mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      mbar_expect_tx(bar, vbytes + cbytes);
-      if (vbytes) tma_bulk_g2s(sv, A.values + va, vbytes, bar, pf);
-      if (cbytes) tma_bulk_g2s(sc, A.col_idx + ca, cbytes, bar, pf);
-    }
-    const int r = r0 + tid;
-    const bool mine = r < r1;
-    typename Op::Data d{};
-    int a = 0, b = 0;
-    if (mine) {
-      d = op.load(r);
-      a = A.row_ptr[r] - p0;
-      b = A.row_ptr[r + 1] - p0;
-    }
-    __syncthreads();            // barrier initialised before anyone waits on it
-    mbar_wait(bar, 0);
-    double* v = sv + (p0 & 1);
-    const int* c = sc + (p0 & 3);
-    for (int base = tid; base < nnz; base += TPB * U) {
-      double xv[U];
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t c = blockIdx.x;
+  const int h = A.chunk_row[c];
+  const int c0 = A.chunk_first[h];
+  const int nch = A.chunk_first[h + 1] - c0;
+  const int64_t p0 = (int64_t)A.heavy_ptr[h] + (c - c0) * (int64_t)GRIDLP_HEAVY_CHUNK;
+  const int64_t pe = A.heavy_ptr[h + 1];
+  const int64_t p1 = p0 + GRIDLP_HEAVY_CHUNK < pe ? p0 + GRIDLP_HEAVY_CHUNK : pe;
+  double s = 0.0;
+  for (int64_t k0 = p0 + tid; k0 < p1; k0 += (int64_t)SELL_NT * U) {
+    int cc[U];
+    double vv[U], xx[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = base + u * TPB;
-        xv[u] = k < nnz ? ld_gather(g + c[k], pl) : 0.0;
-      }
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + (int64_t)u * SELL_NT;
+      cc[u] = k < p1 ? ld_stream(A.heavy_cols + k, pf) : 0;
+      vv[u] = k < p1 ? ld_stream(A.heavy_vals + k, pf) : 0.0;
+    }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = base + u * TPB;
-        if (k < nnz) v[k] = dmul(v[k], xv[u]);
+    for (int u = 0; u < U; ++u) xx[u] = k0 + (int64_t)u * SELL_NT < p1 ? ld_gather(g + cc[u], pl) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k0 + (int64_t)u * SELL_NT < p1) s = dadd(s, dmul(vv[u], xx[u]));
+  }
+  s = warp_sum(s);
+  __shared__ double hs[SELL_WPB];
+  if (lane == 0) hs[warp] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double t = hs[0];
+#pragma unroll
+    for (int w = 1; w < SELL_WPB; ++w) t = dadd(t, hs[w]);
+    bool last = true;
+    if (nch > 1) {
+      // last-arriving chunk CTA of the row adds the chunk sums in chunk order
+      A.chunk_sums[c] = t;
+      __threadfence();
+      last = atomicAdd(&A.chunk_done[h], 1) == nch - 1;
+      if (last) {
+        __threadfence();
+        t = __ldcg(A.chunk_sums + c0);
+        for (int q = 1; q < nch; ++q) t = dadd(t, __ldcg(A.chunk_sums + c0 + q));
+        A.chunk_done[h] = 0;   // self-reset for the next launch (stream-ordered)
       }
     }
-    __syncthreads();
-    if (mine) {
-      double sum = 0.0;
-      for (int k = a; k < b; ++k) sum = dadd(sum, v[k]);
-      op.row(r, sum, d, acc);
+    if (last) {
+      const int row = A.heavy_rows[h];
+      const typename Op::Data d = op.load(row);
+      op.row(row, t, d, acc);
     }
   }
-  store_partials<Op>(acc, partials);
+  cta_partials<Op>(acc, partials);
 }
 
-// SELL-32 window kernel (variant 6). One CTA = one window of 256 rows =
-// 8 warps = 8 slices. Each lane owns one light row of its slice and walks
-// the row's entries in their original order: the column index and value of
-// step j are 32 consecutive elements across the warp (fully coalesced), the
-// gather of x is one 8-byte load, and the sum lives in a register — no
-// shared-memory staging of products, no bank conflicts, no phase barrier.
-// Sums are parked in shared memory by window-local row and the epilogue
-// then runs in natural row order (coalesced vector traffic). Blocks past the
-// windows tree-sum one heavy row each (compact CSR).
-template <class Op, int U, int MINB, bool EARLY>
-__global__ void __launch_bounds__(TPB, MINB) sell_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
-                                                         double* __restrict__ partials) {
-  __shared__ double sums[TPB];
-  __shared__ int have[TPB];
+// Product + fused epilogue over the light rows of a SELL-32 block: each CTA
+// owns SELL_WPB slices; its reduction partials follow the heavy kernel's in
+// the slot array. A slice's warp parks its 32 row sums in shared memory by row, __syncwarp()s
+// and runs the natural-order epilogue of its own 32 rows — no CTA barrier on
+// the light path.
+template <class Op>
+__global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t A, const double* __restrict__ g,
+                                                                   Op op, double* __restrict__ partials) {
+  constexpr int U = SELL_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
-  double acc[NR];
-#pragma unroll
-  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
-  const int tid = threadIdx.x;
-  op.prepare();
-  const uint64_t pf = policy_evict_first();
-  const uint64_t pl = policy_evict_last();
-  const int64_t w = blockIdx.x;
-  if (w >= A.num_windows) {
-    const int64_t h = w - A.num_windows;
-    const int row = A.heavy_rows[h];
-    const int p0 = A.heavy_ptr[h], p1 = A.heavy_ptr[h + 1];
-    typename Op::Data d{};
-    if (tid == 0) d = op.load(row);
-    double s = 0.0;
-    for (int k = p0 + tid; k < p1; k += TPB)
-      s = dadd(s, dmul(ld_stream(A.heavy_vals + k, pf), ld_gather(g + ld_stream(A.heavy_cols + k, pf), pl)));
-    double tmp[1] = {s};
-    __shared__ double hscratch[1][WARPS];
-    block_sum<1>(tmp, hscratch);
-    if (tid == 0) op.row(row, tmp[0], d, acc);
-    __syncthreads();
-  } else {
-    const int64_t r = w * TPB + tid;
-    const bool in_range = r < A.num_rows;
-    typename Op::Data d{};
-    if (EARLY && in_range) d = op.load(r);   // natural-order epilogue operands, issued first
-    have[tid] = 0;
-    const int lane = tid & 31;
-    const int64_t slice = w * WARPS + (tid >> 5);
-    const int info = A.lane_info[slice * 32 + lane];
-    __syncthreads();
-    if (info >= 0) {
-      const int len = info >> 8;
-      const int64_t base = (int64_t)A.slice_off[slice] + lane;
-      const int* __restrict__ cp = A.sell_cols + base;
-      const double* __restrict__ vp = A.sell_vals + base;
-      double s = 0.0;
-      for (int j = 0; j < len; j += U) {
-        int c[U];
-        double v[U], x[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const bool ok = j + u < len;
-          c[u] = ok ? ld_stream(cp + 32 * (j + u), pf) : 0;
-          v[u] = ok ? ld_stream(vp + 32 * (j + u), pf) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = (j + u < len) ? ld_gather(g + c[u], pl) : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
-      }
-      sums[info & 255] = s;
-      have[info & 255] = 1;
-    }
-    if (!EARLY && in_range) d = op.load(r);
-    __syncthreads();
-    if (in_range && have[tid]) op.row(r, sums[tid], d, acc);
-  }
-  store_partials<Op>(acc, partials);
-}
-
-// Warp-window SELL kernel (variant 9): the window is ONE warp (32 rows,
-// sorted by length inside the slice), so there is no CTA-wide barrier — each
-// warp parks its 32 sums in shared memory, __syncwarp()s and runs the
-// natural-order epilogue of its own 32 rows. CTAs are WPB warps; heavy rows
-// (compact CSR) are tree-summed by the blocks past the windows.
-template <class Op, int U, int WPB, bool EARLY, int MINB>
-__global__ void __launch_bounds__(WPB * 32, MINB) sell32_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
-                                                          double* __restrict__ partials) {
-  __shared__ double sums[WPB][32];
-  __shared__ int have[WPB][32];
-  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
-  constexpr int NT = WPB * 32;
+  __shared__ double sums[SELL_WPB][32];
+  __shared__ int have[SELL_WPB][32];
   double acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
@@ -687,32 +495,11 @@ __global__ void __launch_bounds__(WPB * 32, MINB) sell32_kernel(gridlp_csr_t A, 
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
-  const int64_t nblk_win = (A.num_windows + WPB - 1) / WPB;
-  if ((int64_t)blockIdx.x >= nblk_win) {
-    const int64_t h = blockIdx.x - nblk_win;
-    const int row = A.heavy_rows[h];
-    const int p0 = A.heavy_ptr[h], p1 = A.heavy_ptr[h + 1];
-    typename Op::Data d{};
-    if (tid == 0) d = op.load(row);
-    double s = 0.0;
-    for (int k = p0 + tid; k < p1; k += NT)
-      s = dadd(s, dmul(ld_stream(A.heavy_vals + k, pf), ld_gather(g + ld_stream(A.heavy_cols + k, pf), pl)));
-    s = warp_sum(s);
-    __shared__ double hs[WPB];
-    if (lane == 0) hs[warp] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double t = hs[0];
-      for (int w = 1; w < WPB; ++w) t = dadd(t, hs[w]);
-      op.row(row, t, d, acc);
-    }
-  } else {
-    const int64_t slice = (int64_t)blockIdx.x * WPB + warp;
-    if (slice < A.num_windows) {
+  {
+    const int64_t slice = (int64_t)blockIdx.x * SELL_WPB + warp;
+    if (slice < A.num_slices) {
       const int64_t r = slice * 32 + lane;
       const bool in_range = r < A.num_rows;
-      typename Op::Data d{};
-      if (EARLY && in_range) d = op.load(r);
       have[warp][lane] = 0;
       const int info = A.lane_info[slice * 32 + lane];
       __syncwarp();
@@ -740,148 +527,15 @@ __global__ void __launch_bounds__(WPB * 32, MINB) sell32_kernel(gridlp_csr_t A, 
         sums[warp][info & 31] = s;
         have[warp][info & 31] = 1;
       }
-      if (!EARLY && in_range) d = op.load(r);
+      // epilogue operands are loaded after the sums: issuing them first costs
+      // registers (occupancy) and measured slower (profiles/r1, variant 10)
+      typename Op::Data d{};
+      if (in_range) d = op.load(r);
       __syncwarp();
       if (in_range && have[warp][lane]) op.row(r, sums[warp][lane], d, acc);
     }
   }
-  if constexpr (Op::NRED > 0) {
-    // deterministic: warp tree, then warps in order
-    __shared__ double rs[Op::NRED][WPB];
-#pragma unroll
-    for (int q = 0; q < Op::NRED; ++q) {
-      const double v = warp_sum(acc[q]);
-      if (lane == 0) rs[q][warp] = v;
-    }
-    __syncthreads();
-    if (tid == 0) {
-#pragma unroll
-      for (int q = 0; q < Op::NRED; ++q) {
-        double t = rs[q][0];
-        for (int w = 1; w < WPB; ++w) t = dadd(t, rs[q][w]);
-        partials[(int64_t)blockIdx.x * GRIDLP_MAX_RED + q] = t;
-      }
-    }
-  }
-}
-
-// Persistent, TMA-pipelined product + epilogue kernel (variant 0).
-// Each CTA walks its light tiles (round-robin over light_tiles) with a
-// two-slot pipeline: while tile i is gathered and summed, the TMA unit
-// streams tile i+1's values and column indices into the other slot. The
-// gathers of the dense vector are 8-byte LDGSTS (cp.async) straight into
-// shared memory, so every gather of a tile is in flight at once without
-// holding registers. Row sums are the same sequential +0.0-seeded sums as
-// the one-CTA-per-tile kernel (bit-identical to scipy). Heavy tiles follow,
-// tree-summed by the whole CTA. Reduction partials are per CTA, in a fixed
-// tile order, hence deterministic.
-struct PipeLayout {
-  int cap;
-  __host__ __device__ size_t vals_bytes() const { return (size_t)(cap + 4) * 8; }
-  __host__ __device__ size_t cols_bytes() const { return (size_t)(cap + 8) * 4; }
-  __host__ __device__ size_t slot_bytes() const { return vals_bytes() + cols_bytes(); }
-  __host__ __device__ size_t total() const { return 2 * slot_bytes() + (size_t)cap * 8 + 64; }
-};
-
-template <class Op>
-__global__ void __launch_bounds__(TPB) tile_kernel_pipe(gridlp_csr_t A, const double* __restrict__ g,
-                                                        Op op, double* __restrict__ partials) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const PipeLayout L{A.tile_nnz_cap};
-  double* xbuf = reinterpret_cast<double*>(smem_raw + 2 * L.slot_bytes());
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 2 * L.slot_bytes() + (size_t)L.cap * 8);
-  auto slot_vals = [&](int s) { return reinterpret_cast<double*>(smem_raw + s * L.slot_bytes()); };
-  auto slot_cols = [&](int s) {
-    return reinterpret_cast<int*>(smem_raw + s * L.slot_bytes() + L.vals_bytes());
-  };
-
-  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
-  double acc[NR];
-#pragma unroll
-  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
-  const int tid = threadIdx.x;
-  op.prepare();
-  const uint64_t pf = policy_evict_first();
-  const uint64_t pl = policy_evict_last();
-  const int* __restrict__ rp = A.row_ptr;
-
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  // stage the streams of light tile #idx (in this CTA's sequence) into slot s
-  auto issue = [&](int64_t idx, int s) {
-    const int t = A.light_tiles[idx];
-    const int p0 = rp[A.tile_ptr[t]];
-    const int p1 = rp[A.tile_ptr[t + 1]];
-    const int va = p0 & ~1, vb = (p1 + 1) & ~1;
-    const int ca = p0 & ~3, cb = (p1 + 3) & ~3;
-    const uint32_t vbytes = (uint32_t)(vb - va) * 8u, cbytes = (uint32_t)(cb - ca) * 4u;
-    fence_proxy_async();
-    mbar_expect_tx(&bars[s], vbytes + cbytes);
-    if (vbytes) tma_bulk_g2s(slot_vals(s), A.values + va, vbytes, &bars[s], pf);
-    if (cbytes) tma_bulk_g2s(slot_cols(s), A.col_idx + ca, cbytes, &bars[s], pf);
-  };
-
-  const int64_t stride = gridDim.x;
-  int64_t i = blockIdx.x;
-  uint32_t phase[2] = {0u, 0u};
-  if (i < A.num_light && tid == 0) issue(i, 0);
-  for (int it = 0; i < A.num_light; ++it, i += stride) {
-    const int s = it & 1;
-    const int t = A.light_tiles[i];
-    const int r0 = A.tile_ptr[t];
-    const int r1 = A.tile_ptr[t + 1];
-    const int p0 = rp[r0];
-    const int p1 = rp[r1];
-    const int nnz = p1 - p0;
-    const int r = r0 + tid;
-    const bool mine = r < r1;
-    typename Op::Data d{};
-    int a = 0, b = 0;
-    if (mine) {
-      d = op.load(r);                   // epilogue operands: in flight during the gathers
-      a = rp[r] - p0;
-      b = rp[r + 1] - p0;
-    }
-    if (tid == 0 && i + stride < A.num_light) issue(i + stride, s ^ 1);
-    mbar_wait(&bars[s], phase[s]);
-    phase[s] ^= 1u;
-    const double* sv = slot_vals(s) + (p0 & 1);
-    const int* sc = slot_cols(s) + (p0 & 3);
-    for (int k = tid; k < nnz; k += TPB) cp_async8(&xbuf[k], g + sc[k], pl);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-    for (int k = tid; k < nnz; k += TPB) xbuf[k] = dmul(sv[k], xbuf[k]);
-    __syncthreads();
-    if (mine) {
-      double sum = 0.0;
-      for (int k = a; k < b; ++k) sum = dadd(sum, xbuf[k]);
-      op.row(r, sum, d, acc);
-    }
-    __syncthreads();
-  }
-
-  for (int64_t h = blockIdx.x; h < A.num_heavy; h += stride) {
-    const int t = A.heavy_tiles[h];
-    const int row = A.tile_ptr[t];
-    const int p0 = rp[row], p1 = rp[row + 1];
-    typename Op::Data d{};
-    if (tid == 0) d = op.load(row);
-    double sum = 0.0;
-    for (int k = p0 + tid; k < p1; k += TPB)
-      sum = dadd(sum, dmul(ld_stream(A.values + k, pf), ld_gather(g + ld_stream(A.col_idx + k, pf), pl)));
-    double tmp[1] = {sum};
-    __shared__ double hscratch[1][WARPS];
-    block_sum<1>(tmp, hscratch);
-    if (tid == 0) op.row(row, tmp[0], d, acc);
-    __syncthreads();
-  }
-  store_partials<Op>(acc, partials);
+  cta_partials<Op>(acc, partials);
 }
 
 // Row-wise epilogue over ascending-order sums of partial vectors.
@@ -937,58 +591,27 @@ int64_t rows_blocks(int64_t n) {
 
 int check_csr(const gridlp_csr_t* A) {
   if (!A) return fail(GRIDLP_ERR_ARG, "null matrix");
-  if (A->num_rows < 0 || A->num_cols < 0 || A->nnz < 0 || A->num_tiles < 0)
+  if (A->num_rows < 0 || A->num_cols < 0 || A->nnz < 0 || A->num_slices < 0 || A->num_heavy_rows < 0 ||
+      A->num_chunks < 0)
     return fail(GRIDLP_ERR_ARG, "negative matrix dimension");
   if (A->nnz >= (int64_t(1) << 31)) return fail(GRIDLP_ERR_ARG, "block nnz must be < 2^31");
-  if (A->tile_nnz_cap < 64 || A->tile_nnz_cap > CAP || (A->tile_nnz_cap & 7))
-    return fail(GRIDLP_ERR_ARG, "tile_nnz_cap must be a multiple of 8 in [64, TILE_NNZ_CAP]");
-  if (A->exact_row_max < 0 || A->exact_row_max > A->tile_nnz_cap / 2)
-    return fail(GRIDLP_ERR_ARG, "exact_row_max must be in [0, tile_nnz_cap/2]");
-  if (A->variant < 0 || A->variant > 10) return fail(GRIDLP_ERR_ARG, "unknown kernel variant");
-  if (A->variant >= 6) {
-    const int win = A->variant >= 9 ? 32 : TPB;
-    if (A->num_rows > 0 &&
-        (!A->slice_off || !A->lane_info || A->num_windows != (A->num_rows + win - 1) / win))
-      return fail(GRIDLP_ERR_ARG, "SELL layout missing or inconsistent");
-    if (A->num_heavy_rows > 0 && (!A->heavy_rows || !A->heavy_ptr || !A->heavy_cols || !A->heavy_vals))
-      return fail(GRIDLP_ERR_ARG, "missing heavy-row CSR");
-    if (A->nnz > 0 && (!A->sell_cols || !A->sell_vals)) return fail(GRIDLP_ERR_ARG, "missing SELL arrays");
-    return GRIDLP_OK;
-  }
-  if (A->num_light + A->num_heavy != A->num_tiles)
-    return fail(GRIDLP_ERR_ARG, "light + heavy tiles must cover the tile directory");
-  if (A->num_tiles > 0 && ((A->num_light > 0 && !A->light_tiles) || (A->num_heavy > 0 && !A->heavy_tiles)))
-    return fail(GRIDLP_ERR_ARG, "missing light/heavy tile lists");
-  if (A->num_rows > 0 && (!A->row_ptr || !A->tile_ptr || A->num_tiles < 1))
-    return fail(GRIDLP_ERR_ARG, "missing row_ptr/tile_ptr");
-  if (A->nnz > 0 && (!A->col_idx || !A->values)) return fail(GRIDLP_ERR_ARG, "missing col_idx/values");
+  if (A->exact_row_max < 0 || A->exact_row_max > GRIDLP_EXACT_ROW_MAX_LIMIT)
+    return fail(GRIDLP_ERR_ARG, "exact_row_max out of range");
+  if (A->num_slices != (A->num_rows + 31) / 32) return fail(GRIDLP_ERR_ARG, "num_slices must be ceil(rows/32)");
+  if (A->num_rows > 0 && (!A->slice_off || !A->lane_info)) return fail(GRIDLP_ERR_ARG, "missing SELL slices");
+  if (A->nnz > 0 && (!A->sell_cols || !A->sell_vals)) return fail(GRIDLP_ERR_ARG, "missing SELL arrays");
+  if (A->num_heavy_rows > 0 &&
+      (!A->heavy_rows || !A->heavy_ptr || !A->heavy_cols || !A->heavy_vals || !A->chunk_first ||
+       !A->chunk_row || !A->chunk_sums || !A->chunk_done || A->num_chunks < A->num_heavy_rows))
+    return fail(GRIDLP_ERR_ARG, "missing or inconsistent heavy-row chunk directory");
   return GRIDLP_OK;
 }
 
-int64_t src_rows(const gridlp_src_t* src) { return src->A ? src->A->num_rows : src->num_rows; }
-
-// CTAs of the persistent kernel: SMs x resident CTAs (cached per op type and
-// shared-memory size).
-template <class Op>
-int pipe_grid(size_t smem) {
-  static size_t cached_smem = 0;
-  static int cached = 0;
-  if (cached > 0 && cached_smem == smem) return cached;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
-  int sms = 0;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
-  if (cudaFuncSetAttribute(tile_kernel_pipe<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return -1;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel_pipe<Op>, TPB, smem) != cudaSuccess)
-    return -1;
-  if (per_sm < 1) per_sm = 1;
-  cached = sms * per_sm;
-  cached_smem = smem;
-  return cached;
+int64_t sell_blocks(const gridlp_csr_t* A) {
+  return A->num_rows > 0 ? A->num_chunks + (A->num_slices + SELL_WPB - 1) / SELL_WPB : 0;
 }
+
+int64_t src_rows(const gridlp_src_t* src) { return src->A ? src->A->num_rows : src->num_rows; }
 
 template <class Op>
 int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* stream,
@@ -1002,9 +625,7 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
     if (rc) return rc;
     if (src->A->num_rows > 0 && src->A->nnz > 0 && !src->gather)
       return fail(GRIDLP_ERR_ARG, std::string(name) + ": missing gather vector");
-    slots = src->A->num_rows <= 0 ? 0
-            : (src->A->variant >= 9 ? (src->A->num_windows + 1) / 2 + src->A->num_heavy_rows
-               : src->A->variant >= 6 ? src->A->num_windows + src->A->num_heavy_rows : src->A->num_tiles);
+    slots = sell_blocks(src->A);
   } else {
     if (src->nparts < 0 || src->nparts > GRIDLP_MAX_PARTS)
       return fail(GRIDLP_ERR_ARG, std::string(name) + ": nparts out of range");
@@ -1023,46 +644,19 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
     }
   }
   if (slots > 0) {
-    if (src->A && src->A->variant == 0) {
-      const size_t smem = PipeLayout{src->A->tile_nnz_cap}.total();
-      int grid = pipe_grid<Op>(smem);
-      if (grid <= 0) return fail(GRIDLP_ERR_CUDA, std::string(name) + ": occupancy query failed");
-      if (grid > slots) grid = (int)slots;
-      slots = grid;
-      tile_kernel_pipe<Op><<<(unsigned)grid, TPB, smem, s>>>(*src->A, src->gather, op, partials);
-    } else if (src->A) {
+    if (src->A) {
       const gridlp_csr_t& M = *src->A;
-      const size_t sm_prod = M.tile_nnz_cap * sizeof(double);
-      const size_t sm_tma = (size_t)(M.tile_nnz_cap + 4) * 8 + (size_t)(M.tile_nnz_cap + 8) * 4 + 16;
-      const unsigned nb = (unsigned)slots;
-      switch (M.variant) {
-        case 2: tile_kernel<Op, 4, 8, true><<<nb, TPB, sm_prod, s>>>(M, src->gather, op, partials); break;
-        case 3: tile_kernel_tma<Op, 4, 8><<<nb, TPB, sm_tma, s>>>(M, src->gather, op, partials); break;
-        case 4: tile_kernel_tma<Op, 8, 5><<<nb, TPB, sm_tma, s>>>(M, src->gather, op, partials); break;
-        case 5: tile_kernel<Op, 4, 6, false><<<nb, TPB, sm_prod, s>>>(M, src->gather, op, partials); break;
-        case 9: case 10: {
-          const int64_t nwb = (M.num_windows + 1) / 2;
-          const unsigned nb9 = (unsigned)(nwb + M.num_heavy_rows);
-          slots = nb9;
-          if (!nb9) break;
-          if (M.variant == 9) sell32_kernel<Op, 4, 2, false, 32><<<nb9, 64, 0, s>>>(M, src->gather, op, partials);
-          else sell32_kernel<Op, 4, 2, true, 21><<<nb9, 64, 0, s>>>(M, src->gather, op, partials);
-          break;
-        }
-        case 6: case 7: case 8: {
-          const unsigned nsell = (unsigned)(M.num_windows + M.num_heavy_rows);
-          slots = nsell;
-          if (!nsell) break;
-          if (M.variant == 6) sell_kernel<Op, 4, 8, false><<<nsell, TPB, 0, s>>>(M, src->gather, op, partials);
-          else if (M.variant == 7) sell_kernel<Op, 8, 6, false><<<nsell, TPB, 0, s>>>(M, src->gather, op, partials);
-          else sell_kernel<Op, 4, 5, true><<<nsell, TPB, 0, s>>>(M, src->gather, op, partials);
-          break;
-        }
-        default: tile_kernel<Op, UNROLL, 5, false><<<nb, TPB, sm_prod, s>>>(M, src->gather, op, partials); break;
+      if (M.num_chunks > 0) {
+        heavy_chunk_kernel<Op><<<(unsigned)M.num_chunks, SELL_NT, 0, s>>>(M, src->gather, op, partials);
+        int rc = check_launch(name);
+        if (rc) return rc;
       }
-    } else {
+      const int64_t nlight = slots - M.num_chunks;
+      if (nlight > 0)
+        sell32_kernel<Op><<<(unsigned)nlight, SELL_NT, 0, s>>>(
+            M, src->gather, op, partials ? partials + M.num_chunks * GRIDLP_MAX_RED : nullptr);
+    } else
       rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials);
-    }
     int rc = check_launch(name);
     if (rc) return rc;
   }
@@ -1080,10 +674,6 @@ gridlp_src_t rows_src(int64_t n) {
   s.num_rows = n;
   return s;
 }
-
-struct KernelAttrInit {
-  KernelAttrInit() {}
-};
 
 }  // namespace
 
@@ -1110,9 +700,7 @@ int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes) {
 
 int64_t gridlp_op_slots(const gridlp_src_t* src) {
   if (!src) return 0;
-  if (src->A && src->A->variant >= 9) return (src->A->num_windows + 1) / 2 + src->A->num_heavy_rows;
-  if (src->A && src->A->variant >= 6) return src->A->num_windows + src->A->num_heavy_rows;
-  if (src->A) return src->A->num_rows > 0 ? src->A->num_tiles : 0;
+  if (src->A) return sell_blocks(src->A);
   return src->num_rows > 0 ? rows_blocks(src->num_rows) : 0;
 }
 

@@ -66,8 +66,6 @@ class EngineOptions:
     omega_max: float = 1e6
     time_limit_seconds: float | None = None
     exact_row_max: int = DEFAULT_EXACT_ROW_MAX
-    tile_cap: int = 2048
-    kernel_variant: int = 9
     device_setup: bool = True
     use_graphs: bool = True
     graph_chunk: int = 128
@@ -192,7 +190,7 @@ class PdhgEngine:
     # ------------------------------------------------------------ setup
     def _build(self, problem):
         lay, dev = self.layout, self.device
-        on_device = dev.type == "cuda" and self.opts.kernel_variant >= 9 and self.opts.device_setup
+        on_device = dev.type == "cuda" and self.opts.device_setup
         tm = self.timings
         if on_device:
             t0 = time.perf_counter()
@@ -231,8 +229,7 @@ class PdhgEngine:
             t = lambda a: torch.as_tensor(np.ascontiguousarray(a[r0:r1]), **f64)  # noqa: E731
             self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
-        kw = dict(exact_row_max=self.opts.exact_row_max, tile_cap=self.opts.tile_cap,
-                  variant=self.opts.kernel_variant)
+        kw = dict(exact_row_max=self.opts.exact_row_max)
         nnz_of = {}
         for (i, j) in local:
             if on_device:

@@ -21,9 +21,8 @@ HEADER = ROOT / "include" / "gridlp_b200.h"
 
 MAX_RED = 8
 MAX_PARTS = 16
-TILE_NNZ_CAP = 4096
-DEFAULT_TILE_CAP = 2048
-TILE_ROWS = 256
+HEAVY_CHUNK = 2048
+EXACT_ROW_MAX_LIMIT = 4096
 F_HALPERN = 1
 F_SUMSQ = 2
 
@@ -36,16 +35,13 @@ NVCC_FLAGS = [
 
 class Csr(ctypes.Structure):
     _fields_ = [("num_rows", c_int64), ("num_cols", c_int64), ("nnz", c_int64),
-                ("row_ptr", c_void_p), ("col_idx", c_void_p), ("values", c_void_p),
-                ("tile_ptr", c_void_p), ("num_tiles", c_int64),
-                ("light_tiles", c_void_p), ("num_light", c_int64),
-                ("heavy_tiles", c_void_p), ("num_heavy", c_int64),
                 ("sell_vals", c_void_p), ("sell_cols", c_void_p), ("slice_off", c_void_p),
-                ("lane_info", c_void_p), ("num_windows", c_int64),
+                ("lane_info", c_void_p), ("num_slices", c_int64),
                 ("heavy_rows", c_void_p), ("heavy_ptr", c_void_p), ("heavy_cols", c_void_p),
                 ("heavy_vals", c_void_p), ("num_heavy_rows", c_int64),
-                ("exact_row_max", c_int32), ("tile_nnz_cap", c_int32),
-                ("variant", c_int32), ("reserved", c_int32)]
+                ("chunk_first", c_void_p), ("chunk_row", c_void_p), ("num_chunks", c_int64),
+                ("chunk_sums", c_void_p), ("chunk_done", c_void_p),
+                ("exact_row_max", c_int32), ("reserved", c_int32)]
 
 
 class Src(ctypes.Structure):

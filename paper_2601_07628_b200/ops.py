@@ -34,6 +34,11 @@ class Parts:
         self.num_rows = int(num_rows)
 
 
+def _heavy(src) -> int:
+    """1 when a product also launches the heavy-row chunk kernel."""
+    return 1 if isinstance(src, Fused) and src.mat.num_chunks else 0
+
+
 def _ptr(t):
     return t.data_ptr() if t is not None and t.numel() else None
 
@@ -107,33 +112,33 @@ class CudaOps:
 
     # -- ops -----------------------------------------------------------------
     def store(self, src, out, slot=None):
-        self.launches += 2 if slot is not None else 1
+        self.launches += (2 if slot is not None else 1) + _heavy(src)
         flags = native.F_SUMSQ if slot is not None else 0
         self.lib.call("gridlp_op_store", self.src(src), _ptr(out), flags,
                       self.red(slot) if slot is not None else None, self.stream())
 
     def primal(self, src, col, it: int, halpern: bool):
-        self.launches += 1
+        self.launches += 1 + _heavy(src)
         self.lib.call("gridlp_op_primal", self.src(src), self.primal_struct(col),
                       self.step.data_ptr(), it, native.F_HALPERN if halpern else 0, self.stream())
 
     def dual(self, src, row, it: int, halpern: bool):
-        self.launches += 1
+        self.launches += 1 + _heavy(src)
         self.lib.call("gridlp_op_dual", self.src(src), self.dual_struct(row),
                       self.step.data_ptr(), it, native.F_HALPERN if halpern else 0, self.stream())
 
     def kkt_rows(self, src, row, ax, slot):
-        self.launches += 2
+        self.launches += 2 + _heavy(src)
         self.lib.call("gridlp_op_kkt_rows", self.src(src), self.dual_struct(row), _ptr(ax),
                       self.red(slot), self.stream())
 
     def kkt_cols(self, src, col, slot):
-        self.launches += 2
+        self.launches += 2 + _heavy(src)
         self.lib.call("gridlp_op_kkt_cols", self.src(src), self.primal_struct(col), _ptr(col.xpb),
                       self.step.data_ptr(), self.red(slot), self.stream())
 
     def probe(self, src, row, ax, dy_out, slot):
-        self.launches += 2
+        self.launches += 2 + _heavy(src)
         self.lib.call("gridlp_op_probe", self.src(src), self.dual_struct(row), _ptr(ax), _ptr(dy_out),
                       self.step.data_ptr(), self.red(slot), self.stream())
 

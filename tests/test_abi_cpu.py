@@ -80,28 +80,26 @@ def test_solve_without_gpu_fails_loudly():
         solve(p)
 
 
-def test_tile_directory_invariants():
-    from paper_2601_07628_b200.blocks import build_tiles
+def test_heavy_chunk_directory():
+    import torch
 
-    rng = np.random.default_rng(0)
-    lens = rng.integers(0, 40, 5000)
-    lens[[7, 100, 4000]] = [3000, 513, 9000]
-    lens[200:600] = 0
-    ptr = np.concatenate([[0], np.cumsum(lens)])
-    t = build_tiles(ptr, 512)
-    assert t[0] == 0 and t[-1] == 5000 and np.all(np.diff(t) > 0)
-    for a, b in zip(t[:-1], t[1:]):
-        nnz = ptr[b] - ptr[a]
-        if b - a == 1 and lens[a] > 512:
-            continue
-        assert b - a <= native.TILE_ROWS
-        assert nnz <= native.TILE_NNZ_CAP
-        assert np.all(lens[a:b] <= 512)
+    from paper_2601_07628_b200.blocks import chunk_directory
+
+    C = native.HEAVY_CHUNK
+    lens = np.array([513, C, C + 1, 5 * C - 3, 40 * C])
+    hptr = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32))
+    first, row = chunk_directory(hptr)
+    want = -(-lens // C)
+    np.testing.assert_array_equal(np.diff(first.numpy()), want)
+    np.testing.assert_array_equal(row.numpy(), np.repeat(np.arange(len(lens)), want))
+    f0, r0 = chunk_directory(torch.zeros(1, dtype=torch.int32))
+    assert f0.tolist() == [0] and r0.numel() == 0
 
 
 def test_sell_layout_roundtrip():
-    """The SELL-32 window layout (variant 6) holds every light row's entries
-    in their original order and every heavy row in the compact CSR."""
+    """The SELL-32 layout holds every light row's entries in their original
+    order, lanes sorted by length inside a slice, and every heavy row in the
+    compact CSR."""
     from paper_2601_07628_b200.blocks import HostCsr, build_sell
 
     rng = np.random.default_rng(1)
@@ -113,7 +111,7 @@ def test_sell_layout_roundtrip():
     col = rng.integers(0, n, int(ptr[-1]))
     val = rng.standard_normal(int(ptr[-1]))
     sd = build_sell(HostCsr(m, n, ptr, col, val), 512)
-    assert sd["num_windows"] == -(-m // 256)
+    assert sd["num_slices"] == -(-m // 32)
     seen = np.zeros(m, dtype=bool)
     off, info = sd["slice_off"], sd["lane_info"]
     for s in range(len(off) - 1):
@@ -121,8 +119,8 @@ def test_sell_layout_roundtrip():
             inf = int(info[32 * s + lane])
             if inf < 0:
                 continue
-            length, local = inf >> 8, inf & 255
-            row = (s // 8) * 256 + local
+            length, local = inf >> 8, inf & 31
+            row = s * 32 + local
             assert length == lens[row] and not seen[row]
             seen[row] = True
             idx = off[s] + lane + 32 * np.arange(length)

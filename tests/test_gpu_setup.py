@@ -56,7 +56,7 @@ def test_device_blocks_match_host(name, grid):
         np.testing.assert_array_equal(at.col[: at.nnz].cpu().numpy(), ht.col)
         np.testing.assert_array_equal(at.val[: at.nnz].cpu().numpy(), ht.val)
         for dev_csr, host_csr in ((a, hb), (at, ht)):
-            want = build_sell(host_csr, 512, window=32)
+            want = build_sell(host_csr, 512)
             got = setup.sell(dev_csr, 512)
             total = int(want["slice_off"][-1])
             np.testing.assert_array_equal(got["slice_off"].cpu().numpy(), want["slice_off"])
