@@ -51,6 +51,18 @@ CONFIGS = {
                  inequality_fraction=0.3, seed=0),
     "cfg1": dict(kind="uniform_random", num_rows=2_000, num_cols=4_000, nnz_target=20_000,
                  inequality_fraction=0.3, seed=0),
+    # device generators (paper_2601_07628_b200/synth.py)
+    "cfg3": dict(gen="powerlaw", num_rows=10_000_000, num_cols=20_000_000, nnz_target=200_000_000,
+                 inequality_fraction=0.3, seed=0),
+    "cfg3s": dict(gen="powerlaw", num_rows=1_000_000, num_cols=2_000_000, nnz_target=20_000_000,
+                  inequality_fraction=0.3, seed=0),
+    "cfg4": dict(gen="mcf", num_nodes=2_000, num_arcs=128_000, num_commodities=1_300, seed=0),
+    "cfg4s": dict(gen="mcf", num_nodes=500, num_arcs=32_000, num_commodities=200, seed=0),
+}
+WORKLOADS = {
+    "uniform_random": "reference generator uniform_random LP",
+    "powerlaw": "power-law (Chung-Lu, exponent 0.8, heavy-first) feasible LP, device generator",
+    "mcf": "block-angular multi-commodity flow LP (planted flow), device generator",
 }
 METRIC = "PDHG iters/s & time-to-1e-4 KKT (FP64) at 1/2/4/8 B200; SpMV HBM GB/s"
 
@@ -128,10 +140,30 @@ def make_problem(name):
     from paper_2601_07628_b200 import GeneratorSpec, generate
 
     t0 = time.perf_counter()
-    p = generate(GeneratorSpec(**CONFIGS[name]))
+    spec = dict(CONFIGS[name])
+    gen = spec.pop("gen", None)
+    if gen is None:
+        p = generate(GeneratorSpec(**spec))
+    else:
+        import torch
+
+        from paper_2601_07628_b200 import synth
+
+        dl = (synth.generate_powerlaw(synth.PowerLawSpec(**spec)) if gen == "powerlaw"
+              else synth.generate_mcf(synth.McfSpec(**spec)))
+        torch.cuda.synchronize()
+        log(f"[bench] device generation {time.perf_counter() - t0:.1f}s")
+        p = dl.to_problem(name)
+        del dl
+        torch.cuda.empty_cache()
     log(f"[bench] generated {name}: m={p.num_constraints} n={p.num_variables} "
         f"nnz={p.matrix.nnz} in {time.perf_counter() - t0:.1f}s")
     return p
+
+
+def workload_name(cfg: str) -> str:
+    c = CONFIGS[cfg]
+    return WORKLOADS[c.get("gen") or c["kind"]]
 
 
 def iteration_bytes(engine) -> dict:
@@ -315,13 +347,22 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         g = select_grid(p.num_constraints, p.num_variables, world)
         base = dict(n_procs=world, grid=(g.rows, g.cols), comm_backend="nccl")
+    elif args.grid:
+        R, C = (int(v) for v in args.grid.lower().split("x"))
+        base = dict(n_procs=R * C, grid=(R, C))       # virtual grid: all blocks on this GPU
     else:
         base = dict(n_procs=1)
+    if args.permutation:
+        base["permutation"] = args.permutation
+    if args.partitioning:
+        base["partitioning"] = args.partitioning
     cfg = SolverConfig(tolerance=1e-300, max_iterations=10**12, seed=0, **base)
     t0 = time.perf_counter()
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev)
     log(f"[bench] rank {rank}: setup {time.perf_counter() - t0:.1f}s {tim}")
     R, C = layout.topology.rows, layout.topology.cols
+    pdn = [v for v in (engine.per_device_nnz or []) if v >= 0]
+    balance = (max(pdn) / (sum(pdn) / len(pdn))) if pdn and sum(pdn) else None
     engine.start(eta, omega)
     for _ in range(args.warmup):
         engine.step()
@@ -403,10 +444,12 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: reference generator uniform_random LP, m={p.num_constraints} "
+        "config": {"workload": f"{args.config}: {workload_name(args.config)}, m={p.num_constraints} "
                                f"n={p.num_variables} nnz={p.matrix.nnz}, ineq 0.3, seed 0; step = 64 PDHG "
                                f"iterations + 1 KKT/restart pass",
-                   "grid": [R, C], "l2": "inputs larger than L2 (A + A^T = "
+                   "grid": [R, C], "permutation": cfg.permutation, "partitioning": cfg.partitioning,
+                   "block_nnz_max_over_mean": balance,
+                   "l2": "inputs larger than L2 (A + A^T = "
                    f"{24 * p.matrix.nnz / 1e6:.0f} MB of 126 MB L2 per iteration, streamed evict-first)",
                    "restarts_in_timed_region": restarts},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -443,6 +486,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmv", action="store_true", help="skip the SpMV-only comparison with cuSPARSE")
+    ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
+    ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")
+    ap.add_argument("--partitioning", default=None, help="SolverConfig.partitioning override")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)
     ap.add_argument("--ref-sample-iters", type=int, default=4)
     args = ap.parse_args()

@@ -282,7 +282,7 @@ int gridlp_csr_transpose(const int32_t* ptr, const int32_t* col, const double* v
                          int64_t ncols, int64_t nnz, int32_t* t_ptr, int32_t* t_col, double* t_val,
                          void* ws, size_t ws_bytes, void* stream);
 
-/* SELL-32 warp-window plan (variants 9/10): lane_info [32*ceil(nrows/32)],
+/* SELL-32 plan: lane_info [32*ceil(nrows/32)],
  * slice_off [ceil(nrows/32)+1], rank_of [nrows], heavy_rows [nrows],
  * heavy_ptr [nrows+1]; sizes (device int64[3]) = {SELL elements, heavy rows,
  * heavy nonzeros}. */
@@ -296,6 +296,49 @@ int gridlp_sell_fill(const int32_t* ptr, const int32_t* col, const double* val, 
                      const int32_t* heavy_rows, const int32_t* heavy_ptr, int64_t num_heavy,
                      int32_t* sell_col, double* sell_val, int64_t sell_elems, int32_t* heavy_col,
                      double* heavy_val, void* stream);
+
+/* --- device generators (csrc/gridlp_gen.cu) --------------------------------
+ * Synthetic LPs of the BASELINE configs with no counterpart in the
+ * reference's generators.py (cfg3 power-law, cfg4 multi-commodity flow).
+ * Every random number is u(seed, stream, a, b) = (mix(mix(mix(seed *
+ * 0x100000001B3 + stream) ^ a) ^ b) >> 11) * 2^-53 with mix = splitmix64's
+ * finaliser, so instances are independent of grid, launch shape and device
+ * and oracle/synth_oracle.py reproduces them bit for bit. */
+size_t gridlp_gen_workspace_bytes(int64_t max_items, int64_t max_rows);
+/* out = exclusive prefix sum of in[0..n) (n < 2^31). */
+int gridlp_gen_scan64(const int64_t* in, int64_t* out, int64_t n, void* ws, size_t ws_bytes, void* stream);
+/* Power-law column samples: entry k of row r (alloc_ptr[r] + k) gets
+ * c = clamp(floor((1 + u(seed,1,r,k) kappa)^5) - 1, 0, n-1). */
+int gridlp_gen_powerlaw_sample(uint64_t seed, const int64_t* alloc_ptr, int64_t m, int64_t n, double kappa,
+                               int32_t* cols, void* stream);
+/* Sort the keys of every row segment ptr[r]..ptr[r+1] ascending. */
+int gridlp_gen_sort_rows(const int64_t* ptr, int64_t m, int64_t items, const int32_t* keys_in,
+                         int32_t* keys_out, void* ws, size_t ws_bytes, void* stream);
+/* counts[r] = distinct keys of sorted row r; counts[m] = 0. */
+int gridlp_gen_dedupe_count(const int64_t* ptr, const int32_t* sorted, int64_t m, int64_t* counts,
+                            void* stream);
+/* Compact the distinct keys into out_ptr's rows; value of (r, c) is
+ * 2 u(seed,2,r,c) - 1. */
+int gridlp_gen_dedupe_fill(const int64_t* ptr, const int32_t* sorted, int64_t m, const int64_t* out_ptr,
+                           uint64_t seed, int32_t* out_cols, double* out_vals, void* stream);
+/* out_i = lo + (hi - lo) u(seed, stream_id, i, 0). */
+int gridlp_gen_uniform(uint64_t seed, uint64_t stream_id, int64_t n, double lo, double hi, double* out,
+                       void* stream);
+/* y = A x with each row summed left to right from +0.0 (scipy csr_matvec
+ * order, the reference's rhs = A x_hat, generators.py:125). */
+int gridlp_csr_spmv_seq(const int64_t* ptr, const int32_t* cols, const double* vals, int64_t m,
+                        const double* x, double* y, void* stream);
+/* Feasible row bounds around b: with probability ineq a row is ranged,
+ * [b - U[0.1,1), b + U[0.1,1)), else lo = hi = b (generators.py:120-142). */
+int gridlp_gen_row_bounds(uint64_t seed, int64_t m, double ineq, const double* b, double* lo, double* hi,
+                          void* stream);
+/* Multi-commodity flow matrix: lens[r] of the K*V conservation rows and E
+ * coupling rows (lens[m] = 0, scan for row_ptr), then the fill. */
+int gridlp_gen_mcf_row_lengths(int64_t K, int64_t V, int64_t E, const int32_t* adj_ptr, int64_t* lens,
+                               void* stream);
+int gridlp_gen_mcf_fill(int64_t K, int64_t V, int64_t E, const int32_t* adj_ptr, const int32_t* adj_arc,
+                        const int8_t* adj_sign, const int64_t* row_ptr, int32_t* cols, double* vals,
+                        void* stream);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libgridlp_b200.so"
-SOURCES = [PKG / "csrc" / "gridlp_b200.cu", PKG / "csrc" / "gridlp_setup.cu"]
+SOURCES = [PKG / "csrc" / "gridlp_b200.cu", PKG / "csrc" / "gridlp_setup.cu", PKG / "csrc" / "gridlp_gen.cu"]
 HEADER = ROOT / "include" / "gridlp_b200.h"
 
 MAX_RED = 8
@@ -95,6 +95,17 @@ SIGNATURES = {
     "gridlp_sell_plan": ([_P, c_int64, c_int32, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], c_int),
     "gridlp_sell_fill": ([_P, _P, _P, c_int64, c_int32, _P, _P, _P, _P, c_int64, _P, _P, c_int64, _P, _P, _P],
                          c_int),
+    "gridlp_gen_workspace_bytes": ([c_int64, c_int64], ctypes.c_size_t),
+    "gridlp_gen_scan64": ([_P, _P, c_int64, _P, ctypes.c_size_t, _P], c_int),
+    "gridlp_gen_powerlaw_sample": ([ctypes.c_uint64, _P, c_int64, c_int64, c_double, _P, _P], c_int),
+    "gridlp_gen_sort_rows": ([_P, c_int64, c_int64, _P, _P, _P, ctypes.c_size_t, _P], c_int),
+    "gridlp_gen_dedupe_count": ([_P, _P, c_int64, _P, _P], c_int),
+    "gridlp_gen_dedupe_fill": ([_P, _P, c_int64, _P, ctypes.c_uint64, _P, _P, _P], c_int),
+    "gridlp_gen_uniform": ([ctypes.c_uint64, ctypes.c_uint64, c_int64, c_double, c_double, _P, _P], c_int),
+    "gridlp_csr_spmv_seq": ([_P, _P, _P, c_int64, _P, _P, _P], c_int),
+    "gridlp_gen_row_bounds": ([ctypes.c_uint64, c_int64, c_double, _P, _P, _P, _P], c_int),
+    "gridlp_gen_mcf_row_lengths": ([c_int64, c_int64, c_int64, _P, _P, _P], c_int),
+    "gridlp_gen_mcf_fill": ([c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P], c_int),
 }
 
 

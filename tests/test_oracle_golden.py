@@ -135,3 +135,25 @@ class TestSolvePins:
                 want = exp["kkt"][key]
                 assert (val == want) or (math.isnan(val) and math.isnan(want)), (m, key)
             assert r.layout == exp["layout"]
+
+
+def test_synth_oracle_instances_are_feasible_and_canonical():
+    """The generator restatement: rows sorted and distinct, the planted
+    point satisfies every bound, and the package's host hash equals it."""
+    from oracle import synth_oracle
+    from paper_2601_07628_b200.synth import host_u01, mcf_graph, McfSpec
+
+    for inst in (synth_oracle.powerlaw(700, 900, 7000, seed=3), synth_oracle.mcf(15, 80, 4, seed=3)):
+        ptr, col = inst["ptr"], inst["col"]
+        for r in range(len(ptr) - 1):
+            assert np.all(np.diff(col[ptr[r]:ptr[r + 1]]) > 0)
+        import scipy.sparse as sp
+
+        A = sp.csr_matrix((inst["val"], col, ptr), shape=(len(ptr) - 1, len(inst["x_hat"])))
+        ax = A.dot(inst["x_hat"])
+        assert np.all(ax >= inst["con_lo"]) and np.all(ax <= inst["con_hi"])
+        assert np.all(inst["x_hat"] >= inst["var_lo"]) and np.all(inst["x_hat"] <= inst["var_hi"])
+    idx = np.arange(1000)
+    np.testing.assert_array_equal(host_u01(7, 3, idx), synth_oracle.u01(7, 3, idx))
+    tail, head, *_ = mcf_graph(McfSpec(30, 500, 2, seed=4))
+    assert np.all(tail != head)
