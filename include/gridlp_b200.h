@@ -53,31 +53,39 @@ enum gridlp_status {
 #define GRIDLP_MAX_PARTS 16
 /* Entries per chunk of a heavy row (one CTA sums one chunk). */
 #define GRIDLP_HEAVY_CHUNK 2048
-/* Largest exact_row_max accepted (rows up to this length are summed
- * sequentially, bit-identical to the reference). */
-#define GRIDLP_EXACT_ROW_MAX_LIMIT 4096
+/* Largest light_row_max / exact_row_max accepted. */
+#define GRIDLP_ROW_MAX_LIMIT 65536
 
 /*
- * One device-resident block A_ij (or its stored transpose) in SELL-32.
- * Replaces SparseMatrix (lp_model.py:40-150) for a LocalBlock matrix /
- * matrix_transpose (partition.py:93-122): int32 column indices, FP64
- * values — 12 B/nnz instead of the reference's 16.
+ * One device-resident block A_ij (or its stored transpose) in SELL-32 plus
+ * a compact CSR of its long rows. Replaces SparseMatrix
+ * (lp_model.py:40-150) for a LocalBlock matrix / matrix_transpose
+ * (partition.py:93-122): int32 column indices, FP64 values — 12 B/nnz
+ * instead of the reference's 16. Every row is summed in one of three ways:
  *
- * Light rows (length <= exact_row_max): rows are cut into slices of 32
- * consecutive rows; inside a slice the lanes are ordered by row length
- * (descending, stable) and entry j of lane l is stored at
- * sell_*[slice_off[s] + 32 j + l] in the row's original entry order, so a
- * warp step reads 32 consecutive values and column indices.
- * lane_info[32 s + l] = (row length << 8) | (row & 31), or -1 for an empty
- * lane (heavy row or past the end).
+ * light (length <= light_row_max): SELL-32. Rows are cut into slices of 32
+ *   consecutive rows; inside a slice the lanes are ordered by row length
+ *   (descending, stable) and entry j of lane l is stored at
+ *   sell_*[slice_off[s] + 32 j + l] in the row's original entry order, so a
+ *   warp step reads 32 consecutive values and column indices; each lane
+ *   adds its row left to right from +0.0 (bit-identical to scipy).
+ *   lane_info[32 s + l] = (row length << 8) | (row & 31), or -1 for an empty
+ *   lane (long row or past the end).
+ * long exact (light_row_max < length <= exact_row_max): compact CSR
+ *   long_rows / long_ptr / long_cols / long_vals; exact_long lists the
+ *   compact-CSR indices h of these rows. One warp per row computes 32
+ *   products per step and adds them to one running sum in entry order
+ *   (bit-identical to scipy).
+ * heavy (length > exact_row_max): the compact-CSR row h is cut into chunks
+ *   of GRIDLP_HEAVY_CHUNK entries, chunk_first[h] .. chunk_first[h+1]-1
+ *   (empty for long exact rows), chunk_row[c] = h; one CTA per chunk
+ *   tree-sums it and the last-arriving chunk CTA adds the chunk sums in
+ *   chunk order (deterministic, FP64 tolerance vs the reference).
  *
- * Heavy rows (length > exact_row_max): a compact CSR (heavy_rows /
- * heavy_ptr / heavy_cols / heavy_vals) cut into chunks of
- * GRIDLP_HEAVY_CHUNK entries: chunks chunk_first[h] .. chunk_first[h+1]-1
- * belong to heavy row h and chunk_row[c] = h. chunk_sums (one double per
- * chunk) and chunk_done (one int per heavy row, zero before the first
- * launch, left zero by every launch) are caller-owned scratch; products
- * over the same block must be stream-ordered.
+ * chunk_sums (one double per chunk) and chunk_done (one int per long row,
+ * zero before the first launch, left zero by every launch) are
+ * caller-owned scratch; products over the same block must be
+ * stream-ordered.
  */
 typedef struct gridlp_csr {
   int64_t num_rows;
@@ -88,18 +96,20 @@ typedef struct gridlp_csr {
   const int32_t* slice_off;   /* [num_slices + 1] */
   const int32_t* lane_info;   /* [32 * num_slices] */
   int64_t num_slices;         /* ceil(num_rows / 32) */
-  const int32_t* heavy_rows;  /* [num_heavy_rows] ascending */
-  const int32_t* heavy_ptr;   /* [num_heavy_rows + 1] */
-  const int32_t* heavy_cols;
-  const double* heavy_vals;
-  int64_t num_heavy_rows;
-  const int32_t* chunk_first; /* [num_heavy_rows + 1] */
+  const int32_t* long_rows;   /* [num_long_rows] ascending */
+  const int32_t* long_ptr;    /* [num_long_rows + 1] */
+  const int32_t* long_cols;
+  const double* long_vals;
+  int64_t num_long_rows;
+  const int32_t* exact_long;  /* [num_exact_long] */
+  int64_t num_exact_long;
+  const int32_t* chunk_first; /* [num_long_rows + 1] */
   const int32_t* chunk_row;   /* [num_chunks] */
   int64_t num_chunks;
   double* chunk_sums;         /* [num_chunks] scratch */
-  int32_t* chunk_done;        /* [num_heavy_rows] scratch, zero-initialised */
-  int32_t exact_row_max;      /* <= GRIDLP_EXACT_ROW_MAX_LIMIT */
-  int32_t reserved;
+  int32_t* chunk_done;        /* [num_long_rows] scratch, zero-initialised */
+  int32_t light_row_max;      /* <= GRIDLP_ROW_MAX_LIMIT */
+  int32_t exact_row_max;      /* >= light_row_max, <= GRIDLP_ROW_MAX_LIMIT */
 } gridlp_csr_t;
 
 /*
@@ -282,20 +292,20 @@ int gridlp_csr_transpose(const int32_t* ptr, const int32_t* col, const double* v
                          int64_t ncols, int64_t nnz, int32_t* t_ptr, int32_t* t_col, double* t_val,
                          void* ws, size_t ws_bytes, void* stream);
 
-/* SELL-32 plan: lane_info [32*ceil(nrows/32)],
- * slice_off [ceil(nrows/32)+1], rank_of [nrows], heavy_rows [nrows],
- * heavy_ptr [nrows+1]; sizes (device int64[3]) = {SELL elements, heavy rows,
- * heavy nonzeros}. */
-int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t exact_row_max, int32_t* lane_info,
-                     int32_t* slice_off, int32_t* rank_of, int32_t* heavy_rows, int32_t* heavy_ptr,
+/* SELL-32 plan for the rows of length <= light_row_max: lane_info
+ * [32*ceil(nrows/32)], slice_off [ceil(nrows/32)+1], rank_of [nrows]; the
+ * longer rows go to long_rows [nrows] / long_ptr [nrows+1]; sizes (device
+ * int64[3]) = {SELL elements, long rows, long-row nonzeros}. */
+int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t light_row_max, int32_t* lane_info,
+                     int32_t* slice_off, int32_t* rank_of, int32_t* long_rows, int32_t* long_ptr,
                      int64_t* sizes, void* ws, size_t ws_bytes, void* stream);
 
 /* SELL-32 fill from a CSR and its plan (padding zeroed). */
 int gridlp_sell_fill(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows,
-                     int32_t exact_row_max, const int32_t* slice_off, const int32_t* rank_of,
-                     const int32_t* heavy_rows, const int32_t* heavy_ptr, int64_t num_heavy,
-                     int32_t* sell_col, double* sell_val, int64_t sell_elems, int32_t* heavy_col,
-                     double* heavy_val, void* stream);
+                     int32_t light_row_max, const int32_t* slice_off, const int32_t* rank_of,
+                     const int32_t* long_rows, const int32_t* long_ptr, int64_t num_long,
+                     int32_t* sell_col, double* sell_val, int64_t sell_elems, int32_t* long_col,
+                     double* long_val, void* stream);
 
 /* --- device generators (csrc/gridlp_gen.cu) --------------------------------
  * Synthetic LPs of the BASELINE configs with no counterpart in the

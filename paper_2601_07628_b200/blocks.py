@@ -4,7 +4,7 @@ layout, and upload into HBM.
 Reference: permute_problem / distribute (partition.py:262-319), slice_block
 and transpose (sparse_kernels.py:27-58). The reference builds CSR with int64
 indices (16 B/nnz); a device block here is SELL-32 with int32 column indices
-and FP64 values (12 B/nnz per orientation) plus a chunked CSR of its heavy
+and FP64 values (12 B/nnz per orientation) plus a compact CSR of its long
 rows (include/gridlp_b200.h, gridlp_csr_t).
 """
 
@@ -18,7 +18,8 @@ import torch
 
 from . import native
 
-DEFAULT_EXACT_ROW_MAX = 512
+DEFAULT_LIGHT_ROW_MAX = 64      # SELL-32 lanes (one lane per row)
+DEFAULT_EXACT_ROW_MAX = 4096    # one warp per row, still sequential sums; longer rows are chunked
 
 
 @dataclass
@@ -86,18 +87,18 @@ def transpose(a: HostCsr) -> HostCsr:
     return HostCsr(a.num_cols, a.num_rows, ptr, rows[order], a.val[order])
 
 
-def build_sell(host: HostCsr, exact_row_max: int):
+def build_sell(host: HostCsr, light_row_max: int):
     """SELL-32 layout of include/gridlp_b200.h on the host (the device build,
     DeviceSetup.sell, must produce the same arrays): per 32-row slice the
     light rows sorted by length (descending, stable), stored column-major;
-    heavy rows as a compact CSR."""
+    rows longer than light_row_max as a compact CSR."""
     ptr, m = host.ptr, host.num_rows
     lens = np.diff(ptr)
-    heavy = lens > exact_row_max
+    heavy = lens > light_row_max
     ns = -(-m // 32) if m else 0
     eff = np.where(heavy, -1, lens)
     sl = np.arange(m, dtype=np.int64) // 32
-    order = np.lexsort((-eff, sl))             # slice-major, longest first, heavy last
+    order = np.lexsort((-eff, sl))             # slice-major, longest first, long rows last
     info = np.full(ns * 32, -1, dtype=np.int64)
     slen = eff[order]
     light = slen >= 0
@@ -133,25 +134,32 @@ def build_sell(host: HostCsr, exact_row_max: int):
     else:
         hcols, hvals = np.zeros(4, np.int32), np.zeros(4)
     return dict(vals=vals, cols=cols, slice_off=slice_off.astype(np.int32),
-                lane_info=info.astype(np.int32), num_slices=ns, heavy_rows=hrows.astype(np.int32),
-                heavy_ptr=hptr.astype(np.int32), heavy_cols=hcols, heavy_vals=hvals)
+                lane_info=info.astype(np.int32), num_slices=ns, long_rows=hrows.astype(np.int32),
+                long_ptr=hptr.astype(np.int32), long_cols=hcols, long_vals=hvals)
 
 
-def chunk_directory(heavy_ptr: torch.Tensor):
-    """Cut each heavy row into GRIDLP_HEAVY_CHUNK-entry chunks: returns
-    (chunk_first [nh+1], chunk_row [num_chunks]) as int32 tensors on the
-    heavy_ptr's device."""
-    hp = heavy_ptr.to(torch.int64)
-    nh = hp.numel() - 1
+def long_row_plan(long_ptr: torch.Tensor, exact_row_max: int):
+    """Split the compact CSR's long rows: rows of length <= exact_row_max are
+    summed exactly by one warp each (exact_long lists them, longest first);
+    longer rows are
+    cut into GRIDLP_HEAVY_CHUNK-entry chunks. Returns int32 tensors
+    (exact_long, chunk_first [nl+1], chunk_row [num_chunks]) on long_ptr's
+    device."""
+    hp = long_ptr.to(torch.int64)
+    nl = hp.numel() - 1
     lens = hp[1:] - hp[:-1]
-    nch = (lens + native.HEAVY_CHUNK - 1) // native.HEAVY_CHUNK
-    first = torch.zeros(nh + 1, dtype=torch.int64, device=hp.device)
-    if nh:
+    heavy = lens > exact_row_max
+    nch = torch.where(heavy, (lens + native.HEAVY_CHUNK - 1) // native.HEAVY_CHUNK, torch.zeros_like(lens))
+    first = torch.zeros(nl + 1, dtype=torch.int64, device=hp.device)
+    if nl:
         first[1:] = torch.cumsum(nch, 0)
-    rows = torch.repeat_interleave(torch.arange(nh, device=hp.device), nch) if nh else first[:0]
+    rows = torch.repeat_interleave(torch.arange(nl, device=hp.device), nch) if nl else first[:0]
     if int(first[-1]) >= 2 ** 31:
         raise ValueError("too many heavy-row chunks for int32")
-    return first.to(torch.int32), rows.to(torch.int32)
+    exact = torch.nonzero(~heavy).flatten() if nl else first[:0]
+    if exact.numel():      # longest first: the longest add chains start in the first wave
+        exact = exact[torch.sort(lens[exact], descending=True, stable=True).indices]
+    return exact.to(torch.int32), first.to(torch.int32), rows.to(torch.int32)
 
 
 class DeviceCsr:
@@ -161,43 +169,57 @@ class DeviceCsr:
     device setup returns (DeviceSetup.sell). Only the SELL arrays, the heavy
     rows' chunked CSR and the chunk scratch live in HBM."""
 
-    def __init__(self, host, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX):
-        if not 0 <= exact_row_max <= native.EXACT_ROW_MAX_LIMIT:
-            raise ValueError(f"exact_row_max must be in [0, {native.EXACT_ROW_MAX_LIMIT}]")
+    def __init__(self, host, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
+                 light_row_max: int = DEFAULT_LIGHT_ROW_MAX):
+        if not 0 <= light_row_max <= exact_row_max <= native.ROW_MAX_LIMIT:
+            raise ValueError(f"need 0 <= light_row_max <= exact_row_max <= {native.ROW_MAX_LIMIT}")
         if isinstance(host, dict):      # SELL arrays already built on the device (DeviceSetup.sell)
             self.num_rows, self.num_cols, self.nnz = host["shape"]
             sd = host
+            if sd.get("light_row_max", light_row_max) != light_row_max:
+                raise ValueError("device SELL arrays were built for another light_row_max")
         else:
             if host.nnz >= 2 ** 31 - 64:
                 raise ValueError("block nnz must be < 2^31 (int32 offsets)")
             self.num_rows, self.num_cols, self.nnz = host.num_rows, host.num_cols, host.nnz
-            sd = build_sell(host, exact_row_max)
-        self.exact_row_max = exact_row_max
+            sd = build_sell(host, light_row_max)
+        self.exact_row_max, self.light_row_max = exact_row_max, light_row_max
         # the host copy is kept only for CPU-resident blocks (the CPU test double)
         self.host = host if torch.device(device).type == "cpu" and not isinstance(host, dict) else None
         self.dev = {}
-        for k in ("vals", "cols", "slice_off", "lane_info", "heavy_rows", "heavy_ptr", "heavy_cols", "heavy_vals"):
+        for k in ("vals", "cols", "slice_off", "lane_info", "long_rows", "long_ptr", "long_cols", "long_vals"):
             a = sd[k]
             self.dev[k] = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a)).to(device)
-        self.heavy_rows = int(self.dev["heavy_rows"].numel())
-        self.dev["chunk_first"], self.dev["chunk_row"] = chunk_directory(self.dev["heavy_ptr"])
+        self.long_rows = int(self.dev["long_rows"].numel())
+        self.dev["exact_long"], self.dev["chunk_first"], self.dev["chunk_row"] = long_row_plan(
+            self.dev["long_ptr"], exact_row_max)
+        self.num_exact_long = int(self.dev["exact_long"].numel())
         self.num_chunks = int(self.dev["chunk_row"].numel())
+        self.heavy_rows = self.long_rows - self.num_exact_long
         self.dev["chunk_sums"] = torch.zeros(max(self.num_chunks, 1), dtype=torch.float64, device=device)
-        self.dev["chunk_done"] = torch.zeros(max(self.heavy_rows, 1), dtype=torch.int32, device=device)
+        self.dev["chunk_done"] = torch.zeros(max(self.long_rows, 1), dtype=torch.int32, device=device)
         self.num_slices = int(sd["num_slices"])
         ptr = lambda k: self.dev[k].data_ptr() if self.dev[k].numel() else None  # noqa: E731
         self.struct = native.Csr(self.num_rows, self.num_cols, self.nnz,
                                  ptr("vals"), ptr("cols"), ptr("slice_off"), ptr("lane_info"), self.num_slices,
-                                 ptr("heavy_rows"), ptr("heavy_ptr"), ptr("heavy_cols"), ptr("heavy_vals"),
-                                 self.heavy_rows, ptr("chunk_first"), ptr("chunk_row") if self.num_chunks else None,
-                                 self.num_chunks, ptr("chunk_sums"), ptr("chunk_done"), exact_row_max, 0)
+                                 ptr("long_rows"), ptr("long_ptr"), ptr("long_cols"), ptr("long_vals"),
+                                 self.long_rows, ptr("exact_long"), self.num_exact_long,
+                                 ptr("chunk_first"), ptr("chunk_row"), self.num_chunks, ptr("chunk_sums"),
+                                 ptr("chunk_done"), light_row_max, exact_row_max)
 
     def tensors(self):
         return tuple(self.dev.values())
 
     def slots(self) -> int:
-        """CTAs of one product (= reduction slots): heavy chunks + slice pairs."""
-        return self.num_chunks + (self.num_slices + 1) // 2 if self.num_rows else 0
+        """CTAs of one product (= reduction slots): heavy chunks + long-row
+        warp pairs + slice pairs."""
+        if not self.num_rows:
+            return 0
+        return self.num_chunks + (self.num_exact_long + 1) // 2 + (self.num_slices + 1) // 2
+
+    def launches(self) -> int:
+        """Kernels one product launches (heavy / long / SELL, when present)."""
+        return int(self.num_chunks > 0) + int(self.num_exact_long > 0) + 1
 
     def src(self, gather: torch.Tensor | None) -> native.Src:
         s = native.Src()
@@ -306,7 +328,7 @@ class DeviceSetup:
                       self.ws_bytes, self._stream())
         return DeviceCsrArrays(a.num_cols, a.num_rows, a.nnz, ptr, col, val)
 
-    def sell(self, a: DeviceCsrArrays, exact_row_max: int) -> dict:
+    def sell(self, a: DeviceCsrArrays, light_row_max: int) -> dict:
         """SELL-32 arrays built on the device (same as build_sell)."""
         dev, m = self.device, a.num_rows
         ns = (m + 31) // 32
@@ -314,24 +336,24 @@ class DeviceSetup:
         lane_info = torch.empty(max(ns * 32, 1), **i32)
         slice_off = torch.empty(ns + 1, **i32)
         rank_of = torch.empty(max(m, 1), **i32)
-        heavy_rows = torch.empty(max(m, 1), **i32)
-        heavy_ptr = torch.empty(m + 1, **i32)
+        long_rows = torch.empty(max(m, 1), **i32)
+        long_ptr = torch.empty(m + 1, **i32)
         sizes = torch.zeros(3, dtype=torch.int64, device=dev)
-        self.lib.call("gridlp_sell_plan", a.ptr.data_ptr(), m, exact_row_max, lane_info.data_ptr(),
-                      slice_off.data_ptr(), rank_of.data_ptr(), heavy_rows.data_ptr(), heavy_ptr.data_ptr(),
+        self.lib.call("gridlp_sell_plan", a.ptr.data_ptr(), m, light_row_max, lane_info.data_ptr(),
+                      slice_off.data_ptr(), rank_of.data_ptr(), long_rows.data_ptr(), long_ptr.data_ptr(),
                       sizes.data_ptr(), self.ws.data_ptr(), self.ws_bytes, self._stream())
         total, nh, hnnz = (int(v) for v in sizes.cpu().tolist())
         sell_col = torch.empty(total + 8, **i32)
         sell_val = torch.empty(total + 8, dtype=torch.float64, device=dev)
         hcol = torch.empty(hnnz + 8, **i32)
         hval = torch.empty(hnnz + 8, dtype=torch.float64, device=dev)
-        self.lib.call("gridlp_sell_fill", a.ptr.data_ptr(), a.col.data_ptr(), a.val.data_ptr(), m, exact_row_max,
-                      slice_off.data_ptr(), rank_of.data_ptr(), heavy_rows.data_ptr(), heavy_ptr.data_ptr(), nh,
+        self.lib.call("gridlp_sell_fill", a.ptr.data_ptr(), a.col.data_ptr(), a.val.data_ptr(), m, light_row_max,
+                      slice_off.data_ptr(), rank_of.data_ptr(), long_rows.data_ptr(), long_ptr.data_ptr(), nh,
                       sell_col.data_ptr(), sell_val.data_ptr(), total, hcol.data_ptr(), hval.data_ptr(),
                       self._stream())
         return dict(vals=sell_val, cols=sell_col, slice_off=slice_off, lane_info=lane_info,
-                    num_slices=ns, heavy_rows=heavy_rows[:nh].clone() if nh else heavy_rows[:0],
-                    heavy_ptr=heavy_ptr[: nh + 1].clone(), heavy_cols=hcol, heavy_vals=hval)
+                    num_slices=ns, long_rows=long_rows[:nh].clone() if nh else long_rows[:0],
+                    long_ptr=long_ptr[: nh + 1].clone(), long_cols=hcol, long_vals=hval)
 
     def release(self):
         for name in ("src_ptr", "src_col", "src_val", "inv_col", "row_perm", "ws"):

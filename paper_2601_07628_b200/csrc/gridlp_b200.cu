@@ -10,11 +10,14 @@
 //    register sum left to right from +0.0 — bit-identical to scipy's
 //    csr_matvec, the reference's kernel (sparse_kernels.py:18-24). The
 //    fused PDHG epilogue then runs in natural row order.
-//  * Rows longer than exact_row_max live in a compact CSR, cut into chunks
-//    of GRIDLP_HEAVY_CHUNK entries; one CTA per chunk tree-sums its part and
+//  * Rows longer than light_row_max live in a compact CSR. Up to
+//    exact_row_max entries one warp owns the row: 32 products per step,
+//    added to a single running sum in entry order through warp shuffles
+//    (still bit-identical to scipy). Longer rows are cut into chunks of
+//    GRIDLP_HEAVY_CHUNK entries; one CTA per chunk tree-sums its part and
 //    the last chunk CTA of a row to arrive adds the chunk sums in chunk order
-//    (deterministic) and applies the epilogue. Chunk CTAs are launched first
-//    so long rows do not form a tail.
+//    (deterministic) and applies the epilogue. The heavy and long kernels
+//    are launched before the SELL kernel so long rows do not form a tail.
 //  * No FMA contraction anywhere: every multiply/add/divide is an explicit
 //    __d*_rn so each numpy expression of the reference is reproduced
 //    operation for operation.
@@ -107,6 +110,16 @@ __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
+
+// ------------------------------------------- programmatic dependent launch
+// The heavy-chunk, long-row and SELL kernels of one product touch disjoint
+// rows, so each lets the next one start as soon as SM slots free up
+// (launch_dependents at entry) and waits for its predecessor only at its very
+// end (wait), so the last kernel's completion still implies the whole
+// product's. The first kernel of a product is launched normally, after the
+// producer of its gather vector.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ------------------------------------------------------- deterministic sums
 __device__ __forceinline__ double warp_sum(double v) {
@@ -414,6 +427,7 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
                                                               double* __restrict__ partials) {
   constexpr int U = SELL_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  pdl_launch_dependents();
   double acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
@@ -426,8 +440,8 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
   const int h = A.chunk_row[c];
   const int c0 = A.chunk_first[h];
   const int nch = A.chunk_first[h + 1] - c0;
-  const int64_t p0 = (int64_t)A.heavy_ptr[h] + (c - c0) * (int64_t)GRIDLP_HEAVY_CHUNK;
-  const int64_t pe = A.heavy_ptr[h + 1];
+  const int64_t p0 = (int64_t)A.long_ptr[h] + (c - c0) * (int64_t)GRIDLP_HEAVY_CHUNK;
+  const int64_t pe = A.long_ptr[h + 1];
   const int64_t p1 = p0 + GRIDLP_HEAVY_CHUNK < pe ? p0 + GRIDLP_HEAVY_CHUNK : pe;
   double s = 0.0;
   for (int64_t k0 = p0 + tid; k0 < p1; k0 += (int64_t)SELL_NT * U) {
@@ -436,8 +450,8 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t k = k0 + (int64_t)u * SELL_NT;
-      cc[u] = k < p1 ? ld_stream(A.heavy_cols + k, pf) : 0;
-      vv[u] = k < p1 ? ld_stream(A.heavy_vals + k, pf) : 0.0;
+      cc[u] = k < p1 ? ld_stream(A.long_cols + k, pf) : 0;
+      vv[u] = k < p1 ? ld_stream(A.long_vals + k, pf) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) xx[u] = k0 + (int64_t)u * SELL_NT < p1 ? ld_gather(g + cc[u], pl) : 0.0;
@@ -467,12 +481,91 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
       }
     }
     if (last) {
-      const int row = A.heavy_rows[h];
+      const int row = A.long_rows[h];
       const typename Op::Data d = op.load(row);
       op.row(row, t, d, acc);
     }
   }
   cta_partials<Op>(acc, partials);
+  pdl_wait();
+}
+
+// Long exact rows (light_row_max < length <= exact_row_max), one warp per
+// row, longest rows first (exact_long is sorted by length). The row is
+// walked in blocks of 32*U entries: the warp streams the block's values and
+// column indices (coalesced), gathers x and forms the rounded products in
+// parallel, parks them in shared memory, and lane 0 adds them to the running
+// sum in entry order — the sequential +0.0-seeded sum of scipy's
+// csr_matvec. The next block's gathers and the block after's streams are in
+// flight while lane 0 runs the add chain, so a row costs about one FP64
+// add latency per entry. Reduction partials follow the heavy kernel's.
+template <class Op>
+__global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
+                                                           double* __restrict__ partials) {
+  constexpr int U = SELL_U;
+  constexpr int B = 32 * U;
+  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  __shared__ double prod[SELL_WPB][B];
+  pdl_launch_dependents();
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+  op.prepare();
+  const uint64_t pf = policy_evict_first();
+  const uint64_t pl = policy_evict_last();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * SELL_WPB + warp;
+  if (q < A.num_exact_long) {
+    const int h = A.exact_long[q];
+    const int64_t p0 = A.long_ptr[h];
+    const int len = A.long_ptr[h + 1] - A.long_ptr[h];
+    const int* __restrict__ cp = A.long_cols + p0;
+    const double* __restrict__ vp = A.long_vals + p0;
+    int ca[U], cb[U];
+    double va[U], vb[U], x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = 32 * u + lane, k2 = B + 32 * u + lane;
+      ca[u] = k < len ? ld_stream(cp + k, pf) : 0;
+      va[u] = k < len ? ld_stream(vp + k, pf) : 0.0;
+      cb[u] = k2 < len ? ld_stream(cp + k2, pf) : 0;
+      vb[u] = k2 < len ? ld_stream(vp + k2, pf) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = 32 * u + lane < len ? ld_gather(g + ca[u], pl) : 0.0;
+    double s = 0.0;
+    for (int j0 = 0; j0 < len; j0 += B) {
+      double p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) p[u] = dmul(va[u], x[u]);
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < U; ++u) prod[warp][32 * u + lane] = p[u];
+      __syncwarp();
+      // in flight during the add chain: gathers of block j0+B, streams of block j0+2B
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        x[u] = j0 + B + 32 * u + lane < len ? ld_gather(g + cb[u], pl) : 0.0;
+        ca[u] = cb[u];
+        va[u] = vb[u];
+        const int k = j0 + 2 * B + 32 * u + lane;
+        cb[u] = k < len ? ld_stream(cp + k, pf) : 0;
+        vb[u] = k < len ? ld_stream(vp + k, pf) : 0.0;
+      }
+      if (lane == 0) {
+        const int cnt = len - j0 < B ? len - j0 : B;
+#pragma unroll 16
+        for (int t = 0; t < cnt; ++t) s = dadd(s, prod[warp][t]);
+      }
+    }
+    if (lane == 0) {
+      const int row = A.long_rows[h];
+      const typename Op::Data d = op.load(row);
+      op.row(row, s, d, acc);
+    }
+  }
+  cta_partials<Op>(acc, partials);
+  pdl_wait();
 }
 
 // Product + fused epilogue over the light rows of a SELL-32 block: each CTA
@@ -536,6 +629,7 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
     }
   }
   cta_partials<Op>(acc, partials);
+  pdl_wait();
 }
 
 // Row-wise epilogue over ascending-order sums of partial vectors.
@@ -591,27 +685,49 @@ int64_t rows_blocks(int64_t n) {
 
 int check_csr(const gridlp_csr_t* A) {
   if (!A) return fail(GRIDLP_ERR_ARG, "null matrix");
-  if (A->num_rows < 0 || A->num_cols < 0 || A->nnz < 0 || A->num_slices < 0 || A->num_heavy_rows < 0 ||
-      A->num_chunks < 0)
-    return fail(GRIDLP_ERR_ARG, "negative matrix dimension");
+  if (A->num_rows < 0 || A->num_cols < 0 || A->nnz < 0 || A->num_slices < 0 || A->num_long_rows < 0 ||
+      A->num_chunks < 0 || A->num_exact_long < 0 || A->num_exact_long > A->num_long_rows)
+    return fail(GRIDLP_ERR_ARG, "negative or inconsistent matrix dimension");
   if (A->nnz >= (int64_t(1) << 31)) return fail(GRIDLP_ERR_ARG, "block nnz must be < 2^31");
-  if (A->exact_row_max < 0 || A->exact_row_max > GRIDLP_EXACT_ROW_MAX_LIMIT)
-    return fail(GRIDLP_ERR_ARG, "exact_row_max out of range");
+  if (A->light_row_max < 0 || A->exact_row_max < A->light_row_max || A->exact_row_max > GRIDLP_ROW_MAX_LIMIT)
+    return fail(GRIDLP_ERR_ARG, "need 0 <= light_row_max <= exact_row_max <= GRIDLP_ROW_MAX_LIMIT");
+  if (A->num_exact_long > 0 && !A->exact_long) return fail(GRIDLP_ERR_ARG, "missing exact_long");
   if (A->num_slices != (A->num_rows + 31) / 32) return fail(GRIDLP_ERR_ARG, "num_slices must be ceil(rows/32)");
   if (A->num_rows > 0 && (!A->slice_off || !A->lane_info)) return fail(GRIDLP_ERR_ARG, "missing SELL slices");
   if (A->nnz > 0 && (!A->sell_cols || !A->sell_vals)) return fail(GRIDLP_ERR_ARG, "missing SELL arrays");
-  if (A->num_heavy_rows > 0 &&
-      (!A->heavy_rows || !A->heavy_ptr || !A->heavy_cols || !A->heavy_vals || !A->chunk_first ||
-       !A->chunk_row || !A->chunk_sums || !A->chunk_done || A->num_chunks < A->num_heavy_rows))
-    return fail(GRIDLP_ERR_ARG, "missing or inconsistent heavy-row chunk directory");
+  if (A->num_long_rows > 0 && (!A->long_rows || !A->long_ptr || !A->long_cols || !A->long_vals))
+    return fail(GRIDLP_ERR_ARG, "missing long-row CSR");
+  if (A->num_chunks > 0 && (!A->chunk_first || !A->chunk_row || !A->chunk_sums || !A->chunk_done))
+    return fail(GRIDLP_ERR_ARG, "missing heavy-row chunk directory");
   return GRIDLP_OK;
 }
 
+int64_t long_blocks(const gridlp_csr_t* A) { return (A->num_exact_long + SELL_WPB - 1) / SELL_WPB; }
+
 int64_t sell_blocks(const gridlp_csr_t* A) {
-  return A->num_rows > 0 ? A->num_chunks + (A->num_slices + SELL_WPB - 1) / SELL_WPB : 0;
+  return A->num_rows > 0 ? A->num_chunks + long_blocks(A) + (A->num_slices + SELL_WPB - 1) / SELL_WPB : 0;
 }
 
 int64_t src_rows(const gridlp_src_t* src) { return src->A ? src->A->num_rows : src->num_rows; }
+
+// Launch one of a product's kernels; `after_sibling` marks a programmatic
+// dependency on the previous kernel of the same product (see pdl_wait).
+template <class Op>
+cudaError_t launch_part(void (*kern)(gridlp_csr_t, const double*, Op, double*), int64_t blocks, bool after_sibling,
+                        cudaStream_t s, const gridlp_csr_t& M, const double* gather, Op op, double* partials) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(SELL_NT);
+  cfg.stream = s;
+  if (after_sibling) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, M, gather, op, partials);
+}
 
 template <class Op>
 int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* stream,
@@ -646,15 +762,23 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
   if (slots > 0) {
     if (src->A) {
       const gridlp_csr_t& M = *src->A;
+      const int64_t nlong = long_blocks(&M);
+      const int64_t nlight = slots - M.num_chunks - nlong;
+      bool prev = false;
+      cudaError_t e = cudaSuccess;
       if (M.num_chunks > 0) {
-        heavy_chunk_kernel<Op><<<(unsigned)M.num_chunks, SELL_NT, 0, s>>>(M, src->gather, op, partials);
-        int rc = check_launch(name);
-        if (rc) return rc;
+        e = launch_part(heavy_chunk_kernel<Op>, M.num_chunks, prev, s, M, src->gather, op, partials);
+        prev = true;
       }
-      const int64_t nlight = slots - M.num_chunks;
-      if (nlight > 0)
-        sell32_kernel<Op><<<(unsigned)nlight, SELL_NT, 0, s>>>(
-            M, src->gather, op, partials ? partials + M.num_chunks * GRIDLP_MAX_RED : nullptr);
+      if (e == cudaSuccess && nlong > 0) {
+        e = launch_part(long_row_kernel<Op>, nlong, prev, s, M, src->gather, op,
+                        partials ? partials + M.num_chunks * GRIDLP_MAX_RED : nullptr);
+        prev = true;
+      }
+      if (e == cudaSuccess && nlight > 0)
+        e = launch_part(sell32_kernel<Op>, nlight, prev, s, M, src->gather, op,
+                        partials ? partials + (M.num_chunks + nlong) * GRIDLP_MAX_RED : nullptr);
+      if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
     } else
       rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials);
     int rc = check_launch(name);

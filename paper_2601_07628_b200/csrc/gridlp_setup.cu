@@ -155,12 +155,12 @@ __global__ void transpose_scatter_kernel(const int32_t* __restrict__ ptr, const 
 }
 
 // SELL-32 plan: one warp per 32-row window. Lane order inside the slice is
-// the rank of (length descending, row ascending); heavy rows (length >
-// exact_row_max) and rows past the end take the last lanes as empty (-1).
-__global__ void sell_plan_kernel(const int32_t* __restrict__ ptr, int64_t nrows, int32_t exact_row_max,
+// the rank of (length descending, row ascending); long rows (length >
+// light_row_max) and rows past the end take the last lanes as empty (-1).
+__global__ void sell_plan_kernel(const int32_t* __restrict__ ptr, int64_t nrows, int32_t light_row_max,
                                  int32_t* __restrict__ lane_info, int32_t* __restrict__ slice_elems,
-                                 int32_t* __restrict__ rank_of, char* __restrict__ heavy_flag,
-                                 int32_t* __restrict__ heavy_len, int64_t nslices) {
+                                 int32_t* __restrict__ rank_of, char* __restrict__ long_flag,
+                                 int32_t* __restrict__ long_len, int64_t nslices) {
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= nslices) return;
@@ -168,9 +168,9 @@ __global__ void sell_plan_kernel(const int32_t* __restrict__ ptr, int64_t nrows,
   int len = 0, eff = -2;
   if (row < nrows) {
     len = ptr[row + 1] - ptr[row];
-    eff = len <= exact_row_max ? len : -1;
-    heavy_flag[row] = len > exact_row_max;
-    heavy_len[row] = len > exact_row_max ? len : 0;
+    eff = len <= light_row_max ? len : -1;
+    long_flag[row] = len > light_row_max;
+    long_len[row] = len > light_row_max ? len : 0;
   }
   int rank = 0, mx = eff > 0 ? eff : 0;
   for (int o = 0; o < 32; ++o) {
@@ -188,29 +188,29 @@ __global__ void iota_kernel(int32_t* __restrict__ out, int64_t n) {
     out[i] = (int32_t)i;
 }
 
-__global__ void gather_len_kernel(const int32_t* __restrict__ heavy_rows, const int64_t* __restrict__ count,
+__global__ void gather_len_kernel(const int32_t* __restrict__ long_rows, const int64_t* __restrict__ count,
                                   const int32_t* __restrict__ ptr, int32_t* __restrict__ hlen) {
   const int64_t n = *count;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
-    hlen[i] = i < n ? ptr[heavy_rows[i] + 1] - ptr[heavy_rows[i]] : 0;
+    hlen[i] = i < n ? ptr[long_rows[i] + 1] - ptr[long_rows[i]] : 0;
 }
 
 __global__ void sizes_kernel(const int32_t* __restrict__ slice_off, int64_t nslices, const int64_t* __restrict__ nh,
-                             const int32_t* __restrict__ heavy_ptr, int64_t* __restrict__ sizes) {
+                             const int32_t* __restrict__ long_ptr, int64_t* __restrict__ sizes) {
   sizes[0] = slice_off[nslices];
   sizes[1] = *nh;
-  sizes[2] = heavy_ptr[*nh];
+  sizes[2] = long_ptr[*nh];
 }
 
 // SELL fill: one thread per light row writes its entries column-major.
 __global__ void sell_fill_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                                 const double* __restrict__ val, int64_t nrows, int32_t exact_row_max,
+                                 const double* __restrict__ val, int64_t nrows, int32_t light_row_max,
                                  const int32_t* __restrict__ slice_off, const int32_t* __restrict__ rank_of,
                                  int32_t* __restrict__ sell_col, double* __restrict__ sell_val) {
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= nrows) return;
   const int32_t a = ptr[row], b = ptr[row + 1];
-  if (b - a > exact_row_max) return;
+  if (b - a > light_row_max) return;
   const int64_t base = (int64_t)slice_off[row >> 5] + rank_of[row];
   for (int32_t k = a; k < b; ++k) {
     sell_col[base + 32 * (int64_t)(k - a)] = col[k];
@@ -218,13 +218,13 @@ __global__ void sell_fill_kernel(const int32_t* __restrict__ ptr, const int32_t*
   }
 }
 
-__global__ void heavy_fill_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                                  const double* __restrict__ val, const int32_t* __restrict__ heavy_rows,
-                                  const int32_t* __restrict__ heavy_ptr, int64_t nh, int32_t* __restrict__ hcol,
+__global__ void long_fill_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                                  const double* __restrict__ val, const int32_t* __restrict__ long_rows,
+                                  const int32_t* __restrict__ long_ptr, int64_t nh, int32_t* __restrict__ hcol,
                                   double* __restrict__ hval) {
   for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
-    const int32_t row = heavy_rows[h];
-    const int32_t a = ptr[row], n = ptr[row + 1] - a, d = heavy_ptr[h];
+    const int32_t row = long_rows[h];
+    const int32_t a = ptr[row], n = ptr[row + 1] - a, d = long_ptr[h];
     for (int32_t j = threadIdx.x; j < n; j += blockDim.x) {
       hcol[d + j] = col[a + j];
       hval[d + j] = val[a + j];
@@ -303,14 +303,14 @@ int gridlp_csr_transpose(const int32_t* ptr, const int32_t* col, const double* v
                  "csr_transpose sort");
 }
 
-int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t exact_row_max, int32_t* lane_info,
-                     int32_t* slice_off, int32_t* rank_of, int32_t* heavy_rows, int32_t* heavy_ptr,
+int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t light_row_max, int32_t* lane_info,
+                     int32_t* slice_off, int32_t* rank_of, int32_t* long_rows, int32_t* long_ptr,
                      int64_t* sizes, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t nslices = (nrows + 31) / 32;
-  if (nrows < 0 || !slice_off || !sizes || (nrows > 0 && (!ptr || !lane_info || !rank_of || !heavy_rows || !heavy_ptr)))
+  if (nrows < 0 || !slice_off || !sizes || (nrows > 0 && (!ptr || !lane_info || !rank_of || !long_rows || !long_ptr)))
     return sfail(GRIDLP_ERR_ARG, "sell_plan: bad argument");
-  // aux: slice elements [nslices+1]; keys: heavy lengths [nrows+1]; vals: flags (char) + count
+  // aux: slice elements [nslices+1]; keys: long-row lengths [nrows+1]; vals: flags (char) + count
   if (ws_bytes < ws_total(nrows + 8, nrows + nslices + 2)) return sfail(GRIDLP_ERR_WORKSPACE, "sell_plan: workspace too small");
   Ws w = carve(ws, nrows + 8, nrows + nslices + 2);
   char* flags = reinterpret_cast<char*>(w.vals);
@@ -320,7 +320,7 @@ int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t exact_row_max, i
   int rc;
   if ((rc = cuda_ok(cudaMemsetAsync(w.aux, 0, 4 * (size_t)(nslices + 1), s), "sell_plan memset"))) return rc;
   if (nslices > 0) {
-    sell_plan_kernel<<<warps_grid(nslices), 256, 0, s>>>(ptr, nrows, exact_row_max, lane_info, w.aux, rank_of, flags,
+    sell_plan_kernel<<<warps_grid(nslices), 256, 0, s>>>(ptr, nrows, light_row_max, lane_info, w.aux, rank_of, flags,
                                                          hlen, nslices);
     if ((rc = cuda_ok(cudaGetLastError(), "sell_plan"))) return rc;
   }
@@ -331,23 +331,23 @@ int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t exact_row_max, i
   if (nrows > 0) {
     iota_kernel<<<1184, 256, 0, s>>>(ids, nrows);
     tb = w.cub_bytes;
-    if ((rc = cuda_ok(cub::DeviceSelect::Flagged(w.cub, tb, ids, flags, heavy_rows, nsel, (int)nrows, s), "select")))
+    if ((rc = cuda_ok(cub::DeviceSelect::Flagged(w.cub, tb, ids, flags, long_rows, nsel, (int)nrows, s), "select")))
       return rc;
   }
-  gather_len_kernel<<<64, 256, 0, s>>>(heavy_rows, nsel, ptr, hlen);
+  gather_len_kernel<<<64, 256, 0, s>>>(long_rows, nsel, ptr, hlen);
   if ((rc = cuda_ok(cudaGetLastError(), "sell_plan lens"))) return rc;
   tb = w.cub_bytes;
-  // heavy_ptr has room for nrows + 1 entries; scan the first (#heavy + 1) — bounded by nrows + 1
-  if ((rc = cuda_ok(cub::DeviceScan::ExclusiveSum(w.cub, tb, hlen, heavy_ptr, (int)(nrows + 1), s), "heavy scan")))
+  // long_ptr has room for nrows + 1 entries; scan the first (#long + 1) — bounded by nrows + 1
+  if ((rc = cuda_ok(cub::DeviceScan::ExclusiveSum(w.cub, tb, hlen, long_ptr, (int)(nrows + 1), s), "long scan")))
     return rc;
-  sizes_kernel<<<1, 1, 0, s>>>(slice_off, nslices, nsel, heavy_ptr, sizes);
+  sizes_kernel<<<1, 1, 0, s>>>(slice_off, nslices, nsel, long_ptr, sizes);
   return cuda_ok(cudaGetLastError(), "sell_plan sizes");
 }
 
-int gridlp_sell_fill(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows, int32_t exact_row_max,
-                     const int32_t* slice_off, const int32_t* rank_of, const int32_t* heavy_rows,
-                     const int32_t* heavy_ptr, int64_t num_heavy, int32_t* sell_col, double* sell_val,
-                     int64_t sell_elems, int32_t* heavy_col, double* heavy_val, void* stream) {
+int gridlp_sell_fill(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows, int32_t light_row_max,
+                     const int32_t* slice_off, const int32_t* rank_of, const int32_t* long_rows,
+                     const int32_t* long_ptr, int64_t num_long, int32_t* sell_col, double* sell_val,
+                     int64_t sell_elems, int32_t* long_col, double* long_val, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (nrows < 0 || sell_elems < 0 || (sell_elems > 0 && (!sell_col || !sell_val)))
     return sfail(GRIDLP_ERR_ARG, "sell_fill: bad argument");
@@ -357,15 +357,15 @@ int gridlp_sell_fill(const int32_t* ptr, const int32_t* col, const double* val, 
     if ((rc = cuda_ok(cudaMemsetAsync(sell_val, 0, 8 * (size_t)sell_elems, s), "sell_fill memset"))) return rc;
   }
   if (nrows > 0) {
-    sell_fill_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(ptr, col, val, nrows, exact_row_max, slice_off,
+    sell_fill_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(ptr, col, val, nrows, light_row_max, slice_off,
                                                                     rank_of, sell_col, sell_val);
     if ((rc = cuda_ok(cudaGetLastError(), "sell_fill"))) return rc;
   }
-  if (num_heavy > 0) {
-    heavy_fill_kernel<<<(unsigned)(num_heavy < 1184 ? num_heavy : 1184), 256, 0, s>>>(ptr, col, val, heavy_rows,
-                                                                                    heavy_ptr, num_heavy, heavy_col,
-                                                                                    heavy_val);
-    if ((rc = cuda_ok(cudaGetLastError(), "heavy_fill"))) return rc;
+  if (num_long > 0) {
+    long_fill_kernel<<<(unsigned)(num_long < 1184 ? num_long : 1184), 256, 0, s>>>(ptr, col, val, long_rows,
+                                                                                    long_ptr, num_long, long_col,
+                                                                                    long_val);
+    if ((rc = cuda_ok(cudaGetLastError(), "long_fill"))) return rc;
   }
   return GRIDLP_OK;
 }

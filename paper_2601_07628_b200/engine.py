@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .blocks import DEFAULT_EXACT_ROW_MAX, DeviceCsr, DeviceSetup, permute_matrix, slice_blocks, transpose
+from .blocks import DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, DeviceCsr, DeviceSetup, permute_matrix, slice_blocks, transpose
 from .comm import Ledger, asc_sum
 from .ops import Fused, Parts
 
@@ -65,7 +65,8 @@ class EngineOptions:
     omega_min: float = 1e-6
     omega_max: float = 1e6
     time_limit_seconds: float | None = None
-    exact_row_max: int = DEFAULT_EXACT_ROW_MAX
+    exact_row_max: int = DEFAULT_EXACT_ROW_MAX   # rows up to this length: sequential (bit-exact) sums
+    light_row_max: int = DEFAULT_LIGHT_ROW_MAX   # rows up to this length: SELL-32 lanes
     device_setup: bool = True
     use_graphs: bool = True
     graph_chunk: int = 128
@@ -229,7 +230,7 @@ class PdhgEngine:
             t = lambda a: torch.as_tensor(np.ascontiguousarray(a[r0:r1]), **f64)  # noqa: E731
             self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
-        kw = dict(exact_row_max=self.opts.exact_row_max)
+        kw = dict(exact_row_max=self.opts.exact_row_max, light_row_max=self.opts.light_row_max)
         nnz_of = {}
         for (i, j) in local:
             if on_device:
@@ -240,9 +241,9 @@ class PdhgEngine:
                 at = setup.transpose(a)
                 torch.cuda.synchronize(dev)
                 t2 = time.perf_counter()
-                sa = setup.sell(a, self.opts.exact_row_max)
+                sa = setup.sell(a, self.opts.light_row_max)
                 sa["shape"] = (a.num_rows, a.num_cols, a.nnz)
-                st = setup.sell(at, self.opts.exact_row_max)
+                st = setup.sell(at, self.opts.light_row_max)
                 st["shape"] = (at.num_rows, at.num_cols, at.nnz)
                 torch.cuda.synchronize(dev)
                 t3 = time.perf_counter()

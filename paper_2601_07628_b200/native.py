@@ -22,7 +22,7 @@ HEADER = ROOT / "include" / "gridlp_b200.h"
 MAX_RED = 8
 MAX_PARTS = 16
 HEAVY_CHUNK = 2048
-EXACT_ROW_MAX_LIMIT = 4096
+ROW_MAX_LIMIT = 65536
 F_HALPERN = 1
 F_SUMSQ = 2
 
@@ -37,11 +37,12 @@ class Csr(ctypes.Structure):
     _fields_ = [("num_rows", c_int64), ("num_cols", c_int64), ("nnz", c_int64),
                 ("sell_vals", c_void_p), ("sell_cols", c_void_p), ("slice_off", c_void_p),
                 ("lane_info", c_void_p), ("num_slices", c_int64),
-                ("heavy_rows", c_void_p), ("heavy_ptr", c_void_p), ("heavy_cols", c_void_p),
-                ("heavy_vals", c_void_p), ("num_heavy_rows", c_int64),
+                ("long_rows", c_void_p), ("long_ptr", c_void_p), ("long_cols", c_void_p),
+                ("long_vals", c_void_p), ("num_long_rows", c_int64),
+                ("exact_long", c_void_p), ("num_exact_long", c_int64),
                 ("chunk_first", c_void_p), ("chunk_row", c_void_p), ("num_chunks", c_int64),
                 ("chunk_sums", c_void_p), ("chunk_done", c_void_p),
-                ("exact_row_max", c_int32), ("reserved", c_int32)]
+                ("light_row_max", c_int32), ("exact_row_max", c_int32)]
 
 
 class Src(ctypes.Structure):

@@ -35,8 +35,9 @@ class Parts:
 
 
 def _heavy(src) -> int:
-    """1 when a product also launches the heavy-row chunk kernel."""
-    return 1 if isinstance(src, Fused) and src.mat.num_chunks else 0
+    """Extra kernels a product launches for its long rows (warp-per-row and
+    heavy-chunk kernels, when present)."""
+    return src.mat.launches() - 1 if isinstance(src, Fused) else 0
 
 
 def _ptr(t):

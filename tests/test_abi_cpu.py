@@ -80,20 +80,22 @@ def test_solve_without_gpu_fails_loudly():
         solve(p)
 
 
-def test_heavy_chunk_directory():
+def test_long_row_plan():
     import torch
 
-    from paper_2601_07628_b200.blocks import chunk_directory
+    from paper_2601_07628_b200.blocks import long_row_plan
 
     C = native.HEAVY_CHUNK
-    lens = np.array([513, C, C + 1, 5 * C - 3, 40 * C])
+    lens = np.array([65, 513, C, 4096, 4097, 5 * C - 3, 40 * C])
     hptr = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32))
-    first, row = chunk_directory(hptr)
-    want = -(-lens // C)
+    exact, first, row = long_row_plan(hptr, 4096)
+    ex = np.flatnonzero(lens <= 4096)
+    np.testing.assert_array_equal(exact.numpy(), ex[np.argsort(-lens[ex], kind="stable")])
+    want = np.where(lens > 4096, -(-lens // C), 0)
     np.testing.assert_array_equal(np.diff(first.numpy()), want)
     np.testing.assert_array_equal(row.numpy(), np.repeat(np.arange(len(lens)), want))
-    f0, r0 = chunk_directory(torch.zeros(1, dtype=torch.int32))
-    assert f0.tolist() == [0] and r0.numel() == 0
+    e0, f0, r0 = long_row_plan(torch.zeros(1, dtype=torch.int32), 4096)
+    assert f0.tolist() == [0] and r0.numel() == 0 and e0.numel() == 0
 
 
 def test_sell_layout_roundtrip():
@@ -127,8 +129,8 @@ def test_sell_layout_roundtrip():
             np.testing.assert_array_equal(sd["cols"][idx], col[ptr[row]:ptr[row + 1]])
             np.testing.assert_array_equal(sd["vals"][idx], val[ptr[row]:ptr[row + 1]])
     heavy = np.flatnonzero(lens > 512)
-    np.testing.assert_array_equal(sd["heavy_rows"], heavy)
+    np.testing.assert_array_equal(sd["long_rows"], heavy)
     assert np.all(seen == (lens <= 512))
     for h, row in enumerate(heavy):
-        a, b = sd["heavy_ptr"][h], sd["heavy_ptr"][h + 1]
-        np.testing.assert_array_equal(sd["heavy_cols"][a:b], col[ptr[row]:ptr[row + 1]])
+        a, b = sd["long_ptr"][h], sd["long_ptr"][h + 1]
+        np.testing.assert_array_equal(sd["long_cols"][a:b], col[ptr[row]:ptr[row + 1]])

@@ -20,7 +20,7 @@ from paper_2601_07628_b200.blocks import (DeviceSetup, HostCsr, build_sell, perm
 DEV = torch.device("cuda", 0)
 
 
-def _problem_with_heavy_rows():
+def _problem_with_long_rows():
     from paper_2601_07628_b200 import LpProblem, SparseMatrix
 
     rng = np.random.default_rng(5)
@@ -40,7 +40,7 @@ CASES = [("u1000", (1, 1)), ("u1000", (2, 2)), ("tall", (2, 3)), ("heavy", (1, 1
 
 @pytest.mark.parametrize("name,grid", CASES)
 def test_device_blocks_match_host(name, grid):
-    p = _problem_with_heavy_rows() if name == "heavy" else golden_problem(load_npz("layouts.npz"), name + "_")
+    p = _problem_with_long_rows() if name == "heavy" else golden_problem(load_npz("layouts.npz"), name + "_")
     lay = build_layout(p, grid[0] * grid[1], grid=GridTopology(*grid), seed=3)
     host = slice_blocks(permute_matrix(p.matrix, lay), lay)
     setup = DeviceSetup(p, lay, DEV)
@@ -64,11 +64,11 @@ def test_device_blocks_match_host(name, grid):
                                           want["lane_info"])
             np.testing.assert_array_equal(got["cols"][:total].cpu().numpy(), want["cols"][:total])
             np.testing.assert_array_equal(got["vals"][:total].cpu().numpy(), want["vals"][:total])
-            np.testing.assert_array_equal(got["heavy_rows"].cpu().numpy(), want["heavy_rows"])
-            np.testing.assert_array_equal(got["heavy_ptr"].cpu().numpy(), want["heavy_ptr"])
-            hn = int(want["heavy_ptr"][-1])
-            np.testing.assert_array_equal(got["heavy_cols"][:hn].cpu().numpy(), want["heavy_cols"][:hn])
-            np.testing.assert_array_equal(got["heavy_vals"][:hn].cpu().numpy(), want["heavy_vals"][:hn])
+            np.testing.assert_array_equal(got["long_rows"].cpu().numpy(), want["long_rows"])
+            np.testing.assert_array_equal(got["long_ptr"].cpu().numpy(), want["long_ptr"])
+            hn = int(want["long_ptr"][-1])
+            np.testing.assert_array_equal(got["long_cols"][:hn].cpu().numpy(), want["long_cols"][:hn])
+            np.testing.assert_array_equal(got["long_vals"][:hn].cpu().numpy(), want["long_vals"][:hn])
 
 
 def test_device_and_host_setup_solve_identically(golden_cfg1):
