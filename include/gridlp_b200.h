@@ -292,6 +292,14 @@ int gridlp_csr_transpose(const int32_t* ptr, const int32_t* col, const double* v
                          int64_t ncols, int64_t nnz, int32_t* t_ptr, int32_t* t_col, double* t_val,
                          void* ws, size_t ws_bytes, void* stream);
 
+/* out row r = row row_order[r] of the input (identity when NULL) with every
+ * column index c replaced by col_label[c] (identity when NULL); entries keep
+ * their order, so row sums are unchanged. Used to put a block in the
+ * engine's internal length-sorted row/column order. */
+int gridlp_csr_permute(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows,
+                       const int32_t* row_order, const int32_t* col_label, int32_t* out_ptr,
+                       int32_t* out_col, double* out_val, void* ws, size_t ws_bytes, void* stream);
+
 /* SELL-32 plan for the rows of length <= light_row_max: lane_info
  * [32*ceil(nrows/32)], slice_off [ceil(nrows/32)+1], rank_of [nrows]; the
  * longer rows go to long_rows [nrows] / long_ptr [nrows+1]; sizes (device

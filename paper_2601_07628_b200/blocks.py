@@ -87,6 +87,30 @@ def transpose(a: HostCsr) -> HostCsr:
     return HostCsr(a.num_cols, a.num_rows, ptr, rows[order], a.val[order])
 
 
+def permute_csr(a: HostCsr, row_order=None, col_label=None) -> HostCsr:
+    """Host twin of gridlp_csr_permute: out row r = row row_order[r], column
+    c relabelled col_label[c], entry order kept (row sums unchanged)."""
+    lens = np.diff(a.ptr)
+    order = np.arange(a.num_rows) if row_order is None else np.asarray(row_order, np.int64)
+    nl = lens[order]
+    ptr = np.concatenate([[0], np.cumsum(nl)]).astype(np.int64)
+    src = np.repeat(a.ptr[:-1][order] - ptr[:-1], nl) + np.arange(int(ptr[-1]), dtype=np.int64)
+    col = a.col[src] if col_label is None else np.asarray(col_label, np.int64)[a.col[src]]
+    return HostCsr(a.num_rows, a.num_cols, ptr, col, a.val[src])
+
+
+def length_order(lens: np.ndarray) -> np.ndarray:
+    """Internal order of a band: longest first, stable (SELL-32 slices then
+    hold rows of nearly equal length)."""
+    return np.argsort(-np.asarray(lens, np.int64), kind="stable")
+
+
+def inverse_order(order: np.ndarray) -> np.ndarray:
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order), dtype=order.dtype)
+    return inv
+
+
 def build_sell(host: HostCsr, light_row_max: int):
     """SELL-32 layout of include/gridlp_b200.h on the host (the device build,
     DeviceSetup.sell, must produce the same arrays): per 32-row slice the
@@ -327,6 +351,19 @@ class DeviceSetup:
                       a.num_cols, a.nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), self.ws.data_ptr(),
                       self.ws_bytes, self._stream())
         return DeviceCsrArrays(a.num_cols, a.num_rows, a.nnz, ptr, col, val)
+
+    def permute(self, a: DeviceCsrArrays, row_order: torch.Tensor | None,
+                col_label: torch.Tensor | None) -> DeviceCsrArrays:
+        """Rows gathered by row_order, columns relabelled by col_label (int32
+        device tensors or None), entry order kept (gridlp_csr_permute)."""
+        ptr = torch.empty(a.num_rows + 1, dtype=torch.int32, device=self.device)
+        col = torch.empty(a.nnz + 8, dtype=torch.int32, device=self.device)
+        val = torch.empty(a.nnz + 8, dtype=torch.float64, device=self.device)
+        p = lambda t: t.data_ptr() if t is not None and t.numel() else None  # noqa: E731
+        self.lib.call("gridlp_csr_permute", a.ptr.data_ptr(), a.col.data_ptr(), a.val.data_ptr(), a.num_rows,
+                      p(row_order), p(col_label), ptr.data_ptr(), col.data_ptr(), val.data_ptr(), self.ws.data_ptr(),
+                      self.ws_bytes, self._stream())
+        return DeviceCsrArrays(a.num_rows, a.num_cols, a.nnz, ptr, col, val)
 
     def sell(self, a: DeviceCsrArrays, light_row_max: int) -> dict:
         """SELL-32 arrays built on the device (same as build_sell)."""

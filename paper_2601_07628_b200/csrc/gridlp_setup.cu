@@ -154,6 +154,35 @@ __global__ void transpose_scatter_kernel(const int32_t* __restrict__ ptr, const 
   }
 }
 
+// Row gather + column relabel (internal length-sorted order):
+// out row r = in row order[r] with every column index c replaced by
+// label[c]; the entries keep their order, so every row sum is unchanged.
+__global__ void permute_len_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ order, int64_t nrows,
+                                   int32_t* __restrict__ lens) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    if (r == nrows) { lens[r] = 0; continue; }
+    const int32_t src = order ? order[r] : (int32_t)r;
+    lens[r] = ptr[src + 1] - ptr[src];
+  }
+}
+
+__global__ void permute_fill_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                                    const double* __restrict__ val, const int32_t* __restrict__ order,
+                                    const int32_t* __restrict__ label, int64_t nrows,
+                                    const int32_t* __restrict__ out_ptr, int32_t* __restrict__ out_col,
+                                    double* __restrict__ out_val) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nrows) return;
+  const int32_t src = order ? order[w] : (int32_t)w;
+  const int32_t a = ptr[src], n = ptr[src + 1] - a, d = out_ptr[w];
+  for (int32_t k = lane; k < n; k += 32) {
+    const int32_t c = col[a + k];
+    out_col[d + k] = label ? label[c] : c;
+    out_val[d + k] = val[a + k];
+  }
+}
+
 // SELL-32 plan: one warp per 32-row window. Lane order inside the slice is
 // the rank of (length descending, row ascending); long rows (length >
 // light_row_max) and rows past the end take the last lanes as empty (-1).
@@ -301,6 +330,25 @@ int gridlp_csr_transpose(const int32_t* ptr, const int32_t* col, const double* v
   return cuda_ok(cub::DeviceSegmentedSort::SortPairs(w.cub, tb, w.keys, t_col, w.vals, t_val, (int)nnz, (int)ncols,
                                                      t_ptr, t_ptr + 1, s),
                  "csr_transpose sort");
+}
+
+int gridlp_csr_permute(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows,
+                       const int32_t* row_order, const int32_t* col_label, int32_t* out_ptr, int32_t* out_col,
+                       double* out_val, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nrows < 0 || !out_ptr || (nrows > 0 && !ptr)) return sfail(GRIDLP_ERR_ARG, "csr_permute: bad argument");
+  if (ws_bytes < ws_total(1, nrows)) return sfail(GRIDLP_ERR_WORKSPACE, "csr_permute: workspace too small");
+  Ws w = carve(ws, 1, nrows);
+  permute_len_kernel<<<warps_grid((nrows + 32) / 32 + 1), 256, 0, s>>>(ptr, row_order, nrows, w.aux);
+  int rc = cuda_ok(cudaGetLastError(), "csr_permute lens");
+  if (rc) return rc;
+  size_t tb = w.cub_bytes;
+  if ((rc = cuda_ok(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.aux, out_ptr, (int)(nrows + 1), s), "permute scan")))
+    return rc;
+  if (nrows == 0) return GRIDLP_OK;
+  permute_fill_kernel<<<warps_grid(nrows), 256, 0, s>>>(ptr, col, val, row_order, col_label, nrows, out_ptr, out_col,
+                                                       out_val);
+  return cuda_ok(cudaGetLastError(), "csr_permute fill");
 }
 
 int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t light_row_max, int32_t* lane_info,

@@ -30,7 +30,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .blocks import DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, DeviceCsr, DeviceSetup, permute_matrix, slice_blocks, transpose
+from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, DeviceCsr, DeviceSetup, inverse_order,
+                     length_order, permute_csr, permute_matrix, slice_blocks, transpose)
 from .comm import Ledger, asc_sum
 from .ops import Fused, Parts
 
@@ -67,6 +68,7 @@ class EngineOptions:
     time_limit_seconds: float | None = None
     exact_row_max: int = DEFAULT_EXACT_ROW_MAX   # rows up to this length: sequential (bit-exact) sums
     light_row_max: int = DEFAULT_LIGHT_ROW_MAX   # rows up to this length: SELL-32 lanes
+    sorted_order: bool = True    # internal length-sorted row/column order per band (CUDA only)
     device_setup: bool = True
     use_graphs: bool = True
     graph_chunk: int = 128
@@ -206,6 +208,7 @@ class PdhgEngine:
             self.per_device_nnz = [host_blocks[c].nnz for c in lay.topology.coords()]
             self.setup_h2d_bytes = 0
         cp, rp = lay.perm.col_perm, lay.perm.row_perm
+        self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order)
         f64 = dict(dtype=torch.float64, device=dev)
         obj = np.asarray(problem.objective, np.float64)[cp]
         vlo = np.asarray(problem.var_lower, np.float64)[cp]
@@ -219,7 +222,7 @@ class PdhgEngine:
         for j in self.local_cols:
             c0, c1 = lay.col_range(j)
             n = c1 - c0
-            t = lambda a: torch.as_tensor(np.ascontiguousarray(a[c0:c1]), **f64)  # noqa: E731
+            t = lambda a: torch.as_tensor(np.ascontiguousarray(self._to_internal_col(j, a[c0:c1])), **f64)  # noqa: E731
             self.cols[j] = ColState(j, n, t(obj), t(vlo), t(vhi), torch.zeros(n, **f64),
                                     torch.zeros(n, **f64), torch.zeros(n, **f64),
                                     torch.zeros(n, **f64), torch.zeros(n, **f64),
@@ -227,7 +230,7 @@ class PdhgEngine:
         for i in self.local_rows:
             r0, r1 = lay.row_range(i)
             m = r1 - r0
-            t = lambda a: torch.as_tensor(np.ascontiguousarray(a[r0:r1]), **f64)  # noqa: E731
+            t = lambda a: torch.as_tensor(np.ascontiguousarray(self._to_internal_row(i, a[r0:r1])), **f64)  # noqa: E731
             self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
         kw = dict(exact_row_max=self.opts.exact_row_max, light_row_max=self.opts.light_row_max)
@@ -239,6 +242,13 @@ class PdhgEngine:
                 torch.cuda.synchronize(dev)
                 t1 = time.perf_counter()
                 at = setup.transpose(a)
+                if self.sorted:
+                    # internal order: A_ij rows by sigma_i, columns by tau_j (and the
+                    # transpose's the other way round); the transpose is taken first
+                    # so its entries stay in layout row order (row sums unchanged)
+                    d32 = lambda o: torch.from_numpy(o.astype(np.int32)).to(dev)  # noqa: E731
+                    a = setup.permute(a, d32(self.row_order[i]), d32(self.col_inv[j]))
+                    at = setup.permute(at, d32(self.col_order[j]), d32(self.row_inv[i]))
                 torch.cuda.synchronize(dev)
                 t2 = time.perf_counter()
                 sa = setup.sell(a, self.opts.light_row_max)
@@ -255,7 +265,11 @@ class PdhgEngine:
                 nnz_of[(i, j)] = self.blocks[(i, j)].A.nnz
             else:
                 hb = host_blocks[(i, j)]
-                self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(transpose(hb), dev, **kw))
+                ht = transpose(hb)
+                if self.sorted:
+                    hb = permute_csr(hb, self.row_order[i], self.col_inv[j])
+                    ht = permute_csr(ht, self.col_order[j], self.row_inv[i])
+                self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(ht, dev, **kw))
         if on_device:
             setup.release()
             del setup
@@ -272,6 +286,52 @@ class PdhgEngine:
                 t.numel() * t.element_size() for c in self.cols.values() for t in (c.c, c.lo, c.hi))
                 + sum(t.numel() * t.element_size() for r in self.rows.values() for t in (r.lo, r.hi)))
         self.passes = 0
+
+    # ------------------------------------------------- internal order
+    def _internal_orders(self, problem, enabled: bool):
+        """Per grid row band i, sigma_i = the band's rows by full row length
+        (longest first, stable); per grid column band j, tau_j = the band's
+        columns by column count. Blocks and vectors live in this order on the
+        device, so every SELL-32 slice holds rows of nearly equal length;
+        entry order inside a row is untouched, so products stay bit-identical
+        and iterates are the reference's up to the permutation. Computed
+        from the host problem, identically on every rank."""
+        self.sorted = bool(enabled)
+        self.row_order, self.row_inv, self.col_order, self.col_inv = {}, {}, {}, {}
+        if not self.sorted:
+            return
+        lay = self.layout
+        A = problem.matrix
+        row_len = np.diff(np.asarray(A.row_offsets, np.int64))[lay.perm.row_perm]
+        col_len = np.bincount(np.asarray(A.col_indices, np.int64), minlength=int(A.num_cols))[lay.perm.col_perm]
+        for i in range(self.R):
+            r0, r1 = lay.row_range(i)
+            self.row_order[i] = length_order(row_len[r0:r1])
+            self.row_inv[i] = inverse_order(self.row_order[i])
+        for j in range(self.C):
+            c0, c1 = lay.col_range(j)
+            self.col_order[j] = length_order(col_len[c0:c1])
+            self.col_inv[j] = inverse_order(self.col_order[j])
+
+    def _to_internal_col(self, j, a):
+        return a[self.col_order[j]] if self.sorted else a
+
+    def _to_internal_row(self, i, a):
+        return a[self.row_order[i]] if self.sorted else a
+
+    def _from_internal_col(self, j, a):
+        if not self.sorted:
+            return a
+        out = np.empty_like(a)
+        out[self.col_order[j]] = a
+        return out
+
+    def _from_internal_row(self, i, a):
+        if not self.sorted:
+            return a
+        out = np.empty_like(a)
+        out[self.row_order[i]] = a
+        return out
 
     def _assign_slots(self):
         s = {}
@@ -369,7 +429,8 @@ class PdhgEngine:
         R, C = float(self.R), float(self.C)
         for j, col in self.cols.items():
             c0, c1 = lay.col_range(j)
-            col.v.copy_(torch.as_tensor(np.ascontiguousarray(probe[c0:c1], dtype=np.float64)))
+            col.v.copy_(torch.as_tensor(np.ascontiguousarray(
+                self._to_internal_col(j, np.asarray(probe[c0:c1], dtype=np.float64)))))
         est = 0.0
         for _ in range(iters):
             for i, row in self.rows.items():
@@ -537,8 +598,8 @@ class PdhgEngine:
         return self._g_sum(tab, 0, self.R), self._g_sum(tab, 1, self.C)
 
     def _snapshot_xy(self):
-        xs = {j: c.x.detach().cpu().numpy().copy() for j, c in self.cols.items()}
-        ys = {i: r.y.detach().cpu().numpy().copy() for i, r in self.rows.items()}
+        xs = {j: self._from_internal_col(j, c.x.detach().cpu().numpy().copy()) for j, c in self.cols.items()}
+        ys = {i: self._from_internal_row(i, r.y.detach().cpu().numpy().copy()) for i, r in self.rows.items()}
         return xs, ys
 
     # The loop of iterate_epoch (pdhg_engine.py:364-476), split so a caller
@@ -658,8 +719,8 @@ class PdhgEngine:
         """x blocks of grid columns (from devices (0, j)) and y blocks of grid
         rows (from (i, 0)) as host arrays (solver_driver.py:246-248)."""
         if self.comm.kind == "virtual":
-            xs = [self.cols[j].x.cpu().numpy() for j in range(self.C)]
-            ys = [self.rows[i].y.cpu().numpy() for i in range(self.R)]
+            xs = [self._from_internal_col(j, self.cols[j].x.cpu().numpy()) for j in range(self.C)]
+            ys = [self._from_internal_row(i, self.rows[i].y.cpu().numpy()) for i in range(self.R)]
             return xs, ys
         lay = self.layout
         lengths = {(i, j): max(int(lay.col_cuts[j + 1] - lay.col_cuts[j]), int(lay.row_cuts[i + 1] - lay.row_cuts[i]))
@@ -671,6 +732,6 @@ class PdhgEngine:
         del lengths
         xa = self.comm.gather_vectors(xl, xlen, self.device)
         ya = self.comm.gather_vectors(yl, ylen, self.device)
-        xs = [xa[(0, j)].cpu().numpy() for j in range(self.C)]
-        ys = [ya[(i, 0)].cpu().numpy() for i in range(self.R)]
+        xs = [self._from_internal_col(j, xa[(0, j)].cpu().numpy()) for j in range(self.C)]
+        ys = [self._from_internal_row(i, ya[(i, 0)].cpu().numpy()) for i in range(self.R)]
         return xs, ys

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from paper_2601_07628_b200 import GridTopology, build_layout  # noqa: E402
+from paper_2601_07628_b200 import GridTopology, build_layout, native  # noqa: E402
 from paper_2601_07628_b200.blocks import (DeviceSetup, HostCsr, build_sell, permute_matrix,  # noqa: E402
                                           slice_blocks, transpose)
 
@@ -82,3 +82,46 @@ def test_device_and_host_setup_solve_identically(golden_cfg1):
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
     assert a.layout == b.layout and a.counters == b.counters
+
+
+def test_device_permute_matches_host():
+    from paper_2601_07628_b200.blocks import DeviceCsrArrays, inverse_order, length_order, permute_csr
+
+    rng = np.random.default_rng(5)
+    m, n = 700, 900
+    lens = rng.integers(0, 40, m)
+    ptr = np.concatenate([[0], np.cumsum(lens)])
+    col = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int64)
+    val = rng.standard_normal(len(col))
+    h = HostCsr(m, n, ptr, col, val)
+    order = length_order(lens)
+    label = inverse_order(rng.permutation(n))
+    want = permute_csr(h, order, label)
+    setup = DeviceSetup.__new__(DeviceSetup)
+    setup.lib, setup.device = native.load(), DEV
+    wsb = int(setup.lib._lib.gridlp_setup_workspace_bytes(len(col) + 64, m + 64))
+    setup.ws, setup.ws_bytes = torch.empty(wsb, dtype=torch.uint8, device=DEV), wsb
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(DEV)  # noqa: E731
+    a = DeviceCsrArrays(m, n, len(col), t(ptr, np.int32), t(np.concatenate([col, np.zeros(8)]), np.int32),
+                        t(np.concatenate([val, np.zeros(8)]), np.float64))
+    got = setup.permute(a, t(order, np.int32), t(label, np.int32))
+    np.testing.assert_array_equal(got.ptr.cpu().numpy(), want.ptr)
+    np.testing.assert_array_equal(got.col[: len(col)].cpu().numpy(), want.col)
+    np.testing.assert_array_equal(got.val[: len(col)].cpu().numpy(), want.val)
+
+
+@pytest.mark.parametrize("grid", [(1, 1), (2, 3)])
+def test_sorted_internal_order_solves_like_natural(grid):
+    """The internal length-sorted order only permutes storage: same status,
+    iterations and restarts, and x / y equal up to reduction-order rounding."""
+    from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate
+    from paper_2601_07628_b200.api import _solve
+
+    p = generate(GeneratorSpec(kind="uniform_random", num_rows=600, num_cols=900, nnz_target=9000,
+                               inequality_fraction=0.3, seed=4))
+    cfg = SolverConfig(tolerance=1e-6, seed=4, n_procs=grid[0] * grid[1], grid=grid)
+    a = _solve(p, cfg, engine_overrides={"sorted_order": True})
+    b = _solve(p, cfg, engine_overrides={"sorted_order": False})
+    assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+    np.testing.assert_allclose(a.x, b.x, rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(a.y, b.y, rtol=1e-9, atol=1e-9)
