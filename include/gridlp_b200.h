@@ -292,6 +292,10 @@ int gridlp_csr_transpose(const int32_t* ptr, const int32_t* col, const double* v
                          int64_t ncols, int64_t nnz, int32_t* t_ptr, int32_t* t_col, double* t_val,
                          void* ws, size_t ws_bytes, void* stream);
 
+/* counts[c] = entries with column c (exact histogram; the column lengths
+ * that order the engine's internal column order). */
+int gridlp_col_counts(const int32_t* col, int64_t nnz, int64_t ncols, int32_t* counts, void* stream);
+
 /* out row r = row row_order[r] of the input (identity when NULL) with every
  * column index c replaced by col_label[c] (identity when NULL); entries keep
  * their order, so row sums are unchanged. Used to put a block in the

@@ -101,8 +101,11 @@ def permute_csr(a: HostCsr, row_order=None, col_label=None) -> HostCsr:
 
 def length_order(lens: np.ndarray) -> np.ndarray:
     """Internal order of a band: longest first, stable (SELL-32 slices then
-    hold rows of nearly equal length)."""
-    return np.argsort(-np.asarray(lens, np.int64), kind="stable")
+    hold rows of nearly equal length). Lengths are clipped at 65535 (longer
+    rows are never SELL lanes) so numpy's stable sort is an O(n) radix sort
+    on uint16 keys."""
+    lens = np.minimum(np.asarray(lens, np.int64), 65535)
+    return np.argsort((65535 - lens).astype(np.uint16), kind="stable")
 
 
 def inverse_order(order: np.ndarray) -> np.ndarray:
@@ -302,6 +305,7 @@ class DeviceSetup:
         if n >= 2 ** 31 - 1 or m >= 2 ** 31 - 1:
             raise ValueError("device setup needs < 2^31 rows and columns per matrix")
         nnz = int(len(A.values))
+        self.nnz, self.n = nnz, n
 
         def t(a, dt):
             return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
@@ -351,6 +355,14 @@ class DeviceSetup:
                       a.num_cols, a.nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), self.ws.data_ptr(),
                       self.ws_bytes, self._stream())
         return DeviceCsrArrays(a.num_cols, a.num_rows, a.nnz, ptr, col, val)
+
+    def col_counts(self) -> np.ndarray:
+        """Entries per column of the uploaded original matrix (device
+        histogram, host int64 result)."""
+        n = int(self.inv_col.numel()) if self.n else 0
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        self.lib.call("gridlp_col_counts", self.src_col.data_ptr(), self.nnz, n, out.data_ptr(), self._stream())
+        return out[:n].cpu().numpy().astype(np.int64)
 
     def permute(self, a: DeviceCsrArrays, row_order: torch.Tensor | None,
                 col_label: torch.Tensor | None) -> DeviceCsrArrays:

@@ -332,6 +332,16 @@ int gridlp_csr_transpose(const int32_t* ptr, const int32_t* col, const double* v
                  "csr_transpose sort");
 }
 
+int gridlp_col_counts(const int32_t* col, int64_t nnz, int64_t ncols, int32_t* counts, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nnz < 0 || ncols < 0 || (ncols > 0 && !counts) || (nnz > 0 && !col))
+    return sfail(GRIDLP_ERR_ARG, "col_counts: bad argument");
+  int rc = cuda_ok(cudaMemsetAsync(counts, 0, 4 * (size_t)ncols, s), "col_counts memset");
+  if (rc || nnz == 0) return rc;
+  col_hist_kernel<<<1184, 256, 0, s>>>(col, nnz, counts);
+  return cuda_ok(cudaGetLastError(), "col_counts");
+}
+
 int gridlp_csr_permute(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows,
                        const int32_t* row_order, const int32_t* col_label, int32_t* out_ptr, int32_t* out_col,
                        double* out_val, void* ws, size_t ws_bytes, void* stream) {

@@ -208,7 +208,10 @@ class PdhgEngine:
             self.per_device_nnz = [host_blocks[c].nnz for c in lay.topology.coords()]
             self.setup_h2d_bytes = 0
         cp, rp = lay.perm.col_perm, lay.perm.row_perm
-        self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order)
+        t0 = time.perf_counter()
+        self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order, setup if on_device else None)
+        tm["setup_orders_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
         f64 = dict(dtype=torch.float64, device=dev)
         obj = np.asarray(problem.objective, np.float64)[cp]
         vlo = np.asarray(problem.var_lower, np.float64)[cp]
@@ -234,6 +237,7 @@ class PdhgEngine:
             self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
         kw = dict(exact_row_max=self.opts.exact_row_max, light_row_max=self.opts.light_row_max)
+        tm["setup_vectors_s"] = time.perf_counter() - t0
         nnz_of = {}
         for (i, j) in local:
             if on_device:
@@ -263,6 +267,7 @@ class PdhgEngine:
                 del a, at
                 self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(sa, dev, **kw), DeviceCsr(st, dev, **kw))
                 nnz_of[(i, j)] = self.blocks[(i, j)].A.nnz
+                tm["setup_csr_s"] = tm.get("setup_csr_s", 0.0) + time.perf_counter() - t3
             else:
                 hb = host_blocks[(i, j)]
                 ht = transpose(hb)
@@ -271,9 +276,11 @@ class PdhgEngine:
                     ht = permute_csr(ht, self.col_order[j], self.row_inv[i])
                 self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(ht, dev, **kw))
         if on_device:
+            t0 = time.perf_counter()
             setup.release()
             del setup
             torch.cuda.empty_cache()
+            tm["setup_release_s"] = time.perf_counter() - t0
             coords = lay.topology.coords()
             self.per_device_nnz = [nnz_of.get(c, -1) for c in coords] if self.comm.kind == "virtual" else None
         del host_blocks
@@ -288,7 +295,7 @@ class PdhgEngine:
         self.passes = 0
 
     # ------------------------------------------------- internal order
-    def _internal_orders(self, problem, enabled: bool):
+    def _internal_orders(self, problem, enabled: bool, setup=None):
         """Per grid row band i, sigma_i = the band's rows by full row length
         (longest first, stable); per grid column band j, tau_j = the band's
         columns by column count. Blocks and vectors live in this order on the
@@ -303,7 +310,8 @@ class PdhgEngine:
         lay = self.layout
         A = problem.matrix
         row_len = np.diff(np.asarray(A.row_offsets, np.int64))[lay.perm.row_perm]
-        col_len = np.bincount(np.asarray(A.col_indices, np.int64), minlength=int(A.num_cols))[lay.perm.col_perm]
+        counts = setup.col_counts() if setup is not None else np.bincount(A.col_indices, minlength=int(A.num_cols))
+        col_len = counts[lay.perm.col_perm]
         for i in range(self.R):
             r0, r1 = lay.row_range(i)
             self.row_order[i] = length_order(row_len[r0:r1])

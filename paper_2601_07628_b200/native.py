@@ -93,6 +93,7 @@ SIGNATURES = {
     "gridlp_block_fill": ([_P, _P, _P, _P, c_int64, _P, c_int32, c_int32, _P, c_int64, _P, _P, _P,
                            ctypes.c_size_t, _P], c_int),
     "gridlp_csr_transpose": ([_P, _P, _P, c_int64, c_int64, c_int64, _P, _P, _P, _P, ctypes.c_size_t, _P], c_int),
+    "gridlp_col_counts": ([_P, c_int64, c_int64, _P, _P], c_int),
     "gridlp_csr_permute": ([_P, _P, _P, c_int64, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], c_int),
     "gridlp_sell_plan": ([_P, c_int64, c_int32, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], c_int),
     "gridlp_sell_fill": ([_P, _P, _P, c_int64, c_int32, _P, _P, _P, _P, c_int64, _P, _P, c_int64, _P, _P, _P],
