@@ -18,7 +18,7 @@ import torch
 
 from . import native
 
-DEFAULT_LIGHT_ROW_MAX = 64      # SELL-32 lanes (one lane per row)
+DEFAULT_LIGHT_ROW_MAX = 128     # SELL-32 lanes (one lane per row); sweep in profiles/r1/row_classes.md
 DEFAULT_EXACT_ROW_MAX = 4096    # one warp per row, still sequential sums; longer rows are chunked
 
 
@@ -99,13 +99,21 @@ def permute_csr(a: HostCsr, row_order=None, col_label=None) -> HostCsr:
     return HostCsr(a.num_rows, a.num_cols, ptr, col, a.val[src])
 
 
+LENGTH_BUCKETS_PER_OCTAVE = 8
+
+
 def length_order(lens: np.ndarray) -> np.ndarray:
-    """Internal order of a band: longest first, stable (SELL-32 slices then
-    hold rows of nearly equal length). Lengths are clipped at 65535 (longer
-    rows are never SELL lanes) so numpy's stable sort is an O(n) radix sort
-    on uint16 keys."""
-    lens = np.minimum(np.asarray(lens, np.int64), 65535)
-    return np.argsort((65535 - lens).astype(np.uint16), kind="stable")
+    """Internal order of a band: rows grouped by length class, longest class
+    first, layout order inside a class (stable). Classes are
+    floor(8 log2(len + 1)) — about 9 % wide — so a SELL-32 slice holds rows
+    within ~9 % of each other's length, the longest slices start first
+    (LPT-like, no tail), and rows of one class keep their layout order, which
+    preserves the gather locality of structured matrices (consecutive rows of
+    one commodity in a flow LP). numpy's stable sort on the uint16 class key
+    is a radix sort."""
+    lens = np.asarray(lens, np.int64)
+    cls = np.floor(LENGTH_BUCKETS_PER_OCTAVE * np.log2(lens.astype(np.float64) + 1.0)).astype(np.int64)
+    return np.argsort((65535 - np.minimum(cls, 65535)).astype(np.uint16), kind="stable")
 
 
 def inverse_order(order: np.ndarray) -> np.ndarray:
@@ -167,8 +175,8 @@ def build_sell(host: HostCsr, light_row_max: int):
 
 def long_row_plan(long_ptr: torch.Tensor, exact_row_max: int):
     """Split the compact CSR's long rows: rows of length <= exact_row_max are
-    summed exactly by one warp each (exact_long lists them, longest first);
-    longer rows are
+    summed exactly by one warp each (exact_long lists them in row order, so
+    neighbouring warps gather neighbouring data); longer rows are
     cut into GRIDLP_HEAVY_CHUNK-entry chunks. Returns int32 tensors
     (exact_long, chunk_first [nl+1], chunk_row [num_chunks]) on long_ptr's
     device."""
@@ -184,8 +192,6 @@ def long_row_plan(long_ptr: torch.Tensor, exact_row_max: int):
     if int(first[-1]) >= 2 ** 31:
         raise ValueError("too many heavy-row chunks for int32")
     exact = torch.nonzero(~heavy).flatten() if nl else first[:0]
-    if exact.numel():      # longest first: the longest add chains start in the first wave
-        exact = exact[torch.sort(lens[exact], descending=True, stable=True).indices]
     return exact.to(torch.int32), first.to(torch.int32), rows.to(torch.int32)
 
 

@@ -89,8 +89,7 @@ def test_long_row_plan():
     lens = np.array([65, 513, C, 4096, 4097, 5 * C - 3, 40 * C])
     hptr = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32))
     exact, first, row = long_row_plan(hptr, 4096)
-    ex = np.flatnonzero(lens <= 4096)
-    np.testing.assert_array_equal(exact.numpy(), ex[np.argsort(-lens[ex], kind="stable")])
+    np.testing.assert_array_equal(exact.numpy(), np.flatnonzero(lens <= 4096))
     want = np.where(lens > 4096, -(-lens // C), 0)
     np.testing.assert_array_equal(np.diff(first.numpy()), want)
     np.testing.assert_array_equal(row.numpy(), np.repeat(np.arange(len(lens)), want))
@@ -134,3 +133,21 @@ def test_sell_layout_roundtrip():
     for h, row in enumerate(heavy):
         a, b = sd["long_ptr"][h], sd["long_ptr"][h + 1]
         np.testing.assert_array_equal(sd["long_cols"][a:b], col[ptr[row]:ptr[row + 1]])
+
+
+def test_length_order_classes():
+    from paper_2601_07628_b200.blocks import length_order
+
+    rng = np.random.default_rng(2)
+    lens = rng.integers(0, 100, 5000)
+    lens[17] = 10 ** 6
+    o = length_order(lens)
+    assert sorted(o.tolist()) == list(range(5000)) and o[0] == 17
+    cls = np.floor(8 * np.log2(lens[o] + 1.0))
+    assert np.all(np.diff(cls) <= 0)                             # longest class first
+    ties = np.diff(cls) == 0
+    assert np.all(np.diff(o)[ties] > 0)                          # layout order inside a class
+    for s in range(0, 4992, 32):                                 # a slice spans <= 2 classes
+        ls = lens[o[s:s + 32]]
+        if 8 < ls.min() and ls.max() < 1000:
+            assert ls.max() <= 1.2 * ls.min() + 1

@@ -87,7 +87,7 @@ class TestProducts:
         h = host_csr(m, n, ptr, col, val)
         want = sp.csr_matrix((val, col, ptr), shape=(m, n)).dot(x)
         A = DeviceCsr(h, DEV)
-        assert A.long_rows == np.count_nonzero(lens > 64)
+        assert A.long_rows == np.count_nonzero(lens > 128)
         assert A.heavy_rows == np.count_nonzero(lens > 4096)
         out = torch.empty(m, dtype=torch.float64, device=DEV)
         ops.store(Fused(A, dev(x)), out)
