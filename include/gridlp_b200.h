@@ -362,6 +362,26 @@ int gridlp_gen_mcf_fill(int64_t K, int64_t V, int64_t E, const int32_t* adj_ptr,
                         const int8_t* adj_sign, const int64_t* row_ptr, int32_t* cols, double* vals,
                         void* stream);
 
+/* --- diagonal preconditioning (csrc/gridlp_scale.cu) -------------------------
+ * Ruiz equilibration + Pock-Chambolle scaling of A, opt-in
+ * (SolverConfig.scaling; the reference has none). Matrices here
+ * are the original problem's CSR (int64 row pointers, int32 columns). */
+/* out[r] = max |a_rk| over row r. */
+int gridlp_row_absmax(const int64_t* ptr, const double* val, int64_t m, double* out, void* stream);
+/* out[r] = sum |a_rk|^power over row r (power 1 or 2), sequential in entry order. */
+int gridlp_row_abssum(const int64_t* ptr, const double* val, int64_t m, int32_t power, double* out,
+                      void* stream);
+/* out[c] = max |a_kc| over column c (order-free atomic max). */
+int gridlp_col_absmax(const int32_t* col, const double* val, int64_t nnz, int64_t ncols, double* out,
+                      void* stream);
+/* step[i] = 1/sqrt(s[i]) (1 when s[i] = 0); d[i] *= step[i]. */
+int gridlp_update_scale(const double* s, int64_t n, double* d, double* step, void* stream);
+/* a_rc <- (dr[r] a_rc) dc[c] in place. */
+int gridlp_scale_matrix(const int64_t* ptr, const int32_t* col, double* val, int64_t m, const double* dr,
+                        const double* dc, void* stream);
+/* v[i] <- v[i] * d[i] (divide = 0) or v[i] / d[i] (divide = 1). */
+int gridlp_scale_vector(double* v, const double* d, int64_t n, int32_t divide, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

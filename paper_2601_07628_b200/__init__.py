@@ -28,14 +28,15 @@ from .layout import (
     uniform_cuts,
     unpermute_solution,
 )
+from .mps import MpsParseError, load_mps, parse_mps, write_mps
 from .problem import LpProblem, SparseMatrix, objective_value, reported_objective
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "GeneratorSpec", "GridTopology", "KktReport", "LpProblem", "PartitionLayout",
+    "GeneratorSpec", "GridTopology", "KktReport", "LpProblem", "MpsParseError", "PartitionLayout",
     "Permutation", "SolveResult", "SolverConfig", "SparseMatrix", "StepSizes",
     "block_random_permutation", "box_lp_optimum", "build_layout", "generate",
-    "layout_summary", "nnz_balanced_cuts", "objective_value", "reference_solve",
-    "reported_objective", "select_grid", "solve", "uniform_cuts", "unpermute_solution",
+    "layout_summary", "load_mps", "nnz_balanced_cuts", "objective_value", "parse_mps", "reference_solve",
+    "reported_objective", "select_grid", "solve", "uniform_cuts", "unpermute_solution", "write_mps",
 ]

@@ -29,6 +29,8 @@ from .comm import Ledger, NcclGrid, VirtualGrid
 from .layout import GridTopology, build_layout, layout_summary, unpermute_solution
 from .ops import CudaOps
 from .problem import reported_objective
+from .scaling import MODES as SCALING_MODES
+from .scaling import scale_problem
 
 STEP_SIZE_SAFETY = 0.998
 BACKENDS = ("cuda", "cooperative", "threads", "nccl")
@@ -112,6 +114,13 @@ class SolverConfig:
     power_iterations: int = 30
     collective_timeout_seconds: float = 120.0
     comm_backend: str = "cuda"
+    # B200 extensions (not in the reference; defaults keep its behaviour):
+    # on-device diagonal preconditioning (scaling.py) — "none", "ruiz",
+    # "pock_chambolle" or "ruiz+pock_chambolle". With scaling the iteration,
+    # restart and termination tests run on the scaled LP (report fields refer
+    # to it); x, y and the objective are returned in the original space.
+    scaling: str = "none"
+    ruiz_iterations: int = 10
 
     def __post_init__(self):
         if self.tolerance <= 0:
@@ -130,6 +139,10 @@ class SolverConfig:
                 raise ValueError(f"grid {rows}x{cols} needs {rows * cols} devices but n_procs={self.n_procs}")
         if self.comm_backend not in BACKENDS:
             raise ValueError(f"unknown backend {self.comm_backend!r}; expected one of {BACKENDS}")
+        if self.scaling not in SCALING_MODES:
+            raise ValueError(f"unknown scaling {self.scaling!r}; expected one of {SCALING_MODES}")
+        if self.ruiz_iterations < 0:
+            raise ValueError("ruiz_iterations must be non-negative")
 
     def engine_options(self) -> eng.EngineOptions:
         return eng.EngineOptions(
@@ -254,8 +267,14 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
 def _solve(problem, cfg: SolverConfig, trace=None, force_1x1=False, ops_factory=None,
            device=None, engine_overrides=None) -> SolveResult:
     t_start = time.perf_counter()
+    scaled = None
+    if cfg.scaling != "none":
+        scaled = scale_problem(problem, cfg.scaling, cfg.ruiz_iterations, device)
+        original, problem = problem, scaled.problem
     engine, layout, eta, omega, timings = prepare(problem, cfg, force_1x1, ops_factory, device,
                                                   engine_overrides)
+    if scaled is not None:
+        timings["scaling_s"] = scaled.seconds
     comm = engine.comm
     setup_events = engine.ledger.snapshot()
     leader = (not comm.local) or comm.local[0] == (0, 0)
@@ -263,6 +282,9 @@ def _solve(problem, cfg: SolverConfig, trace=None, force_1x1=False, ops_factory=
     timings.update(engine.timings)
     xs, ys = engine.solution_blocks()
     x, y = unpermute_solution(layout, xs, ys)
+    if scaled is not None:
+        x, y = scaled.unscale(x, y)
+        problem = original
     rep = out["report"]
     report = KktReport(rep.r_primal, rep.r_dual, rep.r_gap, rep.obj_primal, rep.obj_dual)
     final_events = engine.ledger.snapshot()

@@ -16,7 +16,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libgridlp_b200.so"
-SOURCES = [PKG / "csrc" / "gridlp_b200.cu", PKG / "csrc" / "gridlp_setup.cu", PKG / "csrc" / "gridlp_gen.cu"]
+SOURCES = [PKG / "csrc" / "gridlp_b200.cu", PKG / "csrc" / "gridlp_setup.cu", PKG / "csrc" / "gridlp_gen.cu",
+           PKG / "csrc" / "gridlp_scale.cu"]
 HEADER = ROOT / "include" / "gridlp_b200.h"
 
 MAX_RED = 8
@@ -109,6 +110,12 @@ SIGNATURES = {
     "gridlp_gen_row_bounds": ([ctypes.c_uint64, c_int64, c_double, _P, _P, _P, _P], c_int),
     "gridlp_gen_mcf_row_lengths": ([c_int64, c_int64, c_int64, _P, _P, _P], c_int),
     "gridlp_gen_mcf_fill": ([c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P], c_int),
+    "gridlp_row_absmax": ([_P, _P, c_int64, _P, _P], c_int),
+    "gridlp_row_abssum": ([_P, _P, c_int64, c_int32, _P, _P], c_int),
+    "gridlp_col_absmax": ([_P, _P, c_int64, c_int64, _P, _P], c_int),
+    "gridlp_update_scale": ([_P, c_int64, _P, _P, _P], c_int),
+    "gridlp_scale_matrix": ([_P, _P, _P, c_int64, _P, _P, _P], c_int),
+    "gridlp_scale_vector": ([_P, _P, c_int64, c_int32, _P], c_int),
 }
 
 
