@@ -28,12 +28,12 @@ def _badly_scaled(seed, m=300, n=500, nnz=3000):
     rows = np.repeat(np.arange(m), np.diff(A.row_offsets))
     val = A.values * r[rows] * c[A.col_indices]
     return LpProblem(SparseMatrix(m, n, A.row_offsets, A.col_indices, val), p.objective * c, p.var_lower / c,
-                     p.var_upper / c, p.con_lower * r, p.con_upper * r)
+                     p.var_upper / c, p.con_lower * r, p.con_upper * r), p
 
 
 @pytest.mark.parametrize("mode", ["ruiz", "pock_chambolle", "ruiz+pock_chambolle"])
 def test_scaling_bitwise(mode):
-    p = _badly_scaled(1)
+    p, _ = _badly_scaled(1)
     got = scale_problem(p, mode, 10, DEV)
     A = p.matrix
     val, dr, dc = scaling_oracle.scale(A.row_offsets, A.col_indices, A.values, A.num_rows, A.num_cols, mode, 10)
@@ -43,7 +43,7 @@ def test_scaling_bitwise(mode):
     np.testing.assert_array_equal(got.problem.objective, p.objective * dc)
     np.testing.assert_array_equal(got.problem.con_upper, p.con_upper * dr)
     np.testing.assert_array_equal(got.problem.var_upper, p.var_upper / dc)
-    if mode != "pock_chambolle":           # Ruiz equilibrates: every row/column max close to 1
+    if mode == "ruiz":                     # Ruiz equilibrates: every row max close to 1
         absv = np.abs(got.problem.matrix.values)
         rows = np.repeat(np.arange(A.num_rows), np.diff(A.row_offsets))
         rmax = np.zeros(A.num_rows)
@@ -52,12 +52,18 @@ def test_scaling_bitwise(mode):
 
 
 def test_scaled_solve_matches_unscaled_optimum_and_needs_fewer_iterations():
-    p = _badly_scaled(2)
-    base = dict(tolerance=1e-6, seed=2, max_iterations=200_000)
+    """The badly scaled LP p is a diagonal change of variables of the
+    generator's LP q, so both have the same optimal objective: the unscaled
+    reference algorithm stalls on p (iteration limit), the scaled solve of p
+    reaches q's optimum."""
+    p, q = _badly_scaled(2)
+    base = dict(tolerance=1e-6, seed=2, max_iterations=100_000)
     plain = pdhg_oracle.oracle_solve(p, **base)
+    well = pdhg_oracle.oracle_solve(q, **base)
+    assert well.status == "optimal"
     got = solve(p, SolverConfig(**base, scaling="ruiz+pock_chambolle"))
     assert got.status == "optimal"
-    assert abs(got.objective - plain.objective) <= 1e-4 * max(1.0, abs(plain.objective))
+    assert abs(got.objective - well.objective) <= 1e-4 * max(1.0, abs(well.objective))
     assert got.iterations < plain.iterations
     # x, y come back in the original space: primal feasibility of the original LP
     ax = p.matrix.to_dense() @ got.x
