@@ -358,7 +358,11 @@ def run_ours(args, rank, world, local_rank):
         base["partitioning"] = args.partitioning
     cfg = SolverConfig(tolerance=1e-300, max_iterations=10**12, seed=0, **base)
     t0 = time.perf_counter()
-    over = {"light_row_max": args.light_row_max} if args.light_row_max is not None else None
+    over = {}
+    if args.light_row_max is not None:
+        over["light_row_max"] = args.light_row_max
+    if args.no_graphs:
+        over["use_graphs"] = False
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
     log(f"[bench] rank {rank}: setup {time.perf_counter() - t0:.1f}s {tim}")
     R, C = layout.topology.rows, layout.topology.cols
@@ -488,6 +492,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmv", action="store_true", help="skip the SpMV-only comparison with cuSPARSE")
     ap.add_argument("--light-row-max", type=int, default=None, help="EngineOptions.light_row_max override")
+    ap.add_argument("--no-graphs", action="store_true", help="eager launches (the NCCL executor's path)")
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")
     ap.add_argument("--partitioning", default=None, help="SolverConfig.partitioning override")

@@ -333,6 +333,20 @@ int gridlp_gen_scan64(const int64_t* in, int64_t* out, int64_t n, void* ws, size
  * c = clamp(floor((1 + u(seed,1,r,k) kappa)^5) - 1, 0, n-1). */
 int gridlp_gen_powerlaw_sample(uint64_t seed, const int64_t* alloc_ptr, int64_t m, int64_t n, double kappa,
                                int32_t* cols, void* stream);
+/* Uniform column samples: entry k of row r gets floor(u(seed,1,r,k) n). */
+int gridlp_gen_uniform_sample(uint64_t seed, const int64_t* alloc_ptr, int64_t m, int64_t n, int32_t* cols,
+                              void* stream);
+/* Planted optimum (cfg5): primal point x* and reduced cost r* per column
+ * (30 % at the lower bound with r* > 0, 10 % at the upper bound with
+ * r* < 0, the rest interior with r* = 0). */
+int gridlp_gen_planted_cols(uint64_t seed, int64_t n, double lo, double hi, double* x, double* r,
+                            void* stream);
+/* Planted duals y* and row bounds around b = A x* (35 % lower-active with
+ * y* > 0, 35 % upper-active with y* < 0, 30 % inactive with y* = 0). */
+int gridlp_gen_planted_rows(uint64_t seed, int64_t m, const double* b, double* y, double* lo, double* hi,
+                            void* stream);
+/* out = a + b (c = Aᵀ y* + r*). */
+int gridlp_gen_add(const double* a, const double* b, int64_t n, double* out, void* stream);
 /* Sort the keys of every row segment ptr[r]..ptr[r+1] ascending. */
 int gridlp_gen_sort_rows(const int64_t* ptr, int64_t m, int64_t items, const int32_t* keys_in,
                          int32_t* keys_out, void* ws, size_t ws_bytes, void* stream);

@@ -92,3 +92,36 @@ def mcf(V, E, K, capacity_factor=1.25, seed=0):
     hi[K * V:] = b[K * V:] * capacity_factor
     return dict(ptr=A.indptr.astype(np.int64), col=A.indices.astype(np.int64), val=A.data, x_hat=x_hat, c=cvec,
                 var_lo=np.zeros(n), var_hi=np.full(n, 4.0), con_lo=lo, con_hi=hi)
+
+
+def planted(m, n, d, box=(0.0, 4.0), seed=0):
+    """Planted-optimum LP (cfg5 generator): dict as powerlaw() plus y_star."""
+    rows = np.repeat(np.arange(m, dtype=np.int64), d)
+    k = np.tile(np.arange(d, dtype=np.int64), m)
+    c = np.floor(u01(seed, 1, rows, k) * float(n)).astype(np.int64)
+    c = np.minimum(c, n - 1)
+    key = np.unique(rows * n + c)
+    r, col = key // n, key % n
+    val = 2.0 * u01(seed, 2, r, col) - 1.0
+    ptr = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=m))]).astype(np.int64)
+    A = sp.csr_matrix((val, col, ptr), shape=(m, n))
+    j = np.arange(n)
+    st = u01(seed, 20, j)
+    w = 0.1 + 0.9 * u01(seed, 21, j)
+    lo, hi = box
+    x = np.where(st < 0.3, lo, np.where(st < 0.4, hi, lo + (hi - lo) * (0.1 + 0.8 * u01(seed, 22, j))))
+    rc = np.where(st < 0.3, w, np.where(st < 0.4, -w, 0.0))
+    b = A.dot(x)
+    i = np.arange(m)
+    sti = u01(seed, 23, i)
+    yv = 0.5 + u01(seed, 24, i)
+    wl = 0.1 + 0.9 * u01(seed, 25, i)
+    wh = 0.1 + 0.9 * u01(seed, 26, i)
+    y = np.where(sti < 0.35, yv, np.where(sti < 0.7, -yv, 0.0))
+    clo = np.where(sti < 0.35, b, b - wl)
+    chi = np.where(sti < 0.35, b + wl, np.where(sti < 0.7, b, b + wh))
+    t = A.T.tocsr()
+    t.sort_indices()
+    cvec = t.dot(y) + rc
+    return dict(ptr=ptr, col=col, val=val, x_hat=x, c=cvec, var_lo=np.full(n, lo), var_hi=np.full(n, hi),
+                con_lo=clo, con_hi=chi, y_star=y)

@@ -76,6 +76,68 @@ __global__ void powerlaw_sample_kernel(uint64_t seed, const int64_t* __restrict_
   }
 }
 
+// Uniform column samples: entry k of row r draws c = floor(u(seed,1,r,k) * n).
+__global__ void uniform_sample_kernel(uint64_t seed, const int64_t* __restrict__ alloc_ptr, int64_t m, int64_t n,
+                                      int32_t* __restrict__ cols) {
+  const int64_t total = alloc_ptr[m];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = m;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (alloc_ptr[mid] <= e) lo = mid; else hi = mid;
+    }
+    const int64_t c = (int64_t)floor(__dmul_rn(u01(ghash(seed, 1, (uint64_t)lo, (uint64_t)(e - alloc_ptr[lo]))),
+                                               (double)n));
+    cols[e] = (int32_t)(c < n ? c : n - 1);
+  }
+}
+
+// Planted optimum, per column j: state u(seed,20,j) < 0.3 -> at the lower
+// bound (x* = lo, r* = 0.1 + 0.9 u(seed,21,j)), < 0.4 -> at the upper bound
+// (x* = hi, r* = -(0.1 + 0.9 u21)), else interior (x* = lo + (hi - lo)(0.1 +
+// 0.8 u(seed,22,j)), r* = 0).
+__global__ void planted_cols_kernel(uint64_t seed, int64_t n, double lo, double hi, double* __restrict__ x,
+                                    double* __restrict__ r) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double st = u01(ghash(seed, 20, (uint64_t)j, 0));
+    const double w = __dadd_rn(0.1, __dmul_rn(0.9, u01(ghash(seed, 21, (uint64_t)j, 0))));
+    if (st < 0.3) { x[j] = lo; r[j] = w; }
+    else if (st < 0.4) { x[j] = hi; r[j] = -w; }
+    else {
+      x[j] = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), __dadd_rn(0.1, __dmul_rn(0.8, u01(ghash(seed, 22, (uint64_t)j, 0))))));
+      r[j] = 0.0;
+    }
+  }
+}
+
+// Planted duals and row bounds around b = A x*: state u(seed,23,i) < 0.35 ->
+// lower bound active (y* = 0.5 + u(seed,24,i), lo = b, hi = b + 0.1 + 0.9
+// u(seed,25,i)); < 0.7 -> upper active (y* = -(0.5 + u24), hi = b, lo = b -
+// (0.1 + 0.9 u25)); else inactive (y* = 0, lo = b - (0.1 + 0.9 u25), hi = b +
+// (0.1 + 0.9 u(seed,26,i))).
+__global__ void planted_rows_kernel(uint64_t seed, int64_t m, const double* __restrict__ b, double* __restrict__ y,
+                                    double* __restrict__ lo, double* __restrict__ hi) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const double st = u01(ghash(seed, 23, (uint64_t)i, 0));
+    const double yv = __dadd_rn(0.5, u01(ghash(seed, 24, (uint64_t)i, 0)));
+    const double w = __dadd_rn(0.1, __dmul_rn(0.9, u01(ghash(seed, 25, (uint64_t)i, 0))));
+    const double bi = b[i];
+    if (st < 0.35) { y[i] = yv; lo[i] = bi; hi[i] = __dadd_rn(bi, w); }
+    else if (st < 0.7) { y[i] = -yv; hi[i] = bi; lo[i] = __dsub_rn(bi, w); }
+    else {
+      const double w2 = __dadd_rn(0.1, __dmul_rn(0.9, u01(ghash(seed, 26, (uint64_t)i, 0))));
+      y[i] = 0.0; lo[i] = __dsub_rn(bi, w); hi[i] = __dadd_rn(bi, w2);
+    }
+  }
+}
+
+// c = aty + r (the planted reduced cost makes (x*, y*) a KKT point)
+__global__ void add_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                           double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(a[i], b[i]);
+}
+
 // distinct columns per (sorted) row
 __global__ void dedupe_count_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ sorted, int64_t m,
                                     int64_t* __restrict__ counts) {
@@ -210,6 +272,37 @@ int gridlp_gen_powerlaw_sample(uint64_t seed, const int64_t* alloc_ptr, int64_t 
   if (m == 0) return GRIDLP_OK;
   powerlaw_sample_kernel<<<148 * 16, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, alloc_ptr, m, n, kappa, cols);
   return gcuda(cudaGetLastError(), "gen_powerlaw_sample");
+}
+
+int gridlp_gen_uniform_sample(uint64_t seed, const int64_t* alloc_ptr, int64_t m, int64_t n, int32_t* cols,
+                              void* stream) {
+  if (m < 0 || n < 1 || n >= (int64_t(1) << 31) || !alloc_ptr || (m > 0 && !cols))
+    return gfail(GRIDLP_ERR_ARG, "gen_uniform_sample: bad argument");
+  if (m == 0) return GRIDLP_OK;
+  uniform_sample_kernel<<<148 * 16, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, alloc_ptr, m, n, cols);
+  return gcuda(cudaGetLastError(), "gen_uniform_sample");
+}
+
+int gridlp_gen_planted_cols(uint64_t seed, int64_t n, double lo, double hi, double* x, double* r, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !r)) || !(lo < hi)) return gfail(GRIDLP_ERR_ARG, "gen_planted_cols: bad argument");
+  if (n == 0) return GRIDLP_OK;
+  planted_cols_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, n, lo, hi, x, r);
+  return gcuda(cudaGetLastError(), "gen_planted_cols");
+}
+
+int gridlp_gen_planted_rows(uint64_t seed, int64_t m, const double* b, double* y, double* lo, double* hi,
+                            void* stream) {
+  if (m < 0 || (m > 0 && (!b || !y || !lo || !hi))) return gfail(GRIDLP_ERR_ARG, "gen_planted_rows: bad argument");
+  if (m == 0) return GRIDLP_OK;
+  planted_rows_kernel<<<grid_for(m), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, m, b, y, lo, hi);
+  return gcuda(cudaGetLastError(), "gen_planted_rows");
+}
+
+int gridlp_gen_add(const double* a, const double* b, int64_t n, double* out, void* stream) {
+  if (n < 0 || (n > 0 && (!a || !b || !out))) return gfail(GRIDLP_ERR_ARG, "gen_add: bad argument");
+  if (n == 0) return GRIDLP_OK;
+  add_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, n, out);
+  return gcuda(cudaGetLastError(), "gen_add");
 }
 
 int gridlp_gen_sort_rows(const int64_t* ptr, int64_t m, int64_t items, const int32_t* keys_in, int32_t* keys_out,

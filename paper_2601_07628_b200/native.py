@@ -102,6 +102,10 @@ SIGNATURES = {
     "gridlp_gen_workspace_bytes": ([c_int64, c_int64], ctypes.c_size_t),
     "gridlp_gen_scan64": ([_P, _P, c_int64, _P, ctypes.c_size_t, _P], c_int),
     "gridlp_gen_powerlaw_sample": ([ctypes.c_uint64, _P, c_int64, c_int64, c_double, _P, _P], c_int),
+    "gridlp_gen_uniform_sample": ([ctypes.c_uint64, _P, c_int64, c_int64, _P, _P], c_int),
+    "gridlp_gen_planted_cols": ([ctypes.c_uint64, c_int64, c_double, c_double, _P, _P, _P], c_int),
+    "gridlp_gen_planted_rows": ([ctypes.c_uint64, c_int64, _P, _P, _P, _P, _P], c_int),
+    "gridlp_gen_add": ([_P, _P, c_int64, _P, _P], c_int),
     "gridlp_gen_sort_rows": ([_P, c_int64, c_int64, _P, _P, _P, ctypes.c_size_t, _P], c_int),
     "gridlp_gen_dedupe_count": ([_P, _P, c_int64, _P, _P], c_int),
     "gridlp_gen_dedupe_fill": ([_P, _P, c_int64, _P, ctypes.c_uint64, _P, _P, _P], c_int),

@@ -25,6 +25,14 @@ at small sizes.
   (+1 out-arcs, -1 in-arcs) with lo = hi = the divergence of a planted flow
   x_hat ~ U[0.5, 1.5); rows K*V + e couple the commodities on arc e,
   sum_k x_ke <= 1.25 * (planted load). Costs U[1, 10), box [0, 4].
+* `PlantedSpec` (cfg5): a uniform random matrix (d column draws per row)
+  with a planted primal-dual optimum (x*, y*): x* puts 30 % of the
+  variables at the lower and 10 % at the upper bound, y* makes 35 % of the
+  rows active at their lower and 35 % at their upper bound, the objective is
+  c = Aᵀ y* + r* with a reduced cost r* complementary to x*. (x*, y*)
+  satisfies the KKT conditions exactly, so the optimal objective is c·x* —
+  an analytic oracle that needs no CPU solve, for instances too large for
+  one GPU or the host.
 """
 
 from __future__ import annotations
@@ -91,6 +99,24 @@ class McfSpec:
             raise ValueError("need >= 2 nodes, >= 1 arc, >= 1 commodity")
         if self.num_commodities * self.num_arcs >= 2 ** 31 - 1:
             raise ValueError("K * E must be < 2^31 (int32 column indices)")
+
+
+@dataclass(frozen=True)
+class PlantedSpec:
+    num_rows: int
+    num_cols: int
+    draws_per_row: int = 8
+    box_low: float = 0.0
+    box_high: float = 4.0
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.num_rows < 1 or self.num_cols < 1 or self.draws_per_row < 1:
+            raise ValueError("need num_rows, num_cols, draws_per_row >= 1")
+        if self.num_cols >= 2 ** 31 - 1 or self.num_rows * self.draws_per_row >= 2 ** 31:
+            raise ValueError("one-piece generation needs < 2^31 columns and draws")
+        if self.box_low >= self.box_high:
+            raise ValueError("box_low must be below box_high")
 
 
 def powerlaw_row_alloc(spec: PowerLawSpec) -> np.ndarray:
@@ -252,3 +278,64 @@ def generate_mcf(spec: McfSpec, device=None) -> DeviceLp:
     f64 = dict(dtype=torch.float64, device=dev)
     return DeviceLp(m, n, row_ptr, cols, vals, obj, torch.zeros(n, **f64), torch.full((n,), 4.0, **f64), lo, hi,
                     x_hat)
+
+
+@dataclass
+class PlantedLp(DeviceLp):
+    y_star: torch.Tensor = None
+
+    def optimal_objective(self) -> float:
+        """c·x* — the planted optimum (sequential host sum of the device arrays)."""
+        return float(np.dot(self.objective.cpu().numpy(), self.x_hat.cpu().numpy()))
+
+
+def _dedupe_rows(g: _Gen, alloc_ptr, raw, m, seed):
+    total = int(raw.numel())
+    srt = torch.empty_like(raw)
+    ws, nb = g.ws(total, m)
+    g.lib.call("gridlp_gen_sort_rows", alloc_ptr.data_ptr(), m, total, raw.data_ptr(), srt.data_ptr(), ws.data_ptr(),
+               nb, g.stream())
+    del ws
+    counts = torch.empty(m + 1, dtype=torch.int64, device=g.device)
+    g.lib.call("gridlp_gen_dedupe_count", alloc_ptr.data_ptr(), srt.data_ptr(), m, counts.data_ptr(), g.stream())
+    row_ptr = g.scan(counts)
+    nnz = int(row_ptr[m])
+    cols = torch.empty(max(nnz, 1), dtype=torch.int32, device=g.device)[:nnz]
+    vals = torch.empty(max(nnz, 1), dtype=torch.float64, device=g.device)[:nnz]
+    g.lib.call("gridlp_gen_dedupe_fill", alloc_ptr.data_ptr(), srt.data_ptr(), m, row_ptr.data_ptr(), seed,
+               cols.data_ptr(), vals.data_ptr(), g.stream())
+    return row_ptr, cols, vals
+
+
+def generate_planted(spec: PlantedSpec, device=None) -> PlantedLp:
+    g = _Gen(device)
+    dev, m, n, seed = g.device, spec.num_rows, spec.num_cols, spec.seed
+    f64 = dict(dtype=torch.float64, device=dev)
+    lens = torch.full((m + 1,), spec.draws_per_row, dtype=torch.int64, device=dev)
+    lens[m] = 0
+    alloc_ptr = g.scan(lens)
+    raw = torch.empty(m * spec.draws_per_row, dtype=torch.int32, device=dev)
+    g.lib.call("gridlp_gen_uniform_sample", seed, alloc_ptr.data_ptr(), m, n, raw.data_ptr(), g.stream())
+    row_ptr, cols, vals = _dedupe_rows(g, alloc_ptr, raw, m, seed)
+    del raw, alloc_ptr
+    x, r = torch.empty(n, **f64), torch.empty(n, **f64)
+    g.lib.call("gridlp_gen_planted_cols", seed, n, spec.box_low, spec.box_high, x.data_ptr(), r.data_ptr(), g.stream())
+    b = g.spmv_seq(row_ptr, cols, vals, m, x)
+    y, lo, hi = torch.empty(m, **f64), torch.empty(m, **f64), torch.empty(m, **f64)
+    g.lib.call("gridlp_gen_planted_rows", seed, m, b.data_ptr(), y.data_ptr(), lo.data_ptr(), hi.data_ptr(),
+               g.stream())
+    # c = Aᵀ y* + r*: sequential sums along the rows of the stored transpose
+    nnz = int(cols.numel())
+    wsb = int(g.lib._lib.gridlp_setup_workspace_bytes(nnz + 64, max(m, n) + 64))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    tptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    tcol = torch.empty(nnz + 8, dtype=torch.int32, device=dev)
+    tval = torch.empty(nnz + 8, **f64)
+    g.lib.call("gridlp_csr_transpose", row_ptr.to(torch.int32).data_ptr(), cols.data_ptr(), vals.data_ptr(), m, n,
+               nnz, tptr.data_ptr(), tcol.data_ptr(), tval.data_ptr(), ws.data_ptr(), wsb, g.stream())
+    aty = g.spmv_seq(tptr.to(torch.int64), tcol, tval, n, y)
+    del ws, tptr, tcol, tval
+    c = torch.empty(n, **f64)
+    g.lib.call("gridlp_gen_add", aty.data_ptr(), r.data_ptr(), n, c.data_ptr(), g.stream())
+    return PlantedLp(m, n, row_ptr, cols, vals, c, torch.full((n,), spec.box_low, **f64),
+                     torch.full((n,), spec.box_high, **f64), lo, hi, x, y_star=y)

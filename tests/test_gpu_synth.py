@@ -48,3 +48,25 @@ def test_generated_lp_solves_like_oracle(kind):
     assert got.status == want.status
     assert (got.iterations, got.restarts) == (want.iterations, want.restarts)
     assert abs(got.objective - want.objective) <= 1e-6 * max(1.0, abs(want.objective))
+
+
+@pytest.mark.parametrize("m,n,d,seed", [(2000, 3000, 8, 0), (700, 500, 5, 3)])
+def test_planted_bitwise(m, n, d, seed):
+    from paper_2601_07628_b200.synth import PlantedSpec, generate_planted
+
+    dl = generate_planted(PlantedSpec(m, n, d, seed=seed), DEV)
+    want = synth_oracle.planted(m, n, d, seed=seed)
+    y = want.pop("y_star")
+    _same(dl, want)
+    np.testing.assert_array_equal(dl.y_star.cpu().numpy(), y)
+
+
+def test_planted_optimum_is_reached():
+    """The analytic oracle: the solve converges to c·x* (no CPU solve)."""
+    from paper_2601_07628_b200.synth import PlantedSpec, generate_planted
+
+    dl = generate_planted(PlantedSpec(3000, 4000, 6, seed=7), DEV)
+    star = dl.optimal_objective()
+    got = solve(dl.to_problem(), SolverConfig(tolerance=1e-7, seed=7, n_procs=4, grid=(2, 2), max_iterations=200_000))
+    assert got.status == "optimal"
+    assert abs(got.objective - star) <= 1e-5 * (1.0 + abs(star))
