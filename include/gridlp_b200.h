@@ -336,30 +336,44 @@ int gridlp_gen_powerlaw_sample(uint64_t seed, const int64_t* alloc_ptr, int64_t 
 /* Uniform column samples: entry k of row r gets floor(u(seed,1,r,k) n). */
 int gridlp_gen_uniform_sample(uint64_t seed, const int64_t* alloc_ptr, int64_t m, int64_t n, int32_t* cols,
                               void* stream);
-/* Planted optimum (cfg5): primal point x* and reduced cost r* per column
- * (30 % at the lower bound with r* > 0, 10 % at the upper bound with
- * r* < 0, the rest interior with r* = 0). */
-int gridlp_gen_planted_cols(uint64_t seed, int64_t n, double lo, double hi, double* x, double* r,
+/* Planted optimum (cfg5): primal point x* and reduced cost r* of columns
+ * j0 .. j0+n-1 (30 % at the lower bound with r* > 0, 10 % at the upper
+ * bound with r* < 0, the rest interior with r* = 0). */
+int gridlp_gen_planted_cols(uint64_t seed, int64_t j0, int64_t n, double lo, double hi, double* x, double* r,
                             void* stream);
-/* Planted duals y* and row bounds around b = A x* (35 % lower-active with
- * y* > 0, 35 % upper-active with y* < 0, 30 % inactive with y* = 0). */
-int gridlp_gen_planted_rows(uint64_t seed, int64_t m, const double* b, double* y, double* lo, double* hi,
-                            void* stream);
+/* Planted duals y* and row bounds around b = A x* for rows i0 .. i0+m-1
+ * (35 % lower-active with y* > 0, 35 % upper-active with y* < 0, 30 %
+ * inactive with y* = 0). */
+int gridlp_gen_planted_rows(uint64_t seed, int64_t i0, int64_t m, const double* b, double* y, double* lo,
+                            double* hi, void* stream);
+/* Sharded cfg5 generation (no device ever holds the whole matrix):
+ * d draws per row for rows r0 .. r0+m-1 (row-major, floor(u(seed,1,r,k) n)). */
+int gridlp_gen_band_draws(uint64_t seed, int64_t r0, int64_t m, int32_t d, int64_t n, int32_t* cols,
+                          void* stream);
+/* b[q] = A x* of full (sorted, possibly repeated) row r0+q, sequential in
+ * column order from +0.0 — the one-piece instance's value. */
+int gridlp_gen_planted_row_dot(const int64_t* ptr, const int32_t* sorted, int64_t m, int64_t r0, uint64_t seed,
+                               double lo, double hi, double* b, void* stream);
+/* acc[c] += value * y*(row) over the transposed chunk block, rows ascending
+ * (continues the sequential column sum Aᵀ y* across row chunks). */
+int gridlp_gen_col_accumulate(const int32_t* tptr, const int32_t* trows, const double* tvals, int64_t ncols,
+                              int64_t r0, uint64_t seed, double* acc, void* stream);
 /* out = a + b (c = Aᵀ y* + r*). */
 int gridlp_gen_add(const double* a, const double* b, int64_t n, double* out, void* stream);
 /* Sort the keys of every row segment ptr[r]..ptr[r+1] ascending. */
 int gridlp_gen_sort_rows(const int64_t* ptr, int64_t m, int64_t items, const int32_t* keys_in,
                          int32_t* keys_out, void* ws, size_t ws_bytes, void* stream);
-/* counts[r] = distinct keys of sorted row r; counts[m] = 0. */
-int gridlp_gen_dedupe_count(const int64_t* ptr, const int32_t* sorted, int64_t m, int64_t* counts,
-                            void* stream);
-/* Compact the distinct keys into out_ptr's rows; value of (r, c) is
- * 2 u(seed,2,r,c) - 1. */
-int gridlp_gen_dedupe_fill(const int64_t* ptr, const int32_t* sorted, int64_t m, const int64_t* out_ptr,
-                           uint64_t seed, int32_t* out_cols, double* out_vals, void* stream);
-/* out_i = lo + (hi - lo) u(seed, stream_id, i, 0). */
-int gridlp_gen_uniform(uint64_t seed, uint64_t stream_id, int64_t n, double lo, double hi, double* out,
-                       void* stream);
+/* counts[r] = distinct keys of sorted row r inside [c0, c1); counts[m] = 0. */
+int gridlp_gen_dedupe_count(const int64_t* ptr, const int32_t* sorted, int64_t m, int32_t c0, int32_t c1,
+                            int64_t* counts, void* stream);
+/* Compact those keys into out_ptr's rows as local columns c - c0; value of
+ * global entry (r0 + r, c) is 2 u(seed,2,r0+r,c) - 1. */
+int gridlp_gen_dedupe_fill(const int64_t* ptr, const int32_t* sorted, int64_t m, int64_t r0, int32_t c0,
+                           int32_t c1, const int64_t* out_ptr, uint64_t seed, int32_t* out_cols,
+                           double* out_vals, void* stream);
+/* out_i = lo + (hi - lo) u(seed, stream_id, i0 + i, 0). */
+int gridlp_gen_uniform(uint64_t seed, uint64_t stream_id, int64_t i0, int64_t n, double lo, double hi,
+                       double* out, void* stream);
 /* y = A x with each row summed left to right from +0.0 (scipy csr_matvec
  * order, the reference's rhs = A x_hat, generators.py:125). */
 int gridlp_csr_spmv_seq(const int64_t* ptr, const int32_t* cols, const double* vals, int64_t m,

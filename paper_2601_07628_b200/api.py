@@ -232,6 +232,10 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
     (solver_driver.py:199-227). Returns (engine, layout, eta, omega, timings)."""
     t_start = time.perf_counter()
     timings = {}
+    banded = hasattr(problem, "bands")
+    if banded and (cfg.permutation != "none" or cfg.partitioning != "uniform"):
+        raise ValueError("a band problem (blocks generated per device) needs permutation='none' and "
+                         "partitioning='uniform'")
     grid = GridTopology(1, 1) if force_1x1 else (GridTopology(*cfg.grid) if cfg.grid is not None else None)
     layout = build_layout(problem, n_procs=1 if force_1x1 else cfg.n_procs, block_size=cfg.block_size,
                           seed=cfg.seed, permutation=cfg.permutation, partitioning=cfg.partitioning,
@@ -246,16 +250,19 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
             raise ValueError(f"nccl backend needs world size == grid devices ({R * C}), got {comm.world}")
     else:
         comm = VirtualGrid(R, C)
-    cnorm, bnorm, const = problem_scalars(problem)
-    probe = norm_probe_vector(int(problem.matrix.num_cols), cfg.seed)
+    cnorm, bnorm, const = problem_scalars(problem) if not banded else (0.0, 0.0, 0.0)
+    probe = norm_probe_vector(int(problem.matrix.num_cols), cfg.seed) if not banded else None
     opts = cfg.engine_options()
     for k, v in (engine_overrides or {}).items():
         setattr(opts, k, v)
     engine = eng.PdhgEngine(problem, layout, opts, comm, ops_factory or CudaOps, device,
                             cnorm, bnorm, const)
     timings.update(engine.timings)
+    if banded:
+        cnorm, bnorm = engine.band_scalars()
+        engine.cnorm, engine.bnorm = cnorm, bnorm
     t0 = time.perf_counter()
-    estimate = engine.power_estimate(cfg.power_iterations, probe)
+    estimate = engine.power_estimate(cfg.power_iterations, probe, cfg.seed)
     timings["power_s"] = time.perf_counter() - t0
     timings["estimate"] = estimate
     eta = eta_from_estimate(cfg, estimate)
@@ -302,7 +309,7 @@ def _solve(problem, cfg: SolverConfig, trace=None, force_1x1=False, ops_factory=
         objective=reported_objective(problem, report.obj_primal),
         iterations=out["iterations"], restarts=out["restarts"],
         wall_seconds=time.perf_counter() - t_start, counters=counters,
-        layout=layout_summary(problem, layout, engine.per_device_nnz if comm.kind == "virtual" else None),
+        layout=layout_summary(problem, layout, engine.per_device_nnz),
         timings=timings,
     )
 

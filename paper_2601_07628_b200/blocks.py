@@ -413,3 +413,32 @@ class DeviceSetup:
     def release(self):
         for name in ("src_ptr", "src_col", "src_val", "inv_col", "row_perm", "ws"):
             setattr(self, name, None)
+
+
+class BandSetup(DeviceSetup):
+    """DeviceSetup for a band problem (synth.BandProblem): nothing is
+    uploaded; block(i, j) is generated on the device by the problem's band
+    generator, then transposed / permuted / laid out like any other block."""
+
+    def __init__(self, problem, layout, device):
+        self.lib = native.load()
+        self.device = device
+        self.layout = layout
+        self.bands = problem.bands
+        self.h2d_bytes = 0
+        self.ws, self.ws_bytes = None, 0
+
+    def _workspace(self, items: int, segs: int):
+        need = int(self.lib._lib.gridlp_setup_workspace_bytes(items + 64, segs + 64))
+        if need > self.ws_bytes:
+            self.ws, self.ws_bytes = torch.empty(need, dtype=torch.uint8, device=self.device), need
+
+    def block(self, i: int, j: int) -> DeviceCsrArrays:
+        r0, r1 = self.layout.row_range(i)
+        c0, c1 = self.layout.col_range(j)
+        a = self.bands.block(r0, r1, c0, c1)
+        self._workspace(a.nnz, max(r1 - r0, c1 - c0))
+        return a
+
+    def release(self):
+        self.ws = None

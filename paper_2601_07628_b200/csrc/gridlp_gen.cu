@@ -96,18 +96,33 @@ __global__ void uniform_sample_kernel(uint64_t seed, const int64_t* __restrict__
 // bound (x* = lo, r* = 0.1 + 0.9 u(seed,21,j)), < 0.4 -> at the upper bound
 // (x* = hi, r* = -(0.1 + 0.9 u21)), else interior (x* = lo + (hi - lo)(0.1 +
 // 0.8 u(seed,22,j)), r* = 0).
-__global__ void planted_cols_kernel(uint64_t seed, int64_t n, double lo, double hi, double* __restrict__ x,
-                                    double* __restrict__ r) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    const double st = u01(ghash(seed, 20, (uint64_t)j, 0));
-    const double w = __dadd_rn(0.1, __dmul_rn(0.9, u01(ghash(seed, 21, (uint64_t)j, 0))));
-    if (st < 0.3) { x[j] = lo; r[j] = w; }
-    else if (st < 0.4) { x[j] = hi; r[j] = -w; }
-    else {
-      x[j] = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), __dadd_rn(0.1, __dmul_rn(0.8, u01(ghash(seed, 22, (uint64_t)j, 0))))));
-      r[j] = 0.0;
-    }
+__device__ __forceinline__ void planted_col(uint64_t seed, int64_t j, double lo, double hi, double& x, double& r) {
+  const double st = u01(ghash(seed, 20, (uint64_t)j, 0));
+  const double w = __dadd_rn(0.1, __dmul_rn(0.9, u01(ghash(seed, 21, (uint64_t)j, 0))));
+  if (st < 0.3) { x = lo; r = w; }
+  else if (st < 0.4) { x = hi; r = -w; }
+  else {
+    x = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), __dadd_rn(0.1, __dmul_rn(0.8, u01(ghash(seed, 22, (uint64_t)j, 0))))));
+    r = 0.0;
   }
+}
+
+// planted dual of row i (state u(seed,23,i): < 0.35 -> 0.5 + u24, < 0.7 -> -(0.5 + u24), else 0)
+__device__ __forceinline__ double planted_y(uint64_t seed, int64_t i) {
+  const double st = u01(ghash(seed, 23, (uint64_t)i, 0));
+  const double yv = __dadd_rn(0.5, u01(ghash(seed, 24, (uint64_t)i, 0)));
+  return st < 0.35 ? yv : (st < 0.7 ? -yv : 0.0);
+}
+
+// value of matrix entry (r, c): 2 u(seed, 2, r, c) - 1
+__device__ __forceinline__ double entry_value(uint64_t seed, int64_t r, int64_t c) {
+  return __dsub_rn(__dmul_rn(2.0, u01(ghash(seed, 2, (uint64_t)r, (uint64_t)c))), 1.0);
+}
+
+__global__ void planted_cols_kernel(uint64_t seed, int64_t j0, int64_t n, double lo, double hi,
+                                    double* __restrict__ x, double* __restrict__ r) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    planted_col(seed, j0 + j, lo, hi, x[j], r[j]);
 }
 
 // Planted duals and row bounds around b = A x*: state u(seed,23,i) < 0.35 ->
@@ -115,18 +130,19 @@ __global__ void planted_cols_kernel(uint64_t seed, int64_t n, double lo, double 
 // u(seed,25,i)); < 0.7 -> upper active (y* = -(0.5 + u24), hi = b, lo = b -
 // (0.1 + 0.9 u25)); else inactive (y* = 0, lo = b - (0.1 + 0.9 u25), hi = b +
 // (0.1 + 0.9 u(seed,26,i))).
-__global__ void planted_rows_kernel(uint64_t seed, int64_t m, const double* __restrict__ b, double* __restrict__ y,
-                                    double* __restrict__ lo, double* __restrict__ hi) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void planted_rows_kernel(uint64_t seed, int64_t i0, int64_t m, const double* __restrict__ b,
+                                    double* __restrict__ y, double* __restrict__ lo, double* __restrict__ hi) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + q;
     const double st = u01(ghash(seed, 23, (uint64_t)i, 0));
     const double yv = __dadd_rn(0.5, u01(ghash(seed, 24, (uint64_t)i, 0)));
     const double w = __dadd_rn(0.1, __dmul_rn(0.9, u01(ghash(seed, 25, (uint64_t)i, 0))));
-    const double bi = b[i];
-    if (st < 0.35) { y[i] = yv; lo[i] = bi; hi[i] = __dadd_rn(bi, w); }
-    else if (st < 0.7) { y[i] = -yv; hi[i] = bi; lo[i] = __dsub_rn(bi, w); }
+    const double bi = b[q];
+    if (st < 0.35) { y[q] = yv; lo[q] = bi; hi[q] = __dadd_rn(bi, w); }
+    else if (st < 0.7) { y[q] = -yv; hi[q] = bi; lo[q] = __dsub_rn(bi, w); }
     else {
       const double w2 = __dadd_rn(0.1, __dmul_rn(0.9, u01(ghash(seed, 26, (uint64_t)i, 0))));
-      y[i] = 0.0; lo[i] = __dsub_rn(bi, w); hi[i] = __dadd_rn(bi, w2);
+      y[q] = 0.0; lo[q] = __dsub_rn(bi, w); hi[q] = __dadd_rn(bi, w2);
     }
   }
 }
@@ -138,41 +154,87 @@ __global__ void add_kernel(const double* __restrict__ a, const double* __restric
     out[i] = __dadd_rn(a[i], b[i]);
 }
 
-// distinct columns per (sorted) row
+// distinct columns of each sorted row that fall in [c0, c1)
 __global__ void dedupe_count_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ sorted, int64_t m,
-                                    int64_t* __restrict__ counts) {
+                                    int32_t c0, int32_t c1, int64_t* __restrict__ counts) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = ptr[r], b = ptr[r + 1];
     int64_t cnt = 0;
-    for (int64_t k = a; k < b; ++k) cnt += (k == a || sorted[k] != sorted[k - 1]);
+    for (int64_t k = a; k < b; ++k) {
+      const int32_t c = sorted[k];
+      cnt += (k == a || c != sorted[k - 1]) && c >= c0 && c < c1;
+    }
     counts[r] = cnt;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[m] = 0;
 }
 
-// compact distinct columns; value of (r, c) = 2 u(seed, 2, r, c) - 1
+// compact them with local column ids c - c0; value of global entry (r0 + r, c)
+// is 2 u(seed, 2, r0 + r, c) - 1
 __global__ void dedupe_fill_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ sorted, int64_t m,
-                                   const int64_t* __restrict__ out_ptr, uint64_t seed, int32_t* __restrict__ out_cols,
-                                   double* __restrict__ out_vals) {
+                                   int64_t r0, int32_t c0, int32_t c1, const int64_t* __restrict__ out_ptr,
+                                   uint64_t seed, int32_t* __restrict__ out_cols, double* __restrict__ out_vals) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = ptr[r], b = ptr[r + 1];
     int64_t o = out_ptr[r];
     for (int64_t k = a; k < b; ++k) {
-      if (k != a && sorted[k] == sorted[k - 1]) continue;
       const int32_t c = sorted[k];
-      out_cols[o] = c;
-      out_vals[o] = __dsub_rn(__dmul_rn(2.0, u01(ghash(seed, 2, (uint64_t)r, (uint64_t)c))), 1.0);
+      if ((k != a && c == sorted[k - 1]) || c < c0 || c >= c1) continue;
+      out_cols[o] = c - c0;
+      out_vals[o] = entry_value(seed, r0 + r, c);
       ++o;
     }
   }
 }
 
-// out_i = lo + (hi - lo) * u(seed, stream, i, 0)
-__global__ void uniform_kernel(uint64_t seed, uint64_t stream, int64_t n, double lo, double hi,
+// constant-count draws of rows r0 .. r0+m-1: entry k of row r is
+// floor(u(seed,1,r,k) * n) (the uniform sampler of cfg5, row-major, d per row)
+__global__ void band_draws_kernel(uint64_t seed, int64_t r0, int64_t m, int32_t d, int64_t n,
+                                  int32_t* __restrict__ cols) {
+  const int64_t total = m * d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / d, k = e - q * d;
+    const int64_t c = (int64_t)floor(__dmul_rn(u01(ghash(seed, 1, (uint64_t)(r0 + q), (uint64_t)k)), (double)n));
+    cols[e] = (int32_t)(c < n ? c : n - 1);
+  }
+}
+
+// b[q] = sum over the distinct columns c of sorted full row r0+q, in column
+// order from +0.0, of value(r0+q, c) * x*(c)  (the one-piece A x*)
+__global__ void planted_row_dot_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ sorted, int64_t m,
+                                       int64_t r0, uint64_t seed, double lo, double hi, double* __restrict__ b) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = ptr[q]; k < ptr[q + 1]; ++k) {
+      const int32_t c = sorted[k];
+      if (k != ptr[q] && c == sorted[k - 1]) continue;
+      double x, r;
+      planted_col(seed, c, lo, hi, x, r);
+      s = __dadd_rn(s, __dmul_rn(entry_value(seed, r0 + q, c), x));
+    }
+    b[q] = s;
+  }
+}
+
+// acc[c] continues the sequential column sum of value * y* with the entries
+// of one row chunk, rows ascending (tptr/trows/tvals: the chunk's band block
+// transposed; rows local to the chunk starting at global row r0)
+__global__ void col_accumulate_kernel(const int32_t* __restrict__ tptr, const int32_t* __restrict__ trows,
+                                      const double* __restrict__ tvals, int64_t ncols, int64_t r0, uint64_t seed,
+                                      double* __restrict__ acc) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += (int64_t)gridDim.x * blockDim.x) {
+    double s = acc[c];
+    for (int32_t k = tptr[c]; k < tptr[c + 1]; ++k) s = __dadd_rn(s, __dmul_rn(tvals[k], planted_y(seed, r0 + trows[k])));
+    acc[c] = s;
+  }
+}
+
+// out_i = lo + (hi - lo) * u(seed, stream, i0 + i, 0)
+__global__ void uniform_kernel(uint64_t seed, uint64_t stream, int64_t i0, int64_t n, double lo, double hi,
                                double* __restrict__ out) {
   const double w = __dsub_rn(hi, lo);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = __dadd_rn(lo, __dmul_rn(w, u01(ghash(seed, stream, (uint64_t)i, 0))));
+    out[i] = __dadd_rn(lo, __dmul_rn(w, u01(ghash(seed, stream, (uint64_t)(i0 + i), 0))));
 }
 
 // y_r = sequential sum of the row's products from +0.0 (scipy csr_matvec order)
@@ -283,19 +345,46 @@ int gridlp_gen_uniform_sample(uint64_t seed, const int64_t* alloc_ptr, int64_t m
   return gcuda(cudaGetLastError(), "gen_uniform_sample");
 }
 
-int gridlp_gen_planted_cols(uint64_t seed, int64_t n, double lo, double hi, double* x, double* r, void* stream) {
-  if (n < 0 || (n > 0 && (!x || !r)) || !(lo < hi)) return gfail(GRIDLP_ERR_ARG, "gen_planted_cols: bad argument");
+int gridlp_gen_planted_cols(uint64_t seed, int64_t j0, int64_t n, double lo, double hi, double* x, double* r,
+                            void* stream) {
+  if (n < 0 || j0 < 0 || (n > 0 && (!x || !r)) || !(lo < hi)) return gfail(GRIDLP_ERR_ARG, "gen_planted_cols: bad argument");
   if (n == 0) return GRIDLP_OK;
-  planted_cols_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, n, lo, hi, x, r);
+  planted_cols_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, j0, n, lo, hi, x, r);
   return gcuda(cudaGetLastError(), "gen_planted_cols");
 }
 
-int gridlp_gen_planted_rows(uint64_t seed, int64_t m, const double* b, double* y, double* lo, double* hi,
+int gridlp_gen_planted_rows(uint64_t seed, int64_t i0, int64_t m, const double* b, double* y, double* lo, double* hi,
                             void* stream) {
-  if (m < 0 || (m > 0 && (!b || !y || !lo || !hi))) return gfail(GRIDLP_ERR_ARG, "gen_planted_rows: bad argument");
+  if (m < 0 || i0 < 0 || (m > 0 && (!b || !y || !lo || !hi))) return gfail(GRIDLP_ERR_ARG, "gen_planted_rows: bad argument");
   if (m == 0) return GRIDLP_OK;
-  planted_rows_kernel<<<grid_for(m), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, m, b, y, lo, hi);
+  planted_rows_kernel<<<grid_for(m), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, i0, m, b, y, lo, hi);
   return gcuda(cudaGetLastError(), "gen_planted_rows");
+}
+
+int gridlp_gen_band_draws(uint64_t seed, int64_t r0, int64_t m, int32_t d, int64_t n, int32_t* cols, void* stream) {
+  if (m < 0 || r0 < 0 || d < 1 || n < 1 || n >= (int64_t(1) << 31) || (m > 0 && !cols))
+    return gfail(GRIDLP_ERR_ARG, "gen_band_draws: bad argument");
+  if (m == 0) return GRIDLP_OK;
+  band_draws_kernel<<<148 * 16, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, r0, m, d, n, cols);
+  return gcuda(cudaGetLastError(), "gen_band_draws");
+}
+
+int gridlp_gen_planted_row_dot(const int64_t* ptr, const int32_t* sorted, int64_t m, int64_t r0, uint64_t seed,
+                               double lo, double hi, double* b, void* stream) {
+  if (m < 0 || r0 < 0 || (m > 0 && (!ptr || !b))) return gfail(GRIDLP_ERR_ARG, "gen_planted_row_dot: bad argument");
+  if (m == 0) return GRIDLP_OK;
+  planted_row_dot_kernel<<<grid_for(m), 256, 0, static_cast<cudaStream_t>(stream)>>>(ptr, sorted, m, r0, seed, lo, hi,
+                                                                                     b);
+  return gcuda(cudaGetLastError(), "gen_planted_row_dot");
+}
+
+int gridlp_gen_col_accumulate(const int32_t* tptr, const int32_t* trows, const double* tvals, int64_t ncols,
+                              int64_t r0, uint64_t seed, double* acc, void* stream) {
+  if (ncols < 0 || r0 < 0 || (ncols > 0 && (!tptr || !acc))) return gfail(GRIDLP_ERR_ARG, "gen_col_accumulate: bad argument");
+  if (ncols == 0) return GRIDLP_OK;
+  col_accumulate_kernel<<<grid_for(ncols), 256, 0, static_cast<cudaStream_t>(stream)>>>(tptr, trows, tvals, ncols, r0,
+                                                                                        seed, acc);
+  return gcuda(cudaGetLastError(), "gen_col_accumulate");
 }
 
 int gridlp_gen_add(const double* a, const double* b, int64_t n, double* out, void* stream) {
@@ -318,26 +407,27 @@ int gridlp_gen_sort_rows(const int64_t* ptr, int64_t m, int64_t items, const int
                "gen_sort_rows");
 }
 
-int gridlp_gen_dedupe_count(const int64_t* ptr, const int32_t* sorted, int64_t m, int64_t* counts, void* stream) {
-  if (m < 0 || !ptr || !counts) return gfail(GRIDLP_ERR_ARG, "gen_dedupe_count: bad argument");
-  dedupe_count_kernel<<<grid_for(m), 256, 0, static_cast<cudaStream_t>(stream)>>>(ptr, sorted, m, counts);
+int gridlp_gen_dedupe_count(const int64_t* ptr, const int32_t* sorted, int64_t m, int32_t c0, int32_t c1,
+                            int64_t* counts, void* stream) {
+  if (m < 0 || !ptr || !counts || c1 < c0) return gfail(GRIDLP_ERR_ARG, "gen_dedupe_count: bad argument");
+  dedupe_count_kernel<<<grid_for(m), 256, 0, static_cast<cudaStream_t>(stream)>>>(ptr, sorted, m, c0, c1, counts);
   return gcuda(cudaGetLastError(), "gen_dedupe_count");
 }
 
-int gridlp_gen_dedupe_fill(const int64_t* ptr, const int32_t* sorted, int64_t m, const int64_t* out_ptr,
-                           uint64_t seed, int32_t* out_cols, double* out_vals, void* stream) {
-  if (m < 0 || !ptr || !out_ptr) return gfail(GRIDLP_ERR_ARG, "gen_dedupe_fill: bad argument");
+int gridlp_gen_dedupe_fill(const int64_t* ptr, const int32_t* sorted, int64_t m, int64_t r0, int32_t c0, int32_t c1,
+                           const int64_t* out_ptr, uint64_t seed, int32_t* out_cols, double* out_vals, void* stream) {
+  if (m < 0 || r0 < 0 || !ptr || !out_ptr || c1 < c0) return gfail(GRIDLP_ERR_ARG, "gen_dedupe_fill: bad argument");
   if (m == 0) return GRIDLP_OK;
-  dedupe_fill_kernel<<<grid_for(m), 256, 0, static_cast<cudaStream_t>(stream)>>>(ptr, sorted, m, out_ptr, seed,
-                                                                                 out_cols, out_vals);
+  dedupe_fill_kernel<<<grid_for(m), 256, 0, static_cast<cudaStream_t>(stream)>>>(ptr, sorted, m, r0, c0, c1, out_ptr,
+                                                                                 seed, out_cols, out_vals);
   return gcuda(cudaGetLastError(), "gen_dedupe_fill");
 }
 
-int gridlp_gen_uniform(uint64_t seed, uint64_t stream_id, int64_t n, double lo, double hi, double* out,
+int gridlp_gen_uniform(uint64_t seed, uint64_t stream_id, int64_t i0, int64_t n, double lo, double hi, double* out,
                        void* stream) {
-  if (n < 0 || (n > 0 && !out)) return gfail(GRIDLP_ERR_ARG, "gen_uniform: bad argument");
+  if (n < 0 || i0 < 0 || (n > 0 && !out)) return gfail(GRIDLP_ERR_ARG, "gen_uniform: bad argument");
   if (n == 0) return GRIDLP_OK;
-  uniform_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, stream_id, n, lo, hi, out);
+  uniform_kernel<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, stream_id, i0, n, lo, hi, out);
   return gcuda(cudaGetLastError(), "gen_uniform");
 }
 

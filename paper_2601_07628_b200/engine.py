@@ -30,8 +30,9 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, DeviceCsr, DeviceSetup, inverse_order,
+from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, BandSetup, DeviceCsr, DeviceSetup, inverse_order,
                      length_order, permute_csr, permute_matrix, slice_blocks, transpose)
+from . import native
 from .comm import Ledger, asc_sum
 from .ops import Fused, Parts
 
@@ -193,11 +194,12 @@ class PdhgEngine:
     # ------------------------------------------------------------ setup
     def _build(self, problem):
         lay, dev = self.layout, self.device
-        on_device = dev.type == "cuda" and self.opts.device_setup
+        banded = hasattr(problem, "bands")       # blocks generated per device (synth.BandProblem)
+        on_device = dev.type == "cuda" and (self.opts.device_setup or banded)
         tm = self.timings
         if on_device:
             t0 = time.perf_counter()
-            setup = DeviceSetup(problem, lay, dev)
+            setup = BandSetup(problem, lay, dev) if banded else DeviceSetup(problem, lay, dev)
             torch.cuda.synchronize(dev)
             tm["setup_upload_s"] = time.perf_counter() - t0
             self.setup_h2d_bytes = setup.h2d_bytes
@@ -209,15 +211,19 @@ class PdhgEngine:
             self.setup_h2d_bytes = 0
         cp, rp = lay.perm.col_perm, lay.perm.row_perm
         t0 = time.perf_counter()
-        self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order, setup if on_device else None)
+        # a band problem's row lengths are only known per block, and ranks sharing
+        # a band must agree on its order, so it keeps the layout order
+        self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order and not banded,
+                              setup if on_device else None)
         tm["setup_orders_s"] = time.perf_counter() - t0
         t0 = time.perf_counter()
         f64 = dict(dtype=torch.float64, device=dev)
-        obj = np.asarray(problem.objective, np.float64)[cp]
-        vlo = np.asarray(problem.var_lower, np.float64)[cp]
-        vhi = np.asarray(problem.var_upper, np.float64)[cp]
-        clo = np.asarray(problem.con_lower, np.float64)[rp]
-        chi = np.asarray(problem.con_upper, np.float64)[rp]
+        if not banded:
+            obj = np.asarray(problem.objective, np.float64)[cp]
+            vlo = np.asarray(problem.var_lower, np.float64)[cp]
+            vhi = np.asarray(problem.var_upper, np.float64)[cp]
+            clo = np.asarray(problem.con_lower, np.float64)[rp]
+            chi = np.asarray(problem.con_upper, np.float64)[rp]
         local = self.comm.local
         self.local_cols = sorted({j for _, j in local})
         self.local_rows = sorted({i for i, _ in local})
@@ -226,6 +232,10 @@ class PdhgEngine:
             c0, c1 = lay.col_range(j)
             n = c1 - c0
             t = lambda a: torch.as_tensor(np.ascontiguousarray(self._to_internal_col(j, a[c0:c1])), **f64)  # noqa: E731
+            if banded:
+                cj, lj, hj, _ = problem.bands.col_data(c0, c1)
+                t = lambda a: a  # noqa: E731
+                obj, vlo, vhi = cj, lj, hj
             self.cols[j] = ColState(j, n, t(obj), t(vlo), t(vhi), torch.zeros(n, **f64),
                                     torch.zeros(n, **f64), torch.zeros(n, **f64),
                                     torch.zeros(n, **f64), torch.zeros(n, **f64),
@@ -234,6 +244,10 @@ class PdhgEngine:
             r0, r1 = lay.row_range(i)
             m = r1 - r0
             t = lambda a: torch.as_tensor(np.ascontiguousarray(self._to_internal_row(i, a[r0:r1])), **f64)  # noqa: E731
+            if banded:
+                li, hi_, _ = problem.bands.row_data(r0, r1)
+                t = lambda a: a  # noqa: E731
+                clo, chi = li, hi_
             self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
         kw = dict(exact_row_max=self.opts.exact_row_max, light_row_max=self.opts.light_row_max)
@@ -282,7 +296,11 @@ class PdhgEngine:
             torch.cuda.empty_cache()
             tm["setup_release_s"] = time.perf_counter() - t0
             coords = lay.topology.coords()
-            self.per_device_nnz = [nnz_of.get(c, -1) for c in coords] if self.comm.kind == "virtual" else None
+            if self.comm.kind == "virtual":
+                self.per_device_nnz = [nnz_of.get(c, -1) for c in coords]
+            else:      # one block per rank: gather the counts (same sequence on every rank)
+                tab = self.comm.table({c: np.array([float(v)]) for c, v in nnz_of.items()})
+                self.per_device_nnz = [int(tab[c][0]) for c in coords]
         del host_blocks
         tensors = [t for b in self.blocks.values() for d in (b.A, b.AT) for t in d.tensors()]
         tensors += [t for c in self.cols.values() for t in (c.c, c.lo, c.hi)]
@@ -429,14 +447,43 @@ class PdhgEngine:
         return asc_sum([table[(i, j)][field_] / scale for i in range(self.R) for j in range(self.C)])
 
     # ---------------------------------------------------- power iteration
-    def power_estimate(self, iters: int, probe: np.ndarray) -> float:
-        """estimate_spectral_norm (sparse_kernels.py:61-93) on the grid."""
+    def band_scalars(self):
+        """(||c||, ||finite constraint bounds||) of a band problem from its
+        device vectors: per band dot products (gridlp_op_dot), gathered once
+        and summed in ascending band order (a band's vectors are replicated
+        on its row / column of the grid, so each band is counted once)."""
+        def sq(v, j_slot):
+            fin = torch.where(torch.isfinite(v), v, torch.zeros_like(v))
+            self.ops.dot(fin, fin, j_slot)
+        for j, col in self.cols.items():
+            sq(col.c, self.slot[("v", j)])
+        vals = self.ops.read_slots(self.nslots)
+        csq = {j: float(vals[self.slot[("v", j)], 0]) for j in self.cols}
+        bsq = {}
+        for i, row in self.rows.items():
+            sq(row.lo, self.slot[("u", i)])
+            lo_sq = float(self.ops.read_slots(self.nslots)[self.slot[("u", i)], 0])
+            sq(row.hi, self.slot[("u", i)])
+            bsq[i] = lo_sq + float(self.ops.read_slots(self.nslots)[self.slot[("u", i)], 0])
+        tab = self._table({(i, j): np.array([csq[j], bsq[i]]) for (i, j) in self.comm.local})
+        c_sq = asc_sum([tab[(0, j)][0] for j in range(self.C)])
+        b_sq = asc_sum([tab[(i, 0)][1] for i in range(self.R)])
+        return math.sqrt(c_sq), math.sqrt(b_sq)
+
+    def power_estimate(self, iters: int, probe: np.ndarray | None, probe_seed: int = 0) -> float:
+        """estimate_spectral_norm (sparse_kernels.py:61-93) on the grid.
+        probe=None (band problems): each column band draws its own slice of a
+        hash-based probe, u(seed, 31, j) in [-1, 1), on the device."""
         if iters < 1:
             raise ValueError("iters must be >= 1")
         ops, lay = self.ops, self.layout
         R, C = float(self.R), float(self.C)
         for j, col in self.cols.items():
             c0, c1 = lay.col_range(j)
+            if probe is None:
+                native.load().call("gridlp_gen_uniform", probe_seed, 31, c0, c1 - c0, -1.0, 1.0, col.v.data_ptr(),
+                                   torch.cuda.current_stream(self.device).cuda_stream)
+                continue
             col.v.copy_(torch.as_tensor(np.ascontiguousarray(
                 self._to_internal_col(j, np.asarray(probe[c0:c1], dtype=np.float64)))))
         est = 0.0

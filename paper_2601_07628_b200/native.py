@@ -103,13 +103,16 @@ SIGNATURES = {
     "gridlp_gen_scan64": ([_P, _P, c_int64, _P, ctypes.c_size_t, _P], c_int),
     "gridlp_gen_powerlaw_sample": ([ctypes.c_uint64, _P, c_int64, c_int64, c_double, _P, _P], c_int),
     "gridlp_gen_uniform_sample": ([ctypes.c_uint64, _P, c_int64, c_int64, _P, _P], c_int),
-    "gridlp_gen_planted_cols": ([ctypes.c_uint64, c_int64, c_double, c_double, _P, _P, _P], c_int),
-    "gridlp_gen_planted_rows": ([ctypes.c_uint64, c_int64, _P, _P, _P, _P, _P], c_int),
+    "gridlp_gen_planted_cols": ([ctypes.c_uint64, c_int64, c_int64, c_double, c_double, _P, _P, _P], c_int),
+    "gridlp_gen_planted_rows": ([ctypes.c_uint64, c_int64, c_int64, _P, _P, _P, _P, _P], c_int),
+    "gridlp_gen_band_draws": ([ctypes.c_uint64, c_int64, c_int64, c_int32, c_int64, _P, _P], c_int),
+    "gridlp_gen_planted_row_dot": ([_P, _P, c_int64, c_int64, ctypes.c_uint64, c_double, c_double, _P, _P], c_int),
+    "gridlp_gen_col_accumulate": ([_P, _P, _P, c_int64, c_int64, ctypes.c_uint64, _P, _P], c_int),
     "gridlp_gen_add": ([_P, _P, c_int64, _P, _P], c_int),
     "gridlp_gen_sort_rows": ([_P, c_int64, c_int64, _P, _P, _P, ctypes.c_size_t, _P], c_int),
-    "gridlp_gen_dedupe_count": ([_P, _P, c_int64, _P, _P], c_int),
-    "gridlp_gen_dedupe_fill": ([_P, _P, c_int64, _P, ctypes.c_uint64, _P, _P, _P], c_int),
-    "gridlp_gen_uniform": ([ctypes.c_uint64, ctypes.c_uint64, c_int64, c_double, c_double, _P, _P], c_int),
+    "gridlp_gen_dedupe_count": ([_P, _P, c_int64, c_int32, c_int32, _P, _P], c_int),
+    "gridlp_gen_dedupe_fill": ([_P, _P, c_int64, c_int64, c_int32, c_int32, _P, ctypes.c_uint64, _P, _P, _P], c_int),
+    "gridlp_gen_uniform": ([ctypes.c_uint64, ctypes.c_uint64, c_int64, c_int64, c_double, c_double, _P, _P], c_int),
     "gridlp_csr_spmv_seq": ([_P, _P, _P, c_int64, _P, _P, _P], c_int),
     "gridlp_gen_row_bounds": ([ctypes.c_uint64, c_int64, c_double, _P, _P, _P, _P], c_int),
     "gridlp_gen_mcf_row_lengths": ([c_int64, c_int64, c_int64, _P, _P, _P], c_int),

@@ -169,7 +169,7 @@ class _Gen:
 
     def uniform(self, seed, stream_id, n, lo, hi) -> torch.Tensor:
         out = torch.empty(max(n, 1), dtype=torch.float64, device=self.device)[:n]
-        self.lib.call("gridlp_gen_uniform", seed, stream_id, n, float(lo), float(hi),
+        self.lib.call("gridlp_gen_uniform", seed, stream_id, 0, n, float(lo), float(hi),
                       out.data_ptr() if n else None, self.stream())
         return out
 
@@ -230,13 +230,13 @@ def generate_powerlaw(spec: PowerLawSpec, device=None) -> DeviceLp:
                nb, g.stream())
     del raw, ws
     counts = torch.empty(m + 1, dtype=torch.int64, device=dev)
-    g.lib.call("gridlp_gen_dedupe_count", alloc_ptr.data_ptr(), srt.data_ptr(), m, counts.data_ptr(), g.stream())
+    g.lib.call("gridlp_gen_dedupe_count", alloc_ptr.data_ptr(), srt.data_ptr(), m, 0, n, counts.data_ptr(), g.stream())
     row_ptr = g.scan(counts)
     del counts
     nnz = int(row_ptr[m])
     cols = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)[:nnz]
     vals = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)[:nnz]
-    g.lib.call("gridlp_gen_dedupe_fill", alloc_ptr.data_ptr(), srt.data_ptr(), m, row_ptr.data_ptr(), seed,
+    g.lib.call("gridlp_gen_dedupe_fill", alloc_ptr.data_ptr(), srt.data_ptr(), m, 0, 0, n, row_ptr.data_ptr(), seed,
                cols.data_ptr(), vals.data_ptr(), g.stream())
     del srt, alloc_ptr
     x_hat = g.uniform(seed, 3, n, 1.0, 3.0)
@@ -289,53 +289,171 @@ class PlantedLp(DeviceLp):
         return float(np.dot(self.objective.cpu().numpy(), self.x_hat.cpu().numpy()))
 
 
-def _dedupe_rows(g: _Gen, alloc_ptr, raw, m, seed):
-    total = int(raw.numel())
-    srt = torch.empty_like(raw)
-    ws, nb = g.ws(total, m)
-    g.lib.call("gridlp_gen_sort_rows", alloc_ptr.data_ptr(), m, total, raw.data_ptr(), srt.data_ptr(), ws.data_ptr(),
-               nb, g.stream())
-    del ws
-    counts = torch.empty(m + 1, dtype=torch.int64, device=g.device)
-    g.lib.call("gridlp_gen_dedupe_count", alloc_ptr.data_ptr(), srt.data_ptr(), m, counts.data_ptr(), g.stream())
-    row_ptr = g.scan(counts)
-    nnz = int(row_ptr[m])
-    cols = torch.empty(max(nnz, 1), dtype=torch.int32, device=g.device)[:nnz]
-    vals = torch.empty(max(nnz, 1), dtype=torch.float64, device=g.device)[:nnz]
-    g.lib.call("gridlp_gen_dedupe_fill", alloc_ptr.data_ptr(), srt.data_ptr(), m, row_ptr.data_ptr(), seed,
-               cols.data_ptr(), vals.data_ptr(), g.stream())
-    return row_ptr, cols, vals
+class PlantedBands:
+    """The cfg5 planted LP generated band by band: `block(r0, r1, c0, c1)`
+    builds one grid block, `row_data` / `col_data` one row / column band's
+    vectors, and no device ever holds more than one block plus a chunk of
+    draws — the path for LPs whose A + Aᵀ exceed one GPU. Every value is the
+    one-piece instance's bit for bit: b = A x* is summed over each full row
+    (regenerated from the hash), c = Aᵀ y* + r* is accumulated column by
+    column over all rows in ascending order, chunk after chunk."""
+
+    def __init__(self, spec: PlantedSpec, device=None, chunk_draws: int = 1 << 27):
+        self.spec = spec
+        self.g = _Gen(device)
+        self.chunk_rows = max(1, chunk_draws // spec.draws_per_row)
+        self.f64 = dict(dtype=torch.float64, device=self.g.device)
+
+    @property
+    def shape(self):
+        return self.spec.num_rows, self.spec.num_cols
+
+    def _sorted_rows(self, r0: int, r1: int):
+        """Draws of rows [r0, r1), sorted inside each row."""
+        g, sp_, d = self.g, self.spec, self.spec.draws_per_row
+        m = r1 - r0
+        raw = torch.empty(max(m * d, 1), dtype=torch.int32, device=g.device)
+        g.lib.call("gridlp_gen_band_draws", sp_.seed, r0, m, d, sp_.num_cols, raw.data_ptr(), g.stream())
+        ptr = torch.arange(m + 1, dtype=torch.int64, device=g.device) * d
+        srt = torch.empty_like(raw)
+        ws, nb = g.ws(m * d, m)
+        g.lib.call("gridlp_gen_sort_rows", ptr.data_ptr(), m, m * d, raw.data_ptr(), srt.data_ptr(), ws.data_ptr(), nb,
+                   g.stream())
+        return ptr, srt
+
+    def _band_csr(self, ptr, srt, m: int, r0: int, c0: int, c1: int):
+        """Distinct entries of the sorted rows inside [c0, c1): int64 row
+        pointers, local int32 columns, values."""
+        g = self.g
+        counts = torch.empty(m + 1, dtype=torch.int64, device=g.device)
+        g.lib.call("gridlp_gen_dedupe_count", ptr.data_ptr(), srt.data_ptr(), m, c0, c1, counts.data_ptr(), g.stream())
+        out_ptr = g.scan(counts)
+        nnz = int(out_ptr[m])
+        cols = torch.empty(nnz + 8, dtype=torch.int32, device=g.device)
+        vals = torch.empty(nnz + 8, **self.f64)
+        g.lib.call("gridlp_gen_dedupe_fill", ptr.data_ptr(), srt.data_ptr(), m, r0, c0, c1, out_ptr.data_ptr(),
+                   self.spec.seed, cols.data_ptr(), vals.data_ptr(), g.stream())
+        return out_ptr, cols, vals, nnz
+
+    def _chunks(self, r0: int, r1: int):
+        for a in range(r0, r1, self.chunk_rows):
+            yield a, min(r1, a + self.chunk_rows)
+
+    def block(self, r0: int, r1: int, c0: int, c1: int):
+        """Grid block rows [r0, r1) x columns [c0, c1) as DeviceCsrArrays
+        (int32 row pointers, local column ids, entries sorted by column)."""
+        from .blocks import DeviceCsrArrays
+
+        parts = []
+        for a, b in self._chunks(r0, r1):
+            ptr, srt = self._sorted_rows(a, b)
+            parts.append(self._band_csr(ptr, srt, b - a, a, c0, c1))
+            del ptr, srt
+        nnz = sum(p[3] for p in parts)
+        if nnz >= 2 ** 31 - 64:
+            raise ValueError("block nnz must be < 2^31: use a finer grid")
+        dev = self.g.device
+        rp = torch.empty(r1 - r0 + 1, dtype=torch.int64, device=dev)
+        cols = torch.empty(nnz + 8, dtype=torch.int32, device=dev)
+        vals = torch.empty(nnz + 8, **self.f64)
+        rp[0], row, off = 0, 0, 0
+        for p_, c_, v_, k in parts:
+            mm = p_.numel() - 1
+            rp[row + 1: row + mm + 1] = p_[1:] + off
+            cols[off: off + k] = c_[:k]
+            vals[off: off + k] = v_[:k]
+            row, off = row + mm, off + k
+        return DeviceCsrArrays(r1 - r0, c1 - c0, nnz, rp.to(torch.int32), cols, vals)
+
+    def row_data(self, r0: int, r1: int):
+        """(con_lower, con_upper, y*) of rows [r0, r1); b = A x* over full rows."""
+        g, sp_ = self.g, self.spec
+        m = r1 - r0
+        b = torch.empty(max(m, 1), **self.f64)[:m]
+        for a, e in self._chunks(r0, r1):
+            ptr, srt = self._sorted_rows(a, e)
+            g.lib.call("gridlp_gen_planted_row_dot", ptr.data_ptr(), srt.data_ptr(), e - a, a, sp_.seed, sp_.box_low,
+                       sp_.box_high, b[a - r0:].data_ptr(), g.stream())
+        y, lo, hi = (torch.empty(max(m, 1), **self.f64)[:m] for _ in range(3))
+        if m:
+            g.lib.call("gridlp_gen_planted_rows", sp_.seed, r0, m, b.data_ptr(), y.data_ptr(), lo.data_ptr(),
+                       hi.data_ptr(), g.stream())
+        return lo, hi, y
+
+    def col_data(self, c0: int, c1: int):
+        """(c, var_lower, var_upper, x*) of columns [c0, c1); c = Aᵀ y* + r*
+        accumulated over every row chunk in ascending order."""
+        g, sp_ = self.g, self.spec
+        n = c1 - c0
+        acc = torch.zeros(max(n, 1), **self.f64)[:n]
+        wsb = 0
+        for a, e in self._chunks(0, sp_.num_rows):
+            ptr, srt = self._sorted_rows(a, e)
+            bp, bc, bv, nnz = self._band_csr(ptr, srt, e - a, a, c0, c1)
+            del ptr, srt
+            need = int(g.lib._lib.gridlp_setup_workspace_bytes(nnz + 64, max(e - a, n) + 64))
+            if need > wsb:
+                ws, wsb = torch.empty(need, dtype=torch.uint8, device=g.device), need
+            tptr = torch.empty(n + 1, dtype=torch.int32, device=g.device)
+            trow = torch.empty(nnz + 8, dtype=torch.int32, device=g.device)
+            tval = torch.empty(nnz + 8, **self.f64)
+            g.lib.call("gridlp_csr_transpose", bp.to(torch.int32).data_ptr(), bc.data_ptr(), bv.data_ptr(), e - a, n,
+                       nnz, tptr.data_ptr(), trow.data_ptr(), tval.data_ptr(), ws.data_ptr(), wsb, g.stream())
+            g.lib.call("gridlp_gen_col_accumulate", tptr.data_ptr(), trow.data_ptr(), tval.data_ptr(), n, a, sp_.seed,
+                       acc.data_ptr(), g.stream())
+        x, r = torch.empty(max(n, 1), **self.f64)[:n], torch.empty(max(n, 1), **self.f64)[:n]
+        c = torch.empty(max(n, 1), **self.f64)[:n]
+        if n:
+            g.lib.call("gridlp_gen_planted_cols", sp_.seed, c0, n, sp_.box_low, sp_.box_high, x.data_ptr(), r.data_ptr(),
+                       g.stream())
+            g.lib.call("gridlp_gen_add", acc.data_ptr(), r.data_ptr(), n, c.data_ptr(), g.stream())
+        return c, torch.full((n,), sp_.box_low, **self.f64), torch.full((n,), sp_.box_high, **self.f64), x
 
 
 def generate_planted(spec: PlantedSpec, device=None) -> PlantedLp:
-    g = _Gen(device)
-    dev, m, n, seed = g.device, spec.num_rows, spec.num_cols, spec.seed
-    f64 = dict(dtype=torch.float64, device=dev)
-    lens = torch.full((m + 1,), spec.draws_per_row, dtype=torch.int64, device=dev)
-    lens[m] = 0
-    alloc_ptr = g.scan(lens)
-    raw = torch.empty(m * spec.draws_per_row, dtype=torch.int32, device=dev)
-    g.lib.call("gridlp_gen_uniform_sample", seed, alloc_ptr.data_ptr(), m, n, raw.data_ptr(), g.stream())
-    row_ptr, cols, vals = _dedupe_rows(g, alloc_ptr, raw, m, seed)
-    del raw, alloc_ptr
-    x, r = torch.empty(n, **f64), torch.empty(n, **f64)
-    g.lib.call("gridlp_gen_planted_cols", seed, n, spec.box_low, spec.box_high, x.data_ptr(), r.data_ptr(), g.stream())
-    b = g.spmv_seq(row_ptr, cols, vals, m, x)
-    y, lo, hi = torch.empty(m, **f64), torch.empty(m, **f64), torch.empty(m, **f64)
-    g.lib.call("gridlp_gen_planted_rows", seed, m, b.data_ptr(), y.data_ptr(), lo.data_ptr(), hi.data_ptr(),
-               g.stream())
-    # c = Aᵀ y* + r*: sequential sums along the rows of the stored transpose
-    nnz = int(cols.numel())
-    wsb = int(g.lib._lib.gridlp_setup_workspace_bytes(nnz + 64, max(m, n) + 64))
-    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
-    tptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
-    tcol = torch.empty(nnz + 8, dtype=torch.int32, device=dev)
-    tval = torch.empty(nnz + 8, **f64)
-    g.lib.call("gridlp_csr_transpose", row_ptr.to(torch.int32).data_ptr(), cols.data_ptr(), vals.data_ptr(), m, n,
-               nnz, tptr.data_ptr(), tcol.data_ptr(), tval.data_ptr(), ws.data_ptr(), wsb, g.stream())
-    aty = g.spmv_seq(tptr.to(torch.int64), tcol, tval, n, y)
-    del ws, tptr, tcol, tval
-    c = torch.empty(n, **f64)
-    g.lib.call("gridlp_gen_add", aty.data_ptr(), r.data_ptr(), n, c.data_ptr(), g.stream())
-    return PlantedLp(m, n, row_ptr, cols, vals, c, torch.full((n,), spec.box_low, **f64),
-                     torch.full((n,), spec.box_high, **f64), lo, hi, x, y_star=y)
+    """The whole cfg5 instance on one device (small sizes; `PlantedBands`
+    builds the same instance block by block)."""
+    bands = PlantedBands(spec, device)
+    m, n = spec.num_rows, spec.num_cols
+    blk = bands.block(0, m, 0, n)
+    lo, hi, y = bands.row_data(0, m)
+    c, vlo, vhi, x = bands.col_data(0, n)
+    return PlantedLp(m, n, blk.ptr.to(torch.int64), blk.col[: blk.nnz], blk.val[: blk.nnz], c, vlo, vhi, lo, hi, x,
+                     y_star=y)
+
+
+class _Shape:
+    """Matrix stand-in of a band problem: dimensions only."""
+
+    row_offsets = col_indices = values = None
+
+    def __init__(self, m: int, n: int):
+        self.num_rows, self.num_cols = m, n
+
+    @property
+    def nnz(self):
+        raise ValueError("a band problem has no global matrix; its blocks are generated per device")
+
+
+class BandProblem:
+    """LpProblem stand-in for solve() whose blocks and band vectors come from
+    a generator (`bands`) instead of host arrays: each device builds only its
+    own block, so the LP can exceed one GPU's memory and the host's. Needs
+    permutation "none" and partitioning "uniform" (the generator is already
+    unstructured); x / y are returned in full on the host."""
+
+    objective_constant = 0.0
+    maximize = False
+
+    def __init__(self, bands: PlantedBands, name: str = "planted"):
+        self.bands = bands
+        self.matrix = _Shape(*bands.shape)
+        self.name = name
+
+    @property
+    def num_constraints(self):
+        return self.matrix.num_rows
+
+    @property
+    def num_variables(self):
+        return self.matrix.num_cols

@@ -70,3 +70,46 @@ def test_planted_optimum_is_reached():
     got = solve(dl.to_problem(), SolverConfig(tolerance=1e-7, seed=7, n_procs=4, grid=(2, 2), max_iterations=200_000))
     assert got.status == "optimal"
     assert abs(got.objective - star) <= 1e-5 * (1.0 + abs(star))
+
+
+def test_planted_bands_equal_one_piece_instance():
+    """Block-by-block generation (small chunks, so the chunk loops run) gives
+    the one-piece instance bit for bit: every block, b and c."""
+    import scipy.sparse as sp
+
+    from paper_2601_07628_b200.synth import PlantedBands, PlantedSpec
+
+    spec = PlantedSpec(900, 1300, 7, seed=4)
+    want = synth_oracle.planted(900, 1300, 7, seed=4)
+    A = sp.csr_matrix((want["val"], want["col"], want["ptr"]), shape=(900, 1300))
+    bands = PlantedBands(spec, DEV, chunk_draws=7 * 128)
+    for (r0, r1), (c0, c1) in (((0, 300), (0, 500)), ((300, 900), (500, 1300)), ((0, 900), (200, 260))):
+        blk = bands.block(r0, r1, c0, c1)
+        ref = A[r0:r1, c0:c1].tocsr()
+        ref.sort_indices()
+        np.testing.assert_array_equal(blk.ptr.cpu().numpy(), ref.indptr)
+        np.testing.assert_array_equal(blk.col[: blk.nnz].cpu().numpy(), ref.indices)
+        np.testing.assert_array_equal(blk.val[: blk.nnz].cpu().numpy(), ref.data)
+        lo, hi, y = bands.row_data(r0, r1)
+        np.testing.assert_array_equal(lo.cpu().numpy(), want["con_lo"][r0:r1])
+        np.testing.assert_array_equal(hi.cpu().numpy(), want["con_hi"][r0:r1])
+        c, _, _, x = bands.col_data(c0, c1)
+        np.testing.assert_array_equal(c.cpu().numpy(), want["c"][c0:c1])
+        np.testing.assert_array_equal(x.cpu().numpy(), want["x_hat"][c0:c1])
+
+
+def test_band_problem_solves_to_planted_optimum():
+    """solve() on a BandProblem: each grid block generated where it lives,
+    no global matrix anywhere; reaches the analytic optimum c·x*."""
+    from paper_2601_07628_b200.synth import BandProblem, PlantedBands, PlantedSpec, generate_planted
+
+    spec = PlantedSpec(2500, 3500, 6, seed=9)
+    star = generate_planted(spec, DEV).optimal_objective()
+    prob = BandProblem(PlantedBands(spec, DEV, chunk_draws=6 * 700))
+    got = solve(prob, SolverConfig(tolerance=1e-7, seed=9, n_procs=6, grid=(2, 3), permutation="none",
+                                   partitioning="uniform", max_iterations=200_000))
+    assert got.status == "optimal"
+    assert abs(got.objective - star) <= 1e-5 * (1.0 + abs(star))
+    assert got.layout["total_nnz"] > 0 and len(got.x) == 3500 and len(got.y) == 2500
+    with pytest.raises(ValueError, match="permutation='none'"):
+        solve(prob, SolverConfig(n_procs=4, grid=(2, 2)))
