@@ -58,11 +58,16 @@ CONFIGS = {
                   inequality_fraction=0.3, seed=0),
     "cfg4": dict(gen="mcf", num_nodes=2_000, num_arcs=128_000, num_commodities=1_300, seed=0),
     "cfg4s": dict(gen="mcf", num_nodes=500, num_arcs=32_000, num_commodities=200, seed=0),
+    # planted-optimum LP generated block by block (synth.BandProblem): cfg5 is
+    # ~8B nnz (A + A^T > 180 GB, needs >= 4 GPUs); cfg5s is a 1/20 one-GPU cut
+    "cfg5": dict(gen="planted", num_rows=250_000_000, num_cols=400_000_000, draws_per_row=32, seed=0),
+    "cfg5s": dict(gen="planted", num_rows=12_500_000, num_cols=20_000_000, draws_per_row=32, seed=0),
 }
 WORKLOADS = {
     "uniform_random": "reference generator uniform_random LP",
     "powerlaw": "power-law (Chung-Lu, exponent 0.8, heavy-first) feasible LP, device generator",
     "mcf": "block-angular multi-commodity flow LP (planted flow), device generator",
+    "planted": "uniform random LP with a planted optimum, generated block by block on each device",
 }
 METRIC = "PDHG iters/s & time-to-1e-4 KKT (FP64) at 1/2/4/8 B200; SpMV HBM GB/s"
 
@@ -144,6 +149,12 @@ def make_problem(name):
     gen = spec.pop("gen", None)
     if gen is None:
         p = generate(GeneratorSpec(**spec))
+    elif gen == "planted":
+        from paper_2601_07628_b200 import synth
+
+        p = synth.BandProblem(synth.PlantedBands(synth.PlantedSpec(**spec)), name)
+        log(f"[bench] {name}: band problem m={p.num_constraints} n={p.num_variables} (blocks generated per device)")
+        return p
     else:
         import torch
 
@@ -352,6 +363,8 @@ def run_ours(args, rank, world, local_rank):
         base = dict(n_procs=R * C, grid=(R, C))       # virtual grid: all blocks on this GPU
     else:
         base = dict(n_procs=1)
+    if hasattr(p, "bands"):
+        base.update(permutation="none", partitioning="uniform")
     if args.permutation:
         base["permutation"] = args.permutation
     if args.partitioning:
@@ -367,6 +380,7 @@ def run_ours(args, rank, world, local_rank):
     log(f"[bench] rank {rank}: setup {time.perf_counter() - t0:.1f}s {tim}")
     R, C = layout.topology.rows, layout.topology.cols
     pdn = [v for v in (engine.per_device_nnz or []) if v >= 0]
+    nnz_total = int(sum(pdn))
     balance = (max(pdn) / (sum(pdn) / len(pdn))) if pdn and sum(pdn) else None
     engine.start(eta, omega)
     for _ in range(args.warmup):
@@ -413,7 +427,7 @@ def run_ours(args, rank, world, local_rank):
     restarts = engine._s["epoch"]
     del engine
     torch.cuda.empty_cache()
-    spmv = spmv_compare(p, dev) if world == 1 and not args.no_spmv else None
+    spmv = spmv_compare(p, dev) if world == 1 and not args.no_spmv and not hasattr(p, "bands") else None
 
     # e2e through the public API, host arrays in, host arrays out
     e2e = None
@@ -439,7 +453,7 @@ def run_ours(args, rank, world, local_rank):
                "kkt": res.report.as_dict(),
                "breakdown_s": {k: v for k, v in res.timings.items() if k.endswith("_s")}}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not hasattr(p, "bands"):
         cpu = cpu_baseline(p, args.cpu_sample_iters)
     if rank != 0:
         return
@@ -450,12 +464,12 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {workload_name(args.config)}, m={p.num_constraints} "
-                               f"n={p.num_variables} nnz={p.matrix.nnz}, ineq 0.3, seed 0; step = 64 PDHG "
+                               f"n={p.num_variables} nnz={nnz_total}, spec {CONFIGS[args.config]}; step = 64 PDHG "
                                f"iterations + 1 KKT/restart pass",
                    "grid": [R, C], "permutation": cfg.permutation, "partitioning": cfg.partitioning,
                    "block_nnz_max_over_mean": balance,
                    "l2": "inputs larger than L2 (A + A^T = "
-                   f"{24 * p.matrix.nnz / 1e6:.0f} MB of 126 MB L2 per iteration, streamed evict-first)",
+                   f"{24 * nnz_total / 1e6:.0f} MB of 126 MB L2 per iteration, streamed evict-first)",
                    "restarts_in_timed_region": restarts},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
