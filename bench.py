@@ -296,7 +296,7 @@ def run_reference(args, rank, world):
     from paper_2601_07628_b200 import select_grid
 
     p = make_problem(args.config)
-    threads = max(1, min(os.cpu_count() or 1, 8))
+    threads = max(1, min(os.cpu_count() or 1, 32))      # every host core the box has (capped at 32 blocks)
     g = select_grid(p.num_constraints, p.num_variables, threads)
     sample = args.ref_sample_iters
     ctx = threadpool_limits(1) if threadpool_limits else None
