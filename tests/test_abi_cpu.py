@@ -66,6 +66,11 @@ def test_config_validation():
     with pytest.raises(ValueError):
         SolverConfig(comm_backend="mpi")
     SolverConfig(comm_backend="threads")  # reference executors alias the device grid
+    with pytest.raises(ValueError, match="scaling"):
+        SolverConfig(scaling="l2")
+    with pytest.raises(ValueError, match="ruiz_iterations"):
+        SolverConfig(scaling="ruiz", ruiz_iterations=-1)
+    assert SolverConfig().scaling == "none"          # the reference's behaviour by default
 
 
 def test_solve_without_gpu_fails_loudly():
