@@ -1,0 +1,143 @@
+"""Solve-level behaviour of the public API on the B200, restating the
+reference's own solver tests (reference tests/test_solver_driver.py
+"reusable as-is against the new package"): analytic optima, cross-grid
+consistency, determinism, the single-device twin, maximisation, degenerate
+shapes, failure statuses, the JSON payload and the per-pass log line."""
+
+import logging
+import re
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2601_07628_b200 import (  # noqa: E402
+    GeneratorSpec, LpProblem, SolverConfig, SparseMatrix, box_lp_optimum, generate, objective_value, parse_mps,
+    reference_solve, solve,
+)
+
+INF = float("inf")
+
+
+def rand_lp(seed, m=14, n=18, nnz=140, ineq=0.4):
+    return generate(GeneratorSpec(kind="uniform_random", num_rows=m, num_cols=n, nnz_target=nnz,
+                                  inequality_fraction=ineq, seed=seed))
+
+
+def tiny(rows, cols, vals, shape, c, vlo, vhi, clo, chi):
+    return LpProblem(SparseMatrix.from_coo(*shape, rows, cols, vals), np.array(c, float), np.array(vlo, float),
+                     np.array(vhi, float), np.array(clo, float), np.array(chi, float))
+
+
+class TestAnalyticOptima:
+    def test_lower_bounded_variable(self):
+        # min x s.t. x >= 1, x in [0, 10]
+        r = solve(tiny([0], [0], [1.0], (1, 1), [1.0], [0.0], [10.0], [1.0], [INF]), SolverConfig(tolerance=1e-6))
+        assert r.status == "optimal" and abs(r.objective - 1.0) <= 2e-6 and abs(r.x[0] - 1.0) <= 1e-4
+
+    def test_packing_pair(self):
+        # min -x - y s.t. x + y <= 1, x, y in [0, 1]
+        p = tiny([0, 0], [0, 1], [1.0, 1.0], (1, 2), [-1.0, -1.0], [0, 0], [1, 1], [-INF], [1.0])
+        r = solve(p, SolverConfig(tolerance=1e-6))
+        assert r.status == "optimal" and abs(r.objective + 1.0) <= 2e-6
+
+    def test_zero_objective_box_stops_at_first_pass(self):
+        p = tiny([0, 0], [0, 1], [1.0, 1.0], (1, 2), [0, 0], [-1, -1], [1, 1], [-2.0], [2.0])
+        r = solve(p, SolverConfig(tolerance=1e-9))
+        assert (r.status, r.iterations, r.restarts) == ("optimal", 64, 0)
+        np.testing.assert_array_equal(r.y, [0.0])
+        assert reference_solve(p, SolverConfig(tolerance=1e-9)).report.overall == 0.0
+
+
+@pytest.mark.parametrize("seed", [0, 3, 8])
+def test_cross_grid_consistency(seed):
+    p = rand_lp(seed, m=12, n=16, nnz=90)
+    res = [solve(p, SolverConfig(tolerance=1e-8, n_procs=k, seed=seed)) for k in (1, 2, 4)]
+    assert {r.status for r in res} == {"optimal"}
+    obj = [r.objective for r in res]
+    assert max(obj) - min(obj) <= 1e-9 * max(1.0, max(abs(v) for v in obj))
+
+
+def test_bit_identical_repeat_solves_and_backend_aliases():
+    p = rand_lp(5, m=10, n=14, nnz=70)
+    cfg = SolverConfig(tolerance=1e-7, n_procs=4, seed=2)
+    a, b = solve(p, cfg), solve(p, cfg)
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
+    assert (a.report, a.iterations, a.restarts, a.counters) == (b.report, b.iterations, b.restarts, b.counters)
+    assert a.to_json_dict() == b.to_json_dict()
+    base = dict(tolerance=1e-7, n_procs=4, seed=1, grid=(2, 2))
+    c = solve(p, SolverConfig(**base, comm_backend="cooperative"))
+    d = solve(p, SolverConfig(**base, comm_backend="threads"))
+    np.testing.assert_array_equal(c.x, d.x)
+    assert c.counters == d.counters
+
+
+@pytest.mark.parametrize("seed", [0, 7])
+def test_single_device_grid_equals_reference_twin(seed):
+    p = rand_lp(seed, m=9, n=12, nnz=55, ineq=0.5)
+    cfg = SolverConfig(tolerance=1e-8, n_procs=1, seed=seed)
+    a, b = solve(p, cfg), reference_solve(p, cfg)
+    assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
+    assert a.report == b.report
+
+
+def test_maximisation_reports_declared_sense():
+    text = "OBJSENSE\n    MAX\nROWS\n N obj\n L cap\nCOLUMNS\n    x  obj  2.0  cap  1.0\nRHS\n    RHS  cap  3.0\nENDATA\n"
+    r = solve(parse_mps(text), SolverConfig(tolerance=1e-8))
+    assert abs(r.objective - 6.0) <= 1e-5          # max 2x s.t. x <= 3
+
+
+class TestDegenerateShapes:
+    def test_constraint_free_box_lp(self):
+        p = generate(GeneratorSpec(kind="box_lp_known_optimum", num_cols=12, seed=4))
+        r = solve(p, SolverConfig(tolerance=1e-9, n_procs=4))
+        want = box_lp_optimum(p)
+        assert r.status == "optimal" and abs(r.objective - want) <= 1e-8 * max(1.0, abs(want))
+
+    def test_variable_free_problem(self):
+        p = LpProblem(SparseMatrix.from_coo(2, 0, [], [], []), np.empty(0), np.empty(0), np.empty(0),
+                      np.array([-1.0, -INF]), np.array([1.0, 5.0]))
+        r = solve(p, SolverConfig(tolerance=1e-9))
+        assert r.status == "optimal" and r.objective == 0.0
+
+
+class TestFailureModes:
+    def test_divergence_is_a_status(self):
+        p = tiny([0], [0], [1.0], (1, 1), [0.0], [-INF], [INF], [1.0], [1.0])
+        r = solve(p, SolverConfig(tolerance=1e-8, eta=10.0, max_iterations=5000, kkt_interval=64))
+        assert r.status == "numerical_failure"
+
+    def test_iteration_limit(self):
+        r = solve(rand_lp(10, m=12, n=16, nnz=90), SolverConfig(tolerance=1e-12, max_iterations=96))
+        assert (r.status, r.iterations) == ("iteration_limit", 96) and r.report is not None
+
+    def test_time_limit(self):
+        r = solve(rand_lp(11, m=12, n=16, nnz=90),
+                  SolverConfig(tolerance=1e-14, time_limit_seconds=0.0, kkt_interval=8, max_iterations=10 ** 9))
+        assert (r.status, r.iterations) == ("time_limit", 8)
+
+
+def test_json_payload_and_objective_consistency():
+    r = solve(rand_lp(12, m=8, n=10, nnz=40), SolverConfig(tolerance=1e-6, n_procs=2))
+    pay = r.to_json_dict()
+    assert set(pay) == {"status", "objective", "kkt", "iterations", "restarts", "counters", "layout"}
+    assert set(pay["kkt"]) == {"r_primal", "r_dual", "r_gap", "obj_primal", "obj_dual", "overall"}
+    assert {c["device"][0] for c in pay["counters"]["total"]} == {0}
+    assert pay["layout"]["grid"]["rows"] >= 1
+    p = rand_lp(13, m=9, n=11, nnz=50)
+    r = solve(p, SolverConfig(tolerance=1e-8, n_procs=4, seed=3))
+    v = objective_value(p, r.x)
+    assert abs(v - r.objective) <= 1e-9 * max(1.0, abs(v))
+
+
+def test_pass_log_line(caplog):
+    pat = re.compile(r"iter=(\d+) r_primal=(\S+) r_dual=(\S+) r_gap=(\S+) obj_p=(\S+) obj_d=(\S+) "
+                     r"omega=(\S+) eta=(\S+) epoch=(\d+)$")
+    with caplog.at_level(logging.INFO, logger="gridlp.solver"):
+        solve(rand_lp(14, m=8, n=10, nnz=40), SolverConfig(tolerance=1e-300, max_iterations=128, kkt_interval=64))
+    lines = [r.getMessage() for r in caplog.records if r.name == "gridlp.solver"]
+    assert [int(pat.match(x).group(1)) for x in lines] == [64, 128]
