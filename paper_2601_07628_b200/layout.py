@@ -208,8 +208,9 @@ def build_layout(problem, n_procs: int, block_size: int = 64, seed: int = 0,
     if partitioning == "uniform":
         rc, cc = uniform_cuts(m, grid.rows), uniform_cuts(n, grid.cols)
     else:
-        rc = nnz_balanced_cuts(_row_counts(A)[rp], grid.rows)
-        cc = nnz_balanced_cuts(_col_counts(A)[cp], grid.cols)
+        # one part needs no counts: the cut is [0, length] (skips an nnz-long bincount)
+        rc = nnz_balanced_cuts(_row_counts(A)[rp], grid.rows) if grid.rows > 1 else np.array([0, m], np.int64)
+        cc = nnz_balanced_cuts(_col_counts(A)[cp], grid.cols) if grid.cols > 1 else np.array([0, n], np.int64)
     return PartitionLayout(grid, perm, rc, cc)
 
 
