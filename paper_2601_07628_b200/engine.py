@@ -260,6 +260,8 @@ class PdhgEngine:
                 torch.cuda.synchronize(dev)
                 t1 = time.perf_counter()
                 at = setup.transpose(a)
+                torch.cuda.synchronize(dev)
+                tm["setup_transpose_only_s"] = tm.get("setup_transpose_only_s", 0.0) + time.perf_counter() - t1
                 if self.sorted:
                     # internal order: A_ij rows by sigma_i, columns by tau_j (and the
                     # transpose's the other way round); the transpose is taken first
@@ -291,9 +293,8 @@ class PdhgEngine:
                 self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(ht, dev, **kw))
         if on_device:
             t0 = time.perf_counter()
-            setup.release()
+            setup.release()     # the freed setup buffers stay in torch's caching allocator for reuse
             del setup
-            torch.cuda.empty_cache()
             tm["setup_release_s"] = time.perf_counter() - t0
             coords = lay.topology.coords()
             if self.comm.kind == "virtual":
