@@ -125,3 +125,17 @@ def test_sorted_internal_order_solves_like_natural(grid):
     assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
     np.testing.assert_allclose(a.x, b.x, rtol=1e-9, atol=1e-9)
     np.testing.assert_allclose(a.y, b.y, rtol=1e-9, atol=1e-9)
+
+
+def test_staged_upload_converts_and_matches():
+    from paper_2601_07628_b200.blocks import STAGING_BYTES, upload
+
+    rng = np.random.default_rng(0)
+    big = STAGING_BYTES // 4 * 2 + 12345            # three chunks of int32
+    cols = rng.integers(0, 2 ** 31 - 1, big)          # int64 source
+    got = upload(cols, np.int32, DEV)
+    assert got.dtype == torch.int32
+    np.testing.assert_array_equal(got.cpu().numpy(), cols.astype(np.int32))
+    vals = rng.standard_normal(STAGING_BYTES // 8 + 7)
+    np.testing.assert_array_equal(upload(vals, np.float64, DEV).cpu().numpy(), vals)
+    assert upload(np.zeros(0), np.float64, DEV).numel() == 0
