@@ -116,6 +116,19 @@ def length_order(lens: np.ndarray) -> np.ndarray:
     return np.argsort((65535 - np.minimum(cls, 65535)).astype(np.uint16), kind="stable")
 
 
+def length_order_device(lens: torch.Tensor) -> torch.Tensor:
+    """length_order on the device (int64 indices): the same classes
+    floor(8 log2(len + 1)), longest class first, stable inside a class."""
+    cls = torch.floor(LENGTH_BUCKETS_PER_OCTAVE * torch.log2(lens.to(torch.float64) + 1.0)).to(torch.int64)
+    return torch.sort(-cls, stable=True).indices
+
+
+def inverse_order_device(order: torch.Tensor) -> torch.Tensor:
+    inv = torch.empty_like(order)
+    inv[order] = torch.arange(order.numel(), dtype=order.dtype, device=order.device)
+    return inv
+
+
 def inverse_order(order: np.ndarray) -> np.ndarray:
     inv = np.empty_like(order)
     inv[order] = np.arange(len(order), dtype=order.dtype)
@@ -396,6 +409,13 @@ class DeviceSetup:
                       a.num_cols, a.nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), self.ws.data_ptr(),
                       self.ws_bytes, self._stream())
         return DeviceCsrArrays(a.num_cols, a.num_rows, a.nnz, ptr, col, val)
+
+    def col_counts_device(self) -> torch.Tensor:
+        """Entries per column of the uploaded original matrix (device int32)."""
+        n = int(self.inv_col.numel()) if self.n else 0
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        self.lib.call("gridlp_col_counts", self.src_col.data_ptr(), self.nnz, n, out.data_ptr(), self._stream())
+        return out[:n]
 
     def col_counts(self) -> np.ndarray:
         """Entries per column of the uploaded original matrix (device

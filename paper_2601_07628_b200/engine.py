@@ -31,7 +31,8 @@ import numpy as np
 import torch
 
 from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, BandSetup, DeviceCsr, DeviceSetup, inverse_order,
-                     length_order, permute_csr, permute_matrix, slice_blocks, transpose)
+                     inverse_order_device, length_order, length_order_device, permute_csr, permute_matrix,
+                     slice_blocks, transpose, upload)
 from . import native
 from .comm import Ledger, asc_sum
 from .ops import Fused, Parts
@@ -231,7 +232,7 @@ class PdhgEngine:
         for j in self.local_cols:
             c0, c1 = lay.col_range(j)
             n = c1 - c0
-            t = lambda a: torch.as_tensor(np.ascontiguousarray(self._to_internal_col(j, a[c0:c1])), **f64)  # noqa: E731
+            t = lambda a: self._to_internal_col(j, a[c0:c1])  # noqa: E731
             if banded:
                 cj, lj, hj, _ = problem.bands.col_data(c0, c1)
                 t = lambda a: a  # noqa: E731
@@ -243,7 +244,7 @@ class PdhgEngine:
         for i in self.local_rows:
             r0, r1 = lay.row_range(i)
             m = r1 - r0
-            t = lambda a: torch.as_tensor(np.ascontiguousarray(self._to_internal_row(i, a[r0:r1])), **f64)  # noqa: E731
+            t = lambda a: self._to_internal_row(i, a[r0:r1])  # noqa: E731
             if banded:
                 li, hi_, _ = problem.bands.row_data(r0, r1)
                 t = lambda a: a  # noqa: E731
@@ -266,7 +267,8 @@ class PdhgEngine:
                     # internal order: A_ij rows by sigma_i, columns by tau_j (and the
                     # transpose's the other way round); the transpose is taken first
                     # so its entries stay in layout row order (row sums unchanged)
-                    d32 = lambda o: torch.from_numpy(o.astype(np.int32)).to(dev)  # noqa: E731
+                    d32 = lambda o: o.to(torch.int32) if isinstance(o, torch.Tensor) else torch.from_numpy(  # noqa: E731
+                        o.astype(np.int32)).to(dev)
                     a = setup.permute(a, d32(self.row_order[i]), d32(self.col_inv[j]))
                     at = setup.permute(at, d32(self.col_order[j]), d32(self.row_inv[i]))
                 torch.cuda.synchronize(dev)
@@ -288,8 +290,9 @@ class PdhgEngine:
                 hb = host_blocks[(i, j)]
                 ht = transpose(hb)
                 if self.sorted:
-                    hb = permute_csr(hb, self.row_order[i], self.col_inv[j])
-                    ht = permute_csr(ht, self.col_order[j], self.row_inv[i])
+                    ho = self._host_order
+                    hb = permute_csr(hb, ho(self.row_order[i]), ho(self.col_inv[j]))
+                    ht = permute_csr(ht, ho(self.col_order[j]), ho(self.row_inv[i]))
                 self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(ht, dev, **kw))
         if on_device:
             t0 = time.perf_counter()
@@ -316,49 +319,75 @@ class PdhgEngine:
     # ------------------------------------------------- internal order
     def _internal_orders(self, problem, enabled: bool, setup=None):
         """Per grid row band i, sigma_i = the band's rows by full row length
-        (longest first, stable); per grid column band j, tau_j = the band's
-        columns by column count. Blocks and vectors live in this order on the
-        device, so every SELL-32 slice holds rows of nearly equal length;
-        entry order inside a row is untouched, so products stay bit-identical
-        and iterates are the reference's up to the permutation. Computed
-        from the host problem, identically on every rank."""
+        (length classes, longest first, stable); per grid column band j,
+        tau_j = the band's columns by column count. Blocks and vectors live
+        in this order on the device, so every SELL-32 slice holds rows of
+        nearly equal length; entry order inside a row is untouched, so
+        products stay bit-identical and iterates are the reference's up to
+        the permutation. With the device setup the orders are computed and
+        kept on the device (row lengths from the uploaded row pointers, column
+        counts by histogram); every rank computes the same orders from the
+        same problem."""
         self.sorted = bool(enabled)
         self.row_order, self.row_inv, self.col_order, self.col_inv = {}, {}, {}, {}
         if not self.sorted:
             return
         lay = self.layout
-        A = problem.matrix
-        row_len = np.diff(np.asarray(A.row_offsets, np.int64))[lay.perm.row_perm]
-        counts = setup.col_counts() if setup is not None else np.bincount(A.col_indices, minlength=int(A.num_cols))
-        col_len = counts[lay.perm.col_perm]
+        if setup is not None:
+            dev = self.device
+            m, n = lay.num_rows, lay.num_cols
+            row_len = (setup.src_ptr[1:] - setup.src_ptr[:-1])[setup.row_perm[:m]]
+            col_len = setup.col_counts_device()[upload(lay.perm.col_perm, np.int64, dev)] if n else row_len[:0]
+            order, inverse = length_order_device, inverse_order_device
+        else:
+            A = problem.matrix
+            row_len = np.diff(np.asarray(A.row_offsets, np.int64))[lay.perm.row_perm]
+            col_len = np.bincount(A.col_indices, minlength=int(A.num_cols))[lay.perm.col_perm]
+            order, inverse = length_order, inverse_order
         for i in range(self.R):
             r0, r1 = lay.row_range(i)
-            self.row_order[i] = length_order(row_len[r0:r1])
-            self.row_inv[i] = inverse_order(self.row_order[i])
+            self.row_order[i] = order(row_len[r0:r1])
+            self.row_inv[i] = inverse(self.row_order[i])
         for j in range(self.C):
             c0, c1 = lay.col_range(j)
-            self.col_order[j] = length_order(col_len[c0:c1])
-            self.col_inv[j] = inverse_order(self.col_order[j])
+            self.col_order[j] = order(col_len[c0:c1])
+            self.col_inv[j] = inverse(self.col_order[j])
 
-    def _to_internal_col(self, j, a):
-        return a[self.col_order[j]] if self.sorted else a
+    def _vec(self, a) -> torch.Tensor:
+        """Host band slice -> FP64 device tensor (pinned staging on CUDA)."""
+        if self.device.type == "cuda":
+            return upload(a, np.float64, self.device)
+        return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.device)
 
-    def _to_internal_row(self, i, a):
-        return a[self.row_order[i]] if self.sorted else a
+    @staticmethod
+    def _take(v: torch.Tensor, order) -> torch.Tensor:
+        idx = order if isinstance(order, torch.Tensor) else torch.as_tensor(order, device=v.device)
+        return v[idx]
 
-    def _from_internal_col(self, j, a):
-        if not self.sorted:
-            return a
-        out = np.empty_like(a)
-        out[self.col_order[j]] = a
-        return out
+    @staticmethod
+    def _place(v: torch.Tensor, order) -> np.ndarray:
+        idx = order if isinstance(order, torch.Tensor) else torch.as_tensor(order, device=v.device)
+        out = torch.empty_like(v)
+        out[idx] = v
+        return out.cpu().numpy()
 
-    def _from_internal_row(self, i, a):
-        if not self.sorted:
-            return a
-        out = np.empty_like(a)
-        out[self.row_order[i]] = a
-        return out
+    def _to_internal_col(self, j, a) -> torch.Tensor:
+        v = self._vec(a)
+        return self._take(v, self.col_order[j]) if self.sorted else v
+
+    def _to_internal_row(self, i, a) -> torch.Tensor:
+        v = self._vec(a)
+        return self._take(v, self.row_order[i]) if self.sorted else v
+
+    def _from_internal_col(self, j, v: torch.Tensor) -> np.ndarray:
+        return self._place(v, self.col_order[j]) if self.sorted else v.cpu().numpy()
+
+    def _from_internal_row(self, i, v: torch.Tensor) -> np.ndarray:
+        return self._place(v, self.row_order[i]) if self.sorted else v.cpu().numpy()
+
+    @staticmethod
+    def _host_order(o) -> np.ndarray:
+        return o.cpu().numpy() if isinstance(o, torch.Tensor) else o
 
     def _assign_slots(self):
         s = {}
@@ -485,8 +514,7 @@ class PdhgEngine:
                 native.load().call("gridlp_gen_uniform", probe_seed, 31, c0, c1 - c0, -1.0, 1.0, col.v.data_ptr(),
                                    torch.cuda.current_stream(self.device).cuda_stream)
                 continue
-            col.v.copy_(torch.as_tensor(np.ascontiguousarray(
-                self._to_internal_col(j, np.asarray(probe[c0:c1], dtype=np.float64)))))
+            col.v.copy_(self._to_internal_col(j, np.asarray(probe[c0:c1], dtype=np.float64)))
         est = 0.0
         for _ in range(iters):
             for i, row in self.rows.items():
@@ -654,8 +682,8 @@ class PdhgEngine:
         return self._g_sum(tab, 0, self.R), self._g_sum(tab, 1, self.C)
 
     def _snapshot_xy(self):
-        xs = {j: self._from_internal_col(j, c.x.detach().cpu().numpy().copy()) for j, c in self.cols.items()}
-        ys = {i: self._from_internal_row(i, r.y.detach().cpu().numpy().copy()) for i, r in self.rows.items()}
+        xs = {j: self._from_internal_col(j, c.x.detach()).copy() for j, c in self.cols.items()}
+        ys = {i: self._from_internal_row(i, r.y.detach()).copy() for i, r in self.rows.items()}
         return xs, ys
 
     # The loop of iterate_epoch (pdhg_engine.py:364-476), split so a caller
@@ -775,8 +803,8 @@ class PdhgEngine:
         """x blocks of grid columns (from devices (0, j)) and y blocks of grid
         rows (from (i, 0)) as host arrays (solver_driver.py:246-248)."""
         if self.comm.kind == "virtual":
-            xs = [self._from_internal_col(j, self.cols[j].x.cpu().numpy()) for j in range(self.C)]
-            ys = [self._from_internal_row(i, self.rows[i].y.cpu().numpy()) for i in range(self.R)]
+            xs = [self._from_internal_col(j, self.cols[j].x) for j in range(self.C)]
+            ys = [self._from_internal_row(i, self.rows[i].y) for i in range(self.R)]
             return xs, ys
         lay = self.layout
         lengths = {(i, j): max(int(lay.col_cuts[j + 1] - lay.col_cuts[j]), int(lay.row_cuts[i + 1] - lay.row_cuts[i]))
@@ -788,6 +816,6 @@ class PdhgEngine:
         del lengths
         xa = self.comm.gather_vectors(xl, xlen, self.device)
         ya = self.comm.gather_vectors(yl, ylen, self.device)
-        xs = [self._from_internal_col(j, xa[(0, j)].cpu().numpy()) for j in range(self.C)]
-        ys = [self._from_internal_row(i, ya[(i, 0)].cpu().numpy()) for i in range(self.R)]
+        xs = [self._from_internal_col(j, xa[(0, j)]) for j in range(self.C)]
+        ys = [self._from_internal_row(i, ya[(i, 0)]) for i in range(self.R)]
         return xs, ys
