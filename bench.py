@@ -376,6 +376,8 @@ def run_ours(args, rank, world, local_rank):
         over["light_row_max"] = args.light_row_max
     if args.no_graphs:
         over["use_graphs"] = False
+    if args.graph_nccl:
+        over["graph_nccl"] = True
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
     log(f"[bench] rank {rank}: setup {time.perf_counter() - t0:.1f}s {tim}")
     R, C = layout.topology.rows, layout.topology.cols
@@ -507,6 +509,7 @@ def main():
     ap.add_argument("--no-spmv", action="store_true", help="skip the SpMV-only comparison with cuSPARSE")
     ap.add_argument("--light-row-max", type=int, default=None, help="EngineOptions.light_row_max override")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches (the NCCL executor's path)")
+    ap.add_argument("--graph-nccl", action="store_true", help="capture NCCL iterations in CUDA graphs (opt-in)")
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")
     ap.add_argument("--partitioning", default=None, help="SolverConfig.partitioning override")

@@ -73,6 +73,10 @@ class EngineOptions:
     sorted_order: bool = True    # internal length-sorted row/column order per band (CUDA only)
     device_setup: bool = True
     use_graphs: bool = True
+    # capture the NCCL executor's iterations (kernels + NCCL allreduces) in a
+    # CUDA graph too; opt-in until it has run on a multi-GPU box (this round
+    # had one GPU): the eager path is the default there
+    graph_nccl: bool = False
     graph_chunk: int = 128
 
 
@@ -564,7 +568,9 @@ class PdhgEngine:
         ops.step_advance(count)
 
     def _graphable(self) -> bool:
-        return self.opts.use_graphs and self.comm.kind == "virtual" and self.device.type == "cuda"
+        if not (self.opts.use_graphs and self.device.type == "cuda"):
+            return False
+        return self.comm.kind == "virtual" or (self.comm.kind == "nccl" and self.opts.graph_nccl)
 
     def _run_iterations(self, count: int):
         if count <= 0:

@@ -52,3 +52,20 @@ def test_nccl_world1_matches_virtual_grid_bitwise(nccl_world1):
     np.testing.assert_array_equal(a.y, b.y)
     assert a.report == b.report
     assert a.counters == b.counters
+
+
+def test_nccl_graph_capture_option_matches(nccl_world1):
+    """EngineOptions.graph_nccl captures the NCCL executor's iterations in a
+    CUDA graph (collectives included); on a world of one it must reproduce
+    the eager NCCL path bit for bit."""
+    from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate
+    from paper_2601_07628_b200.api import _solve
+
+    p = generate(GeneratorSpec(kind="uniform_random", num_rows=400, num_cols=700, nnz_target=5000,
+                               inequality_fraction=0.3, seed=5))
+    cfg = SolverConfig(tolerance=1e-6, seed=5, comm_backend="nccl")
+    a = _solve(p, cfg, engine_overrides={"graph_nccl": True})
+    b = _solve(p, cfg)
+    assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
