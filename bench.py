@@ -355,7 +355,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     p = make_problem(args.config)
-    if world > 1:
+    if world > 1 or args.force_nccl:
         g = select_grid(p.num_constraints, p.num_variables, world)
         base = dict(n_procs=world, grid=(g.rows, g.cols), comm_backend="nccl")
     elif args.grid:
@@ -513,6 +513,8 @@ def main():
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")
     ap.add_argument("--partitioning", default=None, help="SolverConfig.partitioning override")
+    ap.add_argument("--force-nccl", action="store_true",
+                    help="run the NCCL executor even at world size 1 (exercises the multi-GPU path on one GPU)")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)
     ap.add_argument("--ref-sample-iters", type=int, default=4)
     args = ap.parse_args()
@@ -525,16 +527,21 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    distributed = world > 1 or args.force_nccl
+    if distributed:
         import torch
         import torch.distributed as dist
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if distributed:
             import torch.distributed as dist
 
             dist.destroy_process_group()
