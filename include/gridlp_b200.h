@@ -209,6 +209,16 @@ int gridlp_op_dual(const gridlp_src_t* src, const gridlp_dual_t* dv,
                    const gridlp_step_t* d_step, int32_t iter, uint32_t flags,
                    void* stream);
 
+/* n_iters PDHG iterations of a block whose axes are not split (R = C = 1,
+ * or the single block of a 1x1 grid): per iteration the primal half over
+ * primal_src (= Aᵀ y) then the dual half over dual_src (= A x̄), Halpern
+ * counter inner_k + t, then inner_k += n_iters on the device. The loop body
+ * of iterate_epoch (pdhg_engine.py:394-400; solver_driver.py:376-383); the
+ * engine captures the same sequence in a CUDA graph. */
+int gridlp_pdhg_iterate(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
+                        const gridlp_src_t* dual_src, const gridlp_dual_t* dv, gridlp_step_t* d_step,
+                        int32_t n_iters, uint32_t flags, void* stream);
+
 /* --- KKT pass (pdhg_engine.py:310-346; solver_driver.py:335-358) -------- */
 /* Constraint side, sums = [A x]_i. Writes ax (may be NULL) and reduces
  *   out[0] = ||range_violation(ax)||^2            pdhg_engine.py:206-208, :320-321

@@ -920,4 +920,20 @@ int gridlp_op_step_advance(gridlp_step_t* d_step, int64_t delta, void* stream) {
   return check_launch("op_step_advance");
 }
 
+int gridlp_pdhg_iterate(const gridlp_src_t* primal_src, const gridlp_primal_t* pv, const gridlp_src_t* dual_src,
+                        const gridlp_dual_t* dv, gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,
+                        void* stream) {
+  if (!primal_src || !dual_src || !pv || !dv || !d_step || n_iters < 0)
+    return fail(GRIDLP_ERR_ARG, "pdhg_iterate: bad argument");
+  if (!primal_src->A || !dual_src->A)
+    return fail(GRIDLP_ERR_ARG, "pdhg_iterate: needs fused sources (single-block axes)");
+  for (int32_t t = 0; t < n_iters; ++t) {
+    int rc = gridlp_op_primal(primal_src, pv, d_step, t, flags, stream);
+    if (rc) return rc;
+    rc = gridlp_op_dual(dual_src, dv, d_step, t, flags, stream);
+    if (rc) return rc;
+  }
+  return n_iters > 0 ? gridlp_op_step_advance(d_step, n_iters, stream) : GRIDLP_OK;
+}
+
 }  // extern "C"

@@ -560,6 +560,12 @@ class PdhgEngine:
     # -------------------------------------------------------- main loop
     def _launch_iterations(self, count: int):
         ops, h = self.ops, self.opts.halpern
+        if self.R == 1 and self.C == 1 and hasattr(ops, "iterate") and count > 0:
+            # one block, fused sources: the whole chunk in one C-ABI call
+            (j, col), = self.cols.items()
+            (i, row), = self.rows.items()
+            ops.iterate(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h)
+            return
         for t in range(count):
             for j, col in self.cols.items():
                 ops.primal(self._run_plan(self.plan_primal[j]), col, t, h)

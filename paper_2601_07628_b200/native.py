@@ -89,6 +89,8 @@ SIGNATURES = {
     "gridlp_op_div": ([_P, _P, c_int64, c_double, _P], c_int),
     "gridlp_op_init_primal": ([POINTER(Primal), _P], c_int),
     "gridlp_op_step_advance": ([_P, c_int64, _P], c_int),
+    "gridlp_pdhg_iterate": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32, c_uint32, _P],
+                            c_int),
     "gridlp_setup_workspace_bytes": ([c_int64, c_int64], ctypes.c_size_t),
     "gridlp_block_count": ([_P, _P, _P, c_int64, _P, c_int32, c_int32, _P, _P, ctypes.c_size_t, _P], c_int),
     "gridlp_block_fill": ([_P, _P, _P, _P, c_int64, _P, c_int32, c_int32, _P, c_int64, _P, _P, _P,

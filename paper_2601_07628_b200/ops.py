@@ -164,6 +164,14 @@ class CudaOps:
         self.launches += 1
         self.lib.call("gridlp_op_init_primal", self.primal_struct(col), self.stream())
 
+    def iterate(self, psrc, col, dsrc, row, count: int, halpern: bool):
+        """count fused iterations of a single-block grid in one C call
+        (gridlp_pdhg_iterate), step counter advanced on the device."""
+        self.launches += count * (2 + _heavy(psrc) + _heavy(dsrc)) + (1 if count else 0)
+        self.lib.call("gridlp_pdhg_iterate", self.src(psrc), self.primal_struct(col), self.src(dsrc),
+                      self.dual_struct(row), self.step.data_ptr(), int(count), native.F_HALPERN if halpern else 0,
+                      self.stream())
+
     def step_advance(self, delta: int):
         self.launches += 1
         self.lib.call("gridlp_op_step_advance", self.step.data_ptr(), int(delta), self.stream())

@@ -310,3 +310,29 @@ class TestSolves:
                 assert abs(r.objective - want) <= 1e-6 * max(1.0, abs(want)), m["id"]
                 xr = z[f"S{m['id']}_x"]
                 assert np.max(np.abs(r.x - xr), initial=0.0) <= 1e-6 * max(1.0, np.max(np.abs(xr), initial=0.0))
+
+
+def test_pdhg_iterate_equals_op_by_op(golden_cfg1):
+    """gridlp_pdhg_iterate (one C call for a chunk of iterations) launches
+    the same primal/dual ops as the op-by-op loop: identical iterates and
+    Halpern counter."""
+    from paper_2601_07628_b200.api import prepare
+
+    p = golden_problem(golden_cfg1)
+    states = []
+    for fused in (True, False):
+        eng, _, eta, omega, _ = prepare(p, SolverConfig(seed=0), engine_overrides={"use_graphs": False})
+        eng.start(eta, omega)
+        eng.ops.set_step(eta / omega, eta * omega, 0.0, 0)
+        (j, col), = eng.cols.items()
+        (i, row), = eng.rows.items()
+        if fused:
+            eng.ops.iterate(eng.plan_primal[j][2], col, eng.plan_dual[i][2], row, 37, True)
+        else:
+            for t in range(37):
+                eng.ops.primal(eng.plan_primal[j][2], col, t, True)
+                eng.ops.dual(eng.plan_dual[i][2], row, t, True)
+            eng.ops.step_advance(37)
+        states.append((col.x.cpu().numpy(), row.y.cpu().numpy(), eng.ops.step.cpu().numpy()))
+    for a, b in zip(*states):
+        np.testing.assert_array_equal(a, b)
