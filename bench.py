@@ -518,6 +518,8 @@ def main():
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")
     ap.add_argument("--partitioning", default=None, help="SolverConfig.partitioning override")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gloo lets several ranks share one GPU (orchestration check; timings are not NVLink)")
     ap.add_argument("--force-nccl", action="store_true",
                     help="run the NCCL executor even at world size 1 (exercises the multi-GPU path on one GPU)")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)
@@ -529,6 +531,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":
+        # orchestration check on fewer GPUs than ranks: ranks share devices
+        import torch
+
+        local_rank %= max(torch.cuda.device_count(), 1)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -542,7 +549,10 @@ def main():
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

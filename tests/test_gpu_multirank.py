@@ -1,0 +1,85 @@
+"""The multi-rank executor (comm_backend="nccl": one grid block per process)
+with the REAL device path, on the round's single GPU.
+
+NCCL refuses two ranks on one GPU, but torch.distributed's gloo backend runs
+all_reduce / all_gather on CUDA tensors, so four processes sharing cuda:0
+exercise everything the 8-GPU run does except NCCL itself: per-rank blocks
+built on the device, partial products and the fused epilogues from the
+sm_100a library, axis collectives on device vectors, the once-per-pass
+scalar table and the final x / y gather. With two ranks per reduction group
+an allreduce is one IEEE addition, so a 2x2 grid must reproduce the
+single-process virtual grid bit for bit; wider groups match to FP64
+rounding."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, grid, q):
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, solve
+
+        p = generate(GeneratorSpec(kind="uniform_random", num_rows=700, num_cols=1100, nnz_target=9000,
+                                   inequality_fraction=0.3, seed=6))
+        r = solve(p, SolverConfig(tolerance=1e-6, seed=6, n_procs=world, grid=grid, comm_backend="nccl"))
+        q.put((rank, r.status, r.iterations, r.restarts, r.x, r.y, r.report.as_dict(), r.counters, r.layout))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(grid):
+    import torch.multiprocessing as mp
+
+    world = grid[0] * grid[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, grid, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return sorted(out, key=lambda t: t[0])
+
+
+@pytest.mark.parametrize("grid,bitwise", [((2, 2), True), ((1, 4), False), ((3, 1), False)])
+def test_multirank_device_path_matches_virtual_grid(grid, bitwise):
+    from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, solve
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    p = generate(GeneratorSpec(kind="uniform_random", num_rows=700, num_cols=1100, nnz_target=9000,
+                               inequality_fraction=0.3, seed=6))
+    want = solve(p, SolverConfig(tolerance=1e-6, seed=6, n_procs=grid[0] * grid[1], grid=grid))
+    res = _run(grid)
+    for rank, status, iters, restarts, x, y, kkt, counters, layout in res:
+        assert (status, iters, restarts) == (want.status, want.iterations, want.restarts), rank
+        assert layout == want.layout
+        if bitwise:
+            np.testing.assert_array_equal(x, want.x)
+            np.testing.assert_array_equal(y, want.y)
+            assert kkt == want.report.as_dict()
+            assert counters == want.counters
+        else:
+            np.testing.assert_allclose(x, want.x, rtol=1e-9, atol=1e-9)
+            np.testing.assert_allclose(y, want.y, rtol=1e-9, atol=1e-9)
+        # every rank returns the same solution (replicated, never broadcast)
+        np.testing.assert_array_equal(x, res[0][4])
+        np.testing.assert_array_equal(y, res[0][5])
