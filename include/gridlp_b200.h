@@ -113,11 +113,38 @@ typedef struct gridlp_csr {
 } gridlp_csr_t;
 
 /*
+ * Peer-memory exchange of one grid axis group (G ranks: a grid row for the
+ * C axis, a grid column for the R axis) — the fused replacement of
+ * "partial product -> allreduce -> epilogue" (comm.py:322-329). Every rank
+ * owns a receive buffer of 2 x G slots of `len` doubles and an arrival
+ * counter, mapped into all group members (CUDA IPC; NVLink P2P across
+ * GPUs). The product kernel writes its partial row sums straight into slot
+ * my_slot of every member's buffer (parity = *epoch & 1) and its last CTA
+ * signals every member's counter; the consuming epilogue waits until its
+ * counter reaches (*epoch + 1) * G, adds the G slots in ascending order —
+ * the reference's reduction order, for any G — and the exchange ends with
+ * *epoch += 1. Two parities suffice: a rank cannot produce exchange e + 2
+ * before every member has produced e + 1, i.e. has consumed e.
+ */
+typedef struct gridlp_peer {
+  double* dst[GRIDLP_MAX_PARTS];     /* receive buffer base of each member */
+  uint32_t* flag[GRIDLP_MAX_PARTS];  /* arrival counter of each member */
+  double* recv;                      /* this rank's own receive buffer */
+  uint32_t* my_flag;                 /* this rank's own arrival counter */
+  uint32_t* epoch;                   /* exchanges completed on this axis (device) */
+  uint32_t* cta_count;               /* CTAs of the current product done (device scratch, zero) */
+  int32_t group_size;
+  int32_t my_slot;
+  int64_t len;
+} gridlp_peer_t;
+
+/*
  * Source of the per-row sums an op consumes: either a product with a
  * matrix block (A != NULL: sum_r = (A · gather)_r), or an ascending-order
  * sum of partial vectors (A == NULL: sum_r = ((parts[0]_r + parts[1]_r) +
  * ...), the reduction order of the reference communicator, comm.py:75-84;
- * nparts == 1 after an NCCL allreduce; nparts == 0 means all-zero sums).
+ * nparts == 1 after an NCCL allreduce; nparts == 0 means all-zero sums), or
+ * (peer != NULL, A == NULL) the G slots of a peer exchange, in slot order.
  */
 typedef struct gridlp_src {
   const gridlp_csr_t* A;
@@ -126,6 +153,7 @@ typedef struct gridlp_src {
   int32_t nparts;
   int32_t reserved;
   int64_t num_rows;         /* rows when A == NULL */
+  const gridlp_peer_t* peer;
 } gridlp_src_t;
 
 /* Step parameters, DEVICE-resident so captured graphs pick up updates.
@@ -188,6 +216,13 @@ int64_t gridlp_op_slots(const gridlp_src_t* src);
  * iteration's u_sq / s_sq, sparse_kernels.py:83, :89). */
 int gridlp_op_store(const gridlp_src_t* src, double* out, uint32_t flags,
                     const gridlp_red_t* red, void* stream);
+
+/* Product half of a peer exchange: rows of src->A · src->gather written to
+ * slot peer->my_slot (current parity) of every group member's receive
+ * buffer (and to local_out when not NULL: the block-local partial the
+ * fixed-point cross term needs, pdhg_engine.py:257, :426); the product's
+ * last CTA signals every member. */
+int gridlp_op_store_peer(const gridlp_src_t* src, const gridlp_peer_t* peer, double* local_out, void* stream);
 
 /* --- PDHG iteration halves ------------------------------------------------ */
 /* Primal half over grid column j, rows = variables, sums = [Aᵀ y]_j:

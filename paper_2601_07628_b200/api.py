@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import engine as eng
-from .comm import Ledger, NcclGrid, VirtualGrid
+from .comm import Ledger, NcclGrid, PeerGrid, VirtualGrid
 from .layout import GridTopology, build_layout, layout_summary, unpermute_solution
 from .ops import CudaOps
 from .problem import reported_objective
@@ -33,7 +33,7 @@ from .scaling import MODES as SCALING_MODES
 from .scaling import scale_problem
 
 STEP_SIZE_SAFETY = 0.998
-BACKENDS = ("cuda", "cooperative", "threads", "nccl")
+BACKENDS = ("cuda", "cooperative", "threads", "nccl", "peer")
 
 STATUS_OPTIMAL = eng.OPTIMAL
 STATUS_ITERATION_LIMIT = eng.ITERATION_LIMIT
@@ -244,10 +244,11 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
     R, C = layout.topology.rows, layout.topology.cols
     if device is None:
         device = _device()
-    if cfg.comm_backend == "nccl" and not force_1x1:
-        comm = NcclGrid(R, C, device)
+    if cfg.comm_backend in ("nccl", "peer") and not force_1x1:
+        comm = (PeerGrid if cfg.comm_backend == "peer" else NcclGrid)(R, C, device)
         if comm.world != R * C:
-            raise ValueError(f"nccl backend needs world size == grid devices ({R * C}), got {comm.world}")
+            raise ValueError(f"{cfg.comm_backend} backend needs world size == grid devices ({R * C}), "
+                             f"got {comm.world}")
     else:
         comm = VirtualGrid(R, C)
     cnorm, bnorm, const = problem_scalars(problem) if not banded else (0.0, 0.0, 0.0)

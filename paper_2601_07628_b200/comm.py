@@ -170,3 +170,71 @@ class NcclGrid:
 
     def barrier(self):
         self.dist.barrier()
+
+
+class PeerAxis:
+    """One rank's side of a peer exchange on one axis: its receive buffer
+    (2 parities x G slots x len doubles), arrival counter, epoch and CTA
+    scratch, plus the IPC mappings of every group member's buffer and
+    counter, packed as the C struct gridlp_peer_t."""
+
+    def __init__(self, dist, group, members: list, my_slot: int, length: int, device):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        from . import native
+
+        G = len(members)
+        self.recv = torch.zeros(max(2 * G * length, 1), dtype=torch.float64, device=device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
+        self.cta_count = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        mine = (reduce_tensor(self.recv), reduce_tensor(self.flag))
+        got = [None] * G
+        dist.all_gather_object(got, mine, group=group)
+        self._mapped = []                      # keep the imported tensors (and their IPC mappings) alive
+        c = native.Peer()
+        for q, ((fr, fa), (gr, ga)) in enumerate(got):
+            if q == my_slot:
+                rt, ft = self.recv, self.flag
+            else:
+                rt, ft = fr(*fa), gr(*ga)
+                self._mapped += [rt, ft]
+            c.dst[q] = rt.data_ptr()
+            c.flag[q] = ft.data_ptr()
+        c.recv, c.my_flag = self.recv.data_ptr(), self.flag.data_ptr()
+        c.epoch, c.cta_count = self.epoch.data_ptr(), self.cta_count.data_ptr()
+        c.group_size, c.my_slot, c.len = G, my_slot, length
+        self.struct = c
+        self.length = length
+
+
+class PeerGrid(NcclGrid):
+    """NcclGrid's process layout with in-kernel peer-memory exchanges for
+    the vector sums (torch.distributed only moves the IPC handles at setup
+    and the once-per-pass scalar table)."""
+
+    kind = "peer"
+
+    def __init__(self, rows: int, cols: int, device):
+        super().__init__(rows, cols, device)
+        self.axes = {}
+
+    def setup_axes(self, row_len: int, col_len: int):
+        """Create the C-axis (grid row, vectors of m_i) and R-axis (grid
+        column, vectors of n_j) exchanges of this rank; every rank calls it
+        in the same order."""
+        if not self.active:
+            return
+        i, j = self.coord
+        for ii in range(self.rows):
+            members = [ii * self.cols + jj for jj in range(self.cols)]
+            if ii == i:
+                self.axes["C"] = PeerAxis(self.dist, self.row_groups[ii], members, j, row_len, self.device)
+        for jj in range(self.cols):
+            members = [ii * self.cols + jj for ii in range(self.rows)]
+            if jj == j:
+                self.axes["R"] = PeerAxis(self.dist, self.col_groups[jj], members, i, col_len, self.device)
+
+    def reduce(self, axis, index, partials, scratch=None):
+        raise RuntimeError("PeerGrid sums inside the kernels; reduce() is never called")

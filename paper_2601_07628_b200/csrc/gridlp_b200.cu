@@ -31,6 +31,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
+#include <utility>
 
 namespace {
 
@@ -165,6 +167,35 @@ struct OpStore {
   __device__ void row(int64_t r, double s, const Data&, double* acc) const {
     out[r] = s;
     if (SUMSQ) acc[0] = dadd(acc[0], dmul(s, s));
+  }
+};
+
+// Partial row sums written into every group member's receive slot (peer
+// exchange); the product's last CTA fences and signals the members.
+struct OpPeerStore {
+  static constexpr int NRED = 0;
+  gridlp_peer_t pe;
+  double* local;                     // optional local copy of the partial (block-local cross terms)
+  int64_t base;                      // (parity * G + my_slot) * len
+  int32_t total_ctas;
+  using Data = Empty;
+  __device__ void prepare() { base = ((int64_t)(*pe.epoch & 1u) * pe.group_size + pe.my_slot) * pe.len; }
+  __device__ Data load(int64_t) const { return {}; }
+  __device__ void row(int64_t r, double s, const Data&, double*) const {
+    for (int q = 0; q < pe.group_size; ++q) pe.dst[q][base + r] = s;
+    if (local) local[r] = s;
+  }
+  // called by every CTA after its rows are written
+  __device__ void cta_done() const {
+    __threadfence_system();           // every thread's peer stores before the CTA's arrival
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (atomicAdd(pe.cta_count, 1u) == (uint32_t)total_ctas - 1u) {
+        *pe.cta_count = 0u;
+        __threadfence_system();
+        for (int q = 0; q < pe.group_size; ++q) atomicAdd_system(pe.flag[q], 1u);
+      }
+    }
   }
 };
 
@@ -388,6 +419,19 @@ __device__ __forceinline__ void store_partials(double (&acc)[Op::NRED > 0 ? Op::
   }
 }
 
+template <class T, class = void>
+struct HasCtaDone : std::false_type {};
+template <class T>
+struct HasCtaDone<T, std::void_t<decltype(std::declval<const T&>().cta_done())>> : std::true_type {};
+
+template <class Op>
+__device__ __forceinline__ void product_cta_done(const Op& op) {
+  if constexpr (HasCtaDone<Op>::value) op.cta_done();
+}
+
+#ifndef GRIDLP_PEER_WAIT_CYCLES
+#define GRIDLP_PEER_WAIT_CYCLES (60LL * 2000000000LL)   // ~60 s at 2 GHz
+#endif
 constexpr int SELL_WPB = 2;          // warps (slices) per CTA
 constexpr int SELL_NT = SELL_WPB * 32;
 constexpr int SELL_U = 4;            // steps in flight per lane
@@ -487,6 +531,7 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
     }
   }
   cta_partials<Op>(acc, partials);
+  product_cta_done(op);
   pdl_wait();
 }
 
@@ -565,6 +610,7 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
     }
   }
   cta_partials<Op>(acc, partials);
+  product_cta_done(op);
   pdl_wait();
 }
 
@@ -629,18 +675,47 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
     }
   }
   cta_partials<Op>(acc, partials);
+  product_cta_done(op);
   pdl_wait();
 }
 
 // Row-wise epilogue over ascending-order sums of partial vectors.
 template <class Op>
 __global__ void __launch_bounds__(TPB) rows_kernel(gridlp_src_t src, int64_t n, Op op,
-                                                   double* __restrict__ partials) {
+                                                   double* __restrict__ partials, gridlp_peer_t pe) {
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   double acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
   op.prepare();
+  if (src.peer) {
+    // peer exchange (pe = *src.peer, passed by value): wait for the G
+    // members' partials of this exchange, then add the slots in ascending order
+    const uint32_t e = *pe.epoch;
+    if (threadIdx.x == 0) {
+      const uint32_t target = (e + 1u) * (uint32_t)pe.group_size;
+      const long long t0 = clock64();
+      uint32_t v;
+      while (true) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(pe.my_flag) : "memory");
+        if ((int32_t)(v - target) >= 0) break;
+        // a member that never arrives is a bug or a dead peer: fail the launch
+        // (cudaErrorLaunchFailure) instead of hanging the device
+        if (clock64() - t0 > GRIDLP_PEER_WAIT_CYCLES) __trap();
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
+    const double* __restrict__ slots = pe.recv + (int64_t)(e & 1u) * pe.group_size * pe.len;
+    for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+      const typename Op::Data d = op.load(r);
+      double s = __ldcv(slots + r);
+      for (int q = 1; q < pe.group_size; ++q) s = dadd(s, __ldcv(slots + (int64_t)q * pe.len + r));
+      op.row(r, s, d, acc);
+    }
+    store_partials<Op>(acc, partials);
+    return;
+  }
   const int np = src.nparts;
   for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
     const typename Op::Data d = op.load(r);
@@ -652,6 +727,10 @@ __global__ void __launch_bounds__(TPB) rows_kernel(gridlp_src_t src, int64_t n, 
     op.row(r, s, d, acc);
   }
   store_partials<Op>(acc, partials);
+}
+
+__global__ void epoch_advance_kernel(uint32_t* epoch) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *epoch += 1u;
 }
 
 // Fixed-order final reduction of per-CTA slots.
@@ -743,6 +822,12 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
       return fail(GRIDLP_ERR_ARG, std::string(name) + ": missing gather vector");
     slots = sell_blocks(src->A);
   } else {
+    if (src->peer) {
+      const gridlp_peer_t* pe = src->peer;
+      if (pe->group_size < 1 || pe->group_size > GRIDLP_MAX_PARTS || !pe->recv || !pe->my_flag || !pe->epoch ||
+          pe->len != n)
+        return fail(GRIDLP_ERR_ARG, std::string(name) + ": inconsistent peer source");
+    }
     if (src->nparts < 0 || src->nparts > GRIDLP_MAX_PARTS)
       return fail(GRIDLP_ERR_ARG, std::string(name) + ": nparts out of range");
     for (int q = 0; q < src->nparts; ++q)
@@ -780,12 +865,18 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
                         partials ? partials + (M.num_chunks + nlong) * GRIDLP_MAX_RED : nullptr);
       if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
     } else
-      rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials);
+      rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials,
+                                                      src->peer ? *src->peer : gridlp_peer_t{});
     int rc = check_launch(name);
     if (rc) return rc;
   }
   if (Op::NRED > 0) {
     reduce_kernel<<<1, TPB, 0, s>>>(partials, slots, Op::NRED, red->out);
+    int rc = check_launch(name);
+    if (rc) return rc;
+  }
+  if (!src->A && src->peer) {
+    epoch_advance_kernel<<<1, 32, 0, s>>>(src->peer->epoch);
     int rc = check_launch(name);
     if (rc) return rc;
   }
@@ -834,6 +925,25 @@ int gridlp_op_store(const gridlp_src_t* src, double* out, uint32_t flags, const 
   if (!out && src_rows(src) > 0) return fail(GRIDLP_ERR_ARG, "op_store: null output");
   if (flags & GRIDLP_F_SUMSQ) return launch_op(src, OpStore<true>{out}, red, stream, "op_store");
   return launch_op(src, OpStore<false>{out}, red, stream, "op_store");
+}
+
+int gridlp_op_store_peer(const gridlp_src_t* src, const gridlp_peer_t* peer, double* local_out, void* stream) {
+  if (!src || !src->A || !peer) return fail(GRIDLP_ERR_ARG, "op_store_peer: needs a product source and a peer");
+  if (peer->group_size < 1 || peer->group_size > GRIDLP_MAX_PARTS || peer->my_slot < 0 ||
+      peer->my_slot >= peer->group_size || peer->len != src->A->num_rows || !peer->epoch || !peer->cta_count)
+    return fail(GRIDLP_ERR_ARG, "op_store_peer: inconsistent peer description");
+  for (int q = 0; q < peer->group_size; ++q)
+    if (!peer->dst[q] || !peer->flag[q]) return fail(GRIDLP_ERR_ARG, "op_store_peer: null member buffer");
+  OpPeerStore op{};
+  op.pe = *peer;
+  op.local = local_out;
+  op.total_ctas = (int32_t)sell_blocks(src->A);
+  if (op.total_ctas == 0) {
+    // no CTA would signal: signal from a one-thread kernel instead
+    // (an empty block still takes part in the exchange)
+    return fail(GRIDLP_ERR_ARG, "op_store_peer: empty block (no rows)");
+  }
+  return launch_op(src, op, nullptr, stream, "op_store_peer");
 }
 
 int gridlp_op_primal(const gridlp_src_t* src, const gridlp_primal_t* pv, const gridlp_step_t* d_step,

@@ -35,7 +35,7 @@ from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, BandSetup, De
                      slice_blocks, transpose, upload)
 from . import native
 from .comm import Ledger, asc_sum
-from .ops import Fused, Parts
+from .ops import Fused, Parts, PeerDest, PeerSrc
 
 log = logging.getLogger("gridlp.solver")
 
@@ -186,6 +186,9 @@ class PdhgEngine:
         self.timings = {}
         t0 = time.perf_counter()
         self._build(problem)
+        if comm.kind == "peer":
+            (i0, j0), = comm.local
+            comm.setup_axes(self.rows[i0].m, self.cols[j0].n)
         self.timings["setup_blocks_s"] = time.perf_counter() - t0
         cap = max([b.A.slots() for b in self.blocks.values()]
                   + [b.AT.slots() for b in self.blocks.values()] + [1184])
@@ -424,6 +427,13 @@ class PdhgEngine:
         if single:
             (blk, orient, g), = items
             return [], None, Fused(blk.A if orient == "A" else blk.AT, g)
+        if self.comm.kind == "peer":
+            # fused exchange: the product writes into the group's receive slots,
+            # the consumer adds them in slot order (no host collective)
+            (blk, orient, g), = items
+            local = self._buf(blk, f"{scratch_name}_{orient}", length) if keep else None
+            return ([(Fused(blk.A if orient == "A" else blk.AT, g), PeerDest(self.comm.axes[axis], local))], None,
+                    PeerSrc(self.comm.axes[axis], length))
         pre = []
         bufs = []
         for blk, orient, g in items:
@@ -576,7 +586,7 @@ class PdhgEngine:
     def _graphable(self) -> bool:
         if not (self.opts.use_graphs and self.device.type == "cuda"):
             return False
-        return self.comm.kind == "virtual" or (self.comm.kind == "nccl" and self.opts.graph_nccl)
+        return self.comm.kind in ("virtual", "peer") or (self.comm.kind == "nccl" and self.opts.graph_nccl)
 
     def _run_iterations(self, count: int):
         if count <= 0:

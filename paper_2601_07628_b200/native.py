@@ -46,10 +46,16 @@ class Csr(ctypes.Structure):
                 ("light_row_max", c_int32), ("exact_row_max", c_int32)]
 
 
+class Peer(ctypes.Structure):
+    _fields_ = [("dst", c_void_p * MAX_PARTS), ("flag", c_void_p * MAX_PARTS), ("recv", c_void_p),
+                ("my_flag", c_void_p), ("epoch", c_void_p), ("cta_count", c_void_p), ("group_size", c_int32),
+                ("my_slot", c_int32), ("len", c_int64)]
+
+
 class Src(ctypes.Structure):
     _fields_ = [("A", POINTER(Csr)), ("gather", c_void_p),
                 ("parts", c_void_p * MAX_PARTS), ("nparts", c_int32),
-                ("reserved", c_int32), ("num_rows", c_int64)]
+                ("reserved", c_int32), ("num_rows", c_int64), ("peer", POINTER(Peer))]
 
 
 class Step(ctypes.Structure):
@@ -78,6 +84,7 @@ SIGNATURES = {
     "gridlp_device_info": ([c_int, POINTER(c_int32), POINTER(c_int64)], c_int),
     "gridlp_op_slots": ([POINTER(Src)], c_int64),
     "gridlp_op_store": ([POINTER(Src), _P, c_uint32, POINTER(Red), _P], c_int),
+    "gridlp_op_store_peer": ([POINTER(Src), POINTER(Peer), _P, _P], c_int),
     "gridlp_op_primal": ([POINTER(Src), POINTER(Primal), _P, c_int32, c_uint32, _P], c_int),
     "gridlp_op_dual": ([POINTER(Src), POINTER(Dual), _P, c_int32, c_uint32, _P], c_int),
     "gridlp_op_kkt_rows": ([POINTER(Src), POINTER(Dual), _P, POINTER(Red), _P], c_int),

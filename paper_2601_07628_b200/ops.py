@@ -34,6 +34,23 @@ class Parts:
         self.num_rows = int(num_rows)
 
 
+class PeerDest:
+    """Destination of a product in a peer exchange (comm.PeerAxis), with an
+    optional local copy of the partial."""
+
+    def __init__(self, axis, local=None):
+        self.axis = axis
+        self.local = local
+
+
+class PeerSrc:
+    """Sums are the G slots of a peer exchange (comm.PeerAxis), in order."""
+
+    def __init__(self, axis, num_rows: int):
+        self.axis = axis
+        self.num_rows = int(num_rows)
+
+
 def _heavy(src) -> int:
     """Extra kernels a product launches for its long rows (warp-per-row and
     heavy-chunk kernels, when present)."""
@@ -78,6 +95,9 @@ class CudaOps:
             return ctypes.byref(hit[1])
         if isinstance(s, Fused):
             c = s.mat.src(s.gather)
+        elif isinstance(s, PeerSrc):
+            c = parts_src([], s.num_rows)
+            c.peer = ctypes.pointer(s.axis.struct)
         else:
             c = parts_src(s.parts, s.num_rows)
         self._srcs[key] = (s, c)
@@ -113,6 +133,11 @@ class CudaOps:
 
     # -- ops -----------------------------------------------------------------
     def store(self, src, out, slot=None):
+        if isinstance(out, PeerDest):
+            self.launches += 1 + _heavy(src)
+            self.lib.call("gridlp_op_store_peer", self.src(src), ctypes.byref(out.axis.struct), _ptr(out.local),
+                          self.stream())
+            return
         self.launches += (2 if slot is not None else 1) + _heavy(src)
         flags = native.F_SUMSQ if slot is not None else 0
         self.lib.call("gridlp_op_store", self.src(src), _ptr(out), flags,

@@ -27,7 +27,14 @@ def _port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, grid, q):
+CASE = dict(kind="uniform_random", num_rows=700, num_cols=1100, nnz_target=9000, inequality_fraction=0.3, seed=6)
+# peer exchanges between processes that share ONE GPU wait for the driver's
+# time slicing at every exchange, so those cases run a bounded iteration count
+PEER_CASE = dict(kind="uniform_random", num_rows=300, num_cols=400, nnz_target=3000, inequality_fraction=0.3, seed=6)
+PEER_CFG = dict(tolerance=1e-12, seed=6, max_iterations=192)
+
+
+def _worker(rank, world, port, grid, backend, q):
     import torch.distributed as dist
 
     torch.cuda.set_device(0)
@@ -35,22 +42,25 @@ def _worker(rank, world, port, grid, q):
     try:
         from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, solve
 
-        p = generate(GeneratorSpec(kind="uniform_random", num_rows=700, num_cols=1100, nnz_target=9000,
-                                   inequality_fraction=0.3, seed=6))
-        r = solve(p, SolverConfig(tolerance=1e-6, seed=6, n_procs=world, grid=grid, comm_backend="nccl"))
+        if backend == "peer":
+            p, cfg = generate(GeneratorSpec(**PEER_CASE)), dict(PEER_CFG)
+        else:
+            p, cfg = generate(GeneratorSpec(**CASE)), dict(tolerance=1e-6, seed=6)
+        r = solve(p, SolverConfig(**cfg, n_procs=world, grid=grid, comm_backend=backend))
         q.put((rank, r.status, r.iterations, r.restarts, r.x, r.y, r.report.as_dict(), r.counters, r.layout))
+        dist.barrier()          # members keep their IPC-shared buffers alive until everyone is done
     finally:
         dist.destroy_process_group()
 
 
-def _run(grid):
+def _run(grid, backend="nccl"):
     import torch.multiprocessing as mp
 
     world = grid[0] * grid[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, grid, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, grid, backend, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=600) for _ in range(world)]
@@ -65,8 +75,7 @@ def test_multirank_device_path_matches_virtual_grid(grid, bitwise):
     from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, solve
 
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    p = generate(GeneratorSpec(kind="uniform_random", num_rows=700, num_cols=1100, nnz_target=9000,
-                               inequality_fraction=0.3, seed=6))
+    p = generate(GeneratorSpec(**CASE))
     want = solve(p, SolverConfig(tolerance=1e-6, seed=6, n_procs=grid[0] * grid[1], grid=grid))
     res = _run(grid)
     for rank, status, iters, restarts, x, y, kkt, counters, layout in res:
@@ -83,3 +92,23 @@ def test_multirank_device_path_matches_virtual_grid(grid, bitwise):
         # every rank returns the same solution (replicated, never broadcast)
         np.testing.assert_array_equal(x, res[0][4])
         np.testing.assert_array_equal(y, res[0][5])
+
+
+@pytest.mark.parametrize("grid", [(2, 2), (1, 4), (3, 1), (2, 3)])
+def test_peer_exchange_is_bitwise_the_virtual_grid(grid):
+    """comm_backend="peer": products write their partial rows into the group
+    members' receive buffers (CUDA IPC, here between processes sharing the
+    GPU; NVLink P2P across GPUs) and the epilogue adds the slots in ascending
+    order after a device-side arrival counter — so unlike a ring allreduce
+    the result is the virtual grid's (= the reference's) bit for bit for
+    every group size; iterations run inside CUDA graphs."""
+    from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, solve
+
+    p = generate(GeneratorSpec(**PEER_CASE))
+    want = solve(p, SolverConfig(**PEER_CFG, n_procs=grid[0] * grid[1], grid=grid))
+    for rank, status, iters, restarts, x, y, kkt, counters, layout in _run(grid, "peer"):
+        assert (status, iters, restarts) == (want.status, want.iterations, want.restarts), rank
+        np.testing.assert_array_equal(x, want.x)
+        np.testing.assert_array_equal(y, want.y)
+        assert kkt == want.report.as_dict()
+        assert counters == want.counters
