@@ -357,7 +357,7 @@ def run_ours(args, rank, world, local_rank):
     p = make_problem(args.config)
     if world > 1 or args.force_nccl:
         g = select_grid(p.num_constraints, p.num_variables, world)
-        base = dict(n_procs=world, grid=(g.rows, g.cols), comm_backend="nccl")
+        base = dict(n_procs=world, grid=(g.rows, g.cols), comm_backend=args.comm)
     elif args.grid:
         R, C = (int(v) for v in args.grid.lower().split("x"))
         base = dict(n_procs=R * C, grid=(R, C))       # virtual grid: all blocks on this GPU
@@ -520,6 +520,8 @@ def main():
     ap.add_argument("--partitioning", default=None, help="SolverConfig.partitioning override")
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
                     help="gloo lets several ranks share one GPU (orchestration check; timings are not NVLink)")
+    ap.add_argument("--comm", choices=("nccl", "peer"), default="nccl",
+                    help="multi-GPU vector sums: NCCL allreduce (default) or in-kernel peer-memory exchange")
     ap.add_argument("--force-nccl", action="store_true",
                     help="run the NCCL executor even at world size 1 (exercises the multi-GPU path on one GPU)")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)

@@ -205,6 +205,9 @@ int gridlp_abi_version(void);
 const char* gridlp_last_error(void);
 /* SM count and L2 size of `device` (host ints). */
 int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes);
+/* Let kernels on the current device read and write memory of peer_device
+ * (NVLink P2P for the peer exchange); already-enabled is success. */
+int gridlp_enable_peer_access(int peer_device);
 /* Upper bound on the CTAs (reduction slots) an op over `src` launches. */
 int64_t gridlp_op_slots(const gridlp_src_t* src);
 

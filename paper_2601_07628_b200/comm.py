@@ -200,6 +200,8 @@ class PeerAxis:
             else:
                 rt, ft = fr(*fa), gr(*ga)
                 self._mapped += [rt, ft]
+                if rt.device != self.recv.device:       # another GPU: NVLink P2P from this device
+                    native.load().call("gridlp_enable_peer_access", rt.device.index)
             c.dst[q] = rt.data_ptr()
             c.flag[q] = ft.data_ptr()
         c.recv, c.my_flag = self.recv.data_ptr(), self.flag.data_ptr()

@@ -902,6 +902,23 @@ const char* gridlp_last_error(void) { return g_err.c_str(); }
 // not part of the header: lets the setup translation unit share the error slot
 void gridlp_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
 
+int gridlp_enable_peer_access(int peer_device) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("enable_peer_access: ") + cudaGetErrorString(e));
+  if (peer_device == dev) return GRIDLP_OK;
+  int can = 0;
+  e = cudaDeviceCanAccessPeer(&can, dev, peer_device);
+  if (e != cudaSuccess || !can) return fail(GRIDLP_ERR_CUDA, "enable_peer_access: no P2P path between the devices");
+  e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return GRIDLP_OK;
+  }
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("enable_peer_access: ") + cudaGetErrorString(e));
+  return GRIDLP_OK;
+}
+
 int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes) {
   int v = 0;
   cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);

@@ -82,6 +82,7 @@ SIGNATURES = {
     "gridlp_abi_version": ([], c_int),
     "gridlp_last_error": ([], ctypes.c_char_p),
     "gridlp_device_info": ([c_int, POINTER(c_int32), POINTER(c_int64)], c_int),
+    "gridlp_enable_peer_access": ([c_int], c_int),
     "gridlp_op_slots": ([POINTER(Src)], c_int64),
     "gridlp_op_store": ([POINTER(Src), _P, c_uint32, POINTER(Red), _P], c_int),
     "gridlp_op_store_peer": ([POINTER(Src), POINTER(Peer), _P, _P], c_int),
