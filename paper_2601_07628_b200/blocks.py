@@ -137,16 +137,16 @@ def inverse_order(order: np.ndarray) -> np.ndarray:
 
 def build_sell(host: HostCsr, light_row_max: int):
     """SELL-32 layout of include/gridlp_b200.h on the host (the device build,
-    DeviceSetup.sell, must produce the same arrays): per 32-row slice the
-    light rows sorted by length (descending, stable), stored column-major;
-    rows longer than light_row_max as a compact CSR."""
+    DeviceSetup.sell, must produce the same arrays): per 32-row slice, lane l
+    holds row 32 s + l (empty when the row is long), entries stored
+    column-major; rows longer than light_row_max as a compact CSR."""
     ptr, m = host.ptr, host.num_rows
     lens = np.diff(ptr)
     heavy = lens > light_row_max
     ns = -(-m // 32) if m else 0
     eff = np.where(heavy, -1, lens)
     sl = np.arange(m, dtype=np.int64) // 32
-    order = np.lexsort((-eff, sl))             # slice-major, longest first, long rows last
+    order = np.arange(m, dtype=np.int64)       # lane = row & 31
     info = np.full(ns * 32, -1, dtype=np.int64)
     slen = eff[order]
     light = slen >= 0

@@ -615,17 +615,15 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
 }
 
 // Product + fused epilogue over the light rows of a SELL-32 block: each CTA
-// owns SELL_WPB slices; its reduction partials follow the heavy kernel's in
-// the slot array. A slice's warp parks its 32 row sums in shared memory by row, __syncwarp()s
-// and runs the natural-order epilogue of its own 32 rows — no CTA barrier on
-// the light path.
+// owns SELL_WPB slices; its reduction partials follow the heavy and long
+// kernels' in the slot array. Lane l of a slice's warp owns row 32 s + l,
+// sums it in a register and applies the epilogue to it directly — no shared
+// memory and no barrier on the light path.
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t A, const double* __restrict__ g,
                                                                    Op op, double* __restrict__ partials) {
   constexpr int U = SELL_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
-  __shared__ double sums[SELL_WPB][32];
-  __shared__ int have[SELL_WPB][32];
   double acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
@@ -634,44 +632,36 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
-  {
-    const int64_t slice = (int64_t)blockIdx.x * SELL_WPB + warp;
-    if (slice < A.num_slices) {
-      const int64_t r = slice * 32 + lane;
-      const bool in_range = r < A.num_rows;
-      have[warp][lane] = 0;
-      const int info = A.lane_info[slice * 32 + lane];
-      __syncwarp();
-      if (info >= 0) {
-        const int len = info >> 8;
-        const int64_t base = (int64_t)A.slice_off[slice] + lane;
-        const int* __restrict__ cp = A.sell_cols + base;
-        const double* __restrict__ vp = A.sell_vals + base;
-        double s = 0.0;
-        for (int j = 0; j < len; j += U) {
-          int c[U];
-          double v[U], x[U];
+  const int64_t slice = (int64_t)blockIdx.x * SELL_WPB + warp;
+  if (slice < A.num_slices) {
+    // lane = row & 31 (sell_plan): the lane's sum is its own row's
+    const int64_t r = slice * 32 + lane;
+    const int info = A.lane_info[slice * 32 + lane];
+    if (info >= 0) {
+      const int len = info >> 8;
+      const int64_t base = (int64_t)A.slice_off[slice] + lane;
+      const int* __restrict__ cp = A.sell_cols + base;
+      const double* __restrict__ vp = A.sell_vals + base;
+      double s = 0.0;
+      for (int j = 0; j < len; j += U) {
+        int c[U];
+        double v[U], x[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const bool ok = j + u < len;
-            c[u] = ok ? ld_stream(cp + 32 * (j + u), pf) : 0;
-            v[u] = ok ? ld_stream(vp + 32 * (j + u), pf) : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) x[u] = (j + u < len) ? ld_gather(g + c[u], pl) : 0.0;
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
+        for (int u = 0; u < U; ++u) {
+          const bool ok = j + u < len;
+          c[u] = ok ? ld_stream(cp + 32 * (j + u), pf) : 0;
+          v[u] = ok ? ld_stream(vp + 32 * (j + u), pf) : 0.0;
         }
-        sums[warp][info & 31] = s;
-        have[warp][info & 31] = 1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = (j + u < len) ? ld_gather(g + c[u], pl) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
       }
       // epilogue operands are loaded after the sums: issuing them first costs
       // registers (occupancy) and measured slower (profiles/r1, variant 10)
-      typename Op::Data d{};
-      if (in_range) d = op.load(r);
-      __syncwarp();
-      if (in_range && have[warp][lane]) op.row(r, sums[warp][lane], d, acc);
+      const typename Op::Data d = op.load(r);
+      op.row(r, s, d, acc);
     }
   }
   cta_partials<Op>(acc, partials);

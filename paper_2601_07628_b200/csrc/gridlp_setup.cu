@@ -183,8 +183,7 @@ __global__ void permute_fill_kernel(const int32_t* __restrict__ ptr, const int32
   }
 }
 
-// SELL-32 plan: one warp per 32-row window. Lane order inside the slice is
-// the rank of (length descending, row ascending); long rows (length >
+// SELL-32 plan: one warp per 32-row window, lane = row & 31; long rows (length >
 // light_row_max) and rows past the end take the last lanes as empty (-1).
 __global__ void sell_plan_kernel(const int32_t* __restrict__ ptr, int64_t nrows, int32_t light_row_max,
                                  int32_t* __restrict__ lane_info, int32_t* __restrict__ slice_elems,
@@ -201,14 +200,16 @@ __global__ void sell_plan_kernel(const int32_t* __restrict__ ptr, int64_t nrows,
     long_flag[row] = len > light_row_max;
     long_len[row] = len > light_row_max ? len : 0;
   }
-  int rank = 0, mx = eff > 0 ? eff : 0;
-  for (int o = 0; o < 32; ++o) {
-    const int e = __shfl_sync(0xffffffffu, eff, o);
-    rank += (e > eff) || (e == eff && o < lane);
+  // lane = row & 31: the engine's internal length-class order already puts
+  // rows of nearly equal length in a slice, so each lane keeps its own row
+  // and its sum needs no reshuffle before the epilogue
+  int mx = eff > 0 ? eff : 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    const int e = __shfl_xor_sync(0xffffffffu, mx, o);
     mx = e > mx ? e : mx;
   }
-  lane_info[s * 32 + rank] = eff >= 0 ? ((eff << 8) | lane) : -1;
-  if (row < nrows) rank_of[row] = rank;
+  lane_info[s * 32 + lane] = eff >= 0 ? ((eff << 8) | lane) : -1;
+  if (row < nrows) rank_of[row] = lane;
   if (lane == 0) slice_elems[s] = 32 * mx;
 }
 

@@ -104,7 +104,7 @@ def test_long_row_plan():
 
 def test_sell_layout_roundtrip():
     """The SELL-32 layout holds every light row's entries in their original
-    order, lanes sorted by length inside a slice, and every heavy row in the
+    order (lane l of slice s = row 32 s + l), and every long row in the
     compact CSR."""
     from paper_2601_07628_b200.blocks import HostCsr, build_sell
 
@@ -126,6 +126,7 @@ def test_sell_layout_roundtrip():
             if inf < 0:
                 continue
             length, local = inf >> 8, inf & 31
+            assert local == lane
             row = s * 32 + local
             assert length == lens[row] and not seen[row]
             seen[row] = True
