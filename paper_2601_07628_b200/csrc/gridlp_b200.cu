@@ -436,6 +436,9 @@ constexpr int SELL_WPB = 2;          // warps (slices) per CTA
 constexpr int SELL_NT = SELL_WPB * 32;
 constexpr int SELL_U = 4;            // steps in flight per lane
 constexpr int SELL_MINB = 32;        // 64 warps per SM at <= 32 registers
+#ifndef LONG_U
+#define LONG_U 2                     // long-row kernel: 64-entry blocks (registers -> occupancy)
+#endif
 
 // Deterministic per-CTA reduction of a SELL_NT-thread CTA: warp tree, then
 // warps in order, one slot per CTA.
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
                                                            double* __restrict__ partials) {
-  constexpr int U = SELL_U;
+  constexpr int U = LONG_U;
   constexpr int B = 32 * U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   __shared__ double prod[SELL_WPB][B];
