@@ -207,15 +207,17 @@ GATHER_CEILING_PER_S = 255e9
 
 def spmv_compare(problem, device, reps=20) -> dict:
     """SpMV-only HBM GB/s: y = A·x over the instance's own CSR,
-    our SELL-32 product (gridlp_op_store, bit-identical to scipy) against
-    cuSPARSE csrmv through torch.sparse (FP64, int32 indices) on the same
-    matrix and vector; CUDA events on the launching stream, L2 not flushed
-    (A is 240 MB, > L2). Bytes per product: 12 nnz + 4(rows+1) + 8 cols +
-    8 rows."""
+    our product (gridlp_op_store, bit-identical to scipy) against cuSPARSE
+    csrmv through torch.sparse (FP64, int32 indices) on the same matrix and
+    vector; CUDA events on the launching stream, L2 not flushed (A is 240 MB,
+    > L2). Bytes per product: 12 nnz + 4(rows+1) + 8 cols + 8 rows. Ours is
+    timed in both of its layouts: the rows in the user's order ("ours_us")
+    and in the engine's internal length-class order ("ours_sorted_us", the
+    layout every solve uses; y comes out permuted, same values)."""
     import numpy as np
     import torch
 
-    from paper_2601_07628_b200.blocks import DeviceCsr, HostCsr
+    from paper_2601_07628_b200.blocks import DeviceCsr, HostCsr, length_order, permute_csr
     from paper_2601_07628_b200.ops import CudaOps, Fused
 
     M = problem.matrix
@@ -244,16 +246,23 @@ def spmv_compare(problem, device, reps=20) -> dict:
         return sorted(a.elapsed_time(b) for a, b in evs)[reps // 2] * 1e-3
 
     t_ours = timed(lambda: ops.store(Fused(A, x), ours))
+    order = length_order(np.diff(h.ptr))
+    As = DeviceCsr(permute_csr(h, order), device)
+    ours_s = torch.empty(m, dtype=torch.float64, device=device)
+    t_sorted = timed(lambda: ops.store(Fused(As, x), ours_s))
+    same_sorted = bool(torch.equal(ours_s, ours[torch.from_numpy(order).to(device)]))
     lib = {}
     t_lib = timed(lambda: lib.__setitem__("y", torch.mm(T, xs)))
     same = bool(torch.equal(lib["y"].reshape(m), ours))
     bytes_ = 12 * h.nnz + 4 * (m + 1) + 8 * n + 8 * m
     out = {"rows": m, "cols": n, "nnz": h.nnz, "bytes_per_product": bytes_,
            "ours_us": t_ours * 1e6, "ours_GBs": bytes_ / t_ours / 1e9,
+           "ours_sorted_us": t_sorted * 1e6, "ours_sorted_GBs": bytes_ / t_sorted / 1e9,
+           "sorted_equals_natural_bitwise": same_sorted, "speedup_sorted_vs_cusparse": t_lib / t_sorted,
            "cusparse_us": t_lib * 1e6, "cusparse_GBs": bytes_ / t_lib / 1e9,
            "speedup_vs_cusparse": t_lib / t_ours, "cusparse_bitwise_equal_ours": same,
            "median_of": reps}
-    del A, ops, T
+    del A, As, ops, T
     torch.cuda.empty_cache()
     return out
 
