@@ -1,0 +1,68 @@
+"""The reference's acceptance gate (tests/test_acceptance.py criteria 1, 3
+and 7 — the solve-level ones SURVEY §8c lists as reusable) restated against
+the B200 package: oracle equivalence across grids, the communication
+ledger, and consistency across permutation / partitioning strategies."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, reference_solve, solve  # noqa: E402
+
+GRIDS = [(1, 1), (1, 2), (2, 1), (2, 2)]
+
+
+def rand_lp(seed, m=14, n=18, nnz=140, ineq=0.4):
+    return generate(GeneratorSpec(kind="uniform_random", num_rows=m, num_cols=n, nnz_target=nnz,
+                                  inequality_fraction=ineq, seed=seed))
+
+
+def test_criterion_1_oracle_equivalence_across_grids():
+    worst = 0.0
+    for seed in range(20):
+        p = rand_lp(seed)
+        res = {g: solve(p, SolverConfig(tolerance=1e-8, n_procs=g[0] * g[1], grid=g, seed=seed,
+                                        max_iterations=300_000)) for g in GRIDS}
+        ref = reference_solve(p, SolverConfig(tolerance=1e-8, seed=seed, max_iterations=300_000))
+        assert ref.status == "optimal" and all(r.status == "optimal" for r in res.values()), seed
+        obj = [r.objective for r in res.values()] + [ref.objective]
+        spread = (max(obj) - min(obj)) / max(1.0, max(abs(v) for v in obj))
+        worst = max(worst, spread)
+        assert spread <= 1e-6, (seed, spread)
+        solo = res[(1, 1)]
+        np.testing.assert_array_equal(solo.x, ref.x)
+        np.testing.assert_array_equal(solo.y, ref.y)
+        assert solo.iterations == ref.iterations and solo.report == ref.report
+
+
+def test_criterion_3_communication_ledger():
+    iters, k = 640, 64
+    passes = iters // k
+    cfg = SolverConfig(tolerance=1e-300, max_iterations=iters, kkt_interval=k, beta_sufficient=0.0,
+                       beta_necessary=0.0, beta_artificial=1e12, n_procs=4, grid=(2, 2), seed=17)
+    r = solve(rand_lp(17, m=24, n=32, nnz=300), cfg)
+    assert (r.status, r.iterations, r.restarts) == ("iteration_limit", iters, 0)
+    for entry in r.counters["main_loop"]:
+        ax = entry["axes"]
+        # per iteration one R and one C vector sum; per pass two C products
+        # (constraint, restart probe) and one R product (gradient)
+        assert ax["R"]["vector_calls"] == iters + passes
+        assert ax["C"]["vector_calls"] == iters + 2 * passes
+        assert ax["G"]["vector_calls"] == 0
+        assert (ax["R"]["scalar_calls"], ax["C"]["scalar_calls"], ax["G"]["scalar_calls"]) == \
+            (2 * passes, 3 * passes, 3 * passes)
+
+
+def test_criterion_7_strategy_consistency():
+    for seed in (1, 2, 3, 4, 5):
+        p = generate(GeneratorSpec(kind="block_diagonal", num_blocks=4, block_rows=6, block_cols=8,
+                                   nnz_target=120, seed=seed))
+        obj = []
+        for perm in ("none", "full_random", "block_random"):
+            for part in ("uniform", "nnz"):
+                r = solve(p, SolverConfig(tolerance=1e-7, max_iterations=50_000, n_procs=4, block_size=4,
+                                          permutation=perm, partitioning=part, seed=seed))
+                assert r.status == "optimal", (seed, perm, part)
+                obj.append(r.objective)
+        assert (max(obj) - min(obj)) / max(1.0, max(abs(v) for v in obj)) <= 1e-6, seed
