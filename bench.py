@@ -568,8 +568,12 @@ def main():
         run_ours(args, rank, world, local_rank)
     finally:
         if distributed:
+            import gc
+
             import torch.distributed as dist
 
+            gc.collect()            # drop IPC-imported peer buffers before any producer exits
+            dist.barrier()
             dist.destroy_process_group()
 
 
