@@ -305,6 +305,13 @@ int gridlp_op_dot(const double* a, const double* b, int64_t n,
 int gridlp_op_div(const double* in, double* out, int64_t n, double divisor,
                   void* stream);
 
+/* out_r = in_r / sqrt(*sumsq), the divisor read on the device from a
+ * reduction slot (the same correctly rounded sqrt and division as
+ * gridlp_op_div with divisor = sqrt(s_sq) computed on the host), so a
+ * single-block power iteration needs no host round trip per step. */
+int gridlp_op_div_norm(const double* in, double* out, int64_t n, const double* sumsq,
+                       void* stream);
+
 /* out_r = lo/hi projection of 0 (initial_device_state, pdhg_engine.py:349-353),
  * anchor_r = out_r. */
 int gridlp_op_init_primal(const gridlp_primal_t* pv, void* stream);

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import math
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -26,6 +27,7 @@ import torch
 
 from . import engine as eng
 from .comm import Ledger, NcclGrid, PeerGrid, VirtualGrid
+from .blocks import upload_csr
 from .layout import GridTopology, build_layout, layout_summary, unpermute_solution
 from .ops import CudaOps
 from .problem import reported_objective
@@ -187,6 +189,24 @@ def problem_scalars(problem):
             float(getattr(problem, "objective_constant", 0.0)))
 
 
+_HOST_POOL = []
+HOST_OVERLAP = True
+
+
+class _Done:
+    def __init__(self, value):
+        self.value = value
+
+    def result(self):
+        return self.value
+
+
+def _host_pool():
+    if not _HOST_POOL:
+        _HOST_POOL.append(ThreadPoolExecutor(2, thread_name_prefix="gridlp-host"))
+    return _HOST_POOL[0]
+
+
 def norm_probe_vector(n: int, seed: int) -> np.ndarray:
     """solver_driver.py:161-165."""
     return np.random.default_rng(np.random.SeedSequence(entropy=(seed, 0x5eed))).standard_normal(n)
@@ -233,13 +253,38 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
     t_start = time.perf_counter()
     timings = {}
     banded = hasattr(problem, "bands")
+    # host-only inputs of the step sizes (the reference's numpy RNG stream and
+    # norms, which must stay bit-identical) are computed on a helper thread
+    # while the layout and the device setup run; numpy drops the GIL in both
+    # while the matrix goes up (it does not depend on the layout), the
+    # layout's permutations follow on the same helper thread
+    host_job = lambda: (problem_scalars(problem), norm_probe_vector(int(problem.matrix.num_cols), cfg.seed))  # noqa: E731
     if banded and (cfg.permutation != "none" or cfg.partitioning != "uniform"):
         raise ValueError("a band problem (blocks generated per device) needs permutation='none' and "
                          "partitioning='uniform'")
     grid = GridTopology(1, 1) if force_1x1 else (GridTopology(*cfg.grid) if cfg.grid is not None else None)
-    layout = build_layout(problem, n_procs=1 if force_1x1 else cfg.n_procs, block_size=cfg.block_size,
-                          seed=cfg.seed, permutation=cfg.permutation, partitioning=cfg.partitioning,
-                          grid=grid)
+    layout_job = lambda: build_layout(problem, n_procs=1 if force_1x1 else cfg.n_procs,  # noqa: E731
+                                      block_size=cfg.block_size, seed=cfg.seed, permutation=cfg.permutation,
+                                      partitioning=cfg.partitioning, grid=grid)
+    opts = cfg.engine_options()
+    for k, v in (engine_overrides or {}).items():
+        setattr(opts, k, v)
+    preload = None
+    if (HOST_OVERLAP and not banded and opts.device_setup and torch.cuda.is_available()
+            and (device is None or device.type == "cuda")):
+        layout_f = _host_pool().submit(layout_job)
+        host_f = _host_pool().submit(host_job)
+        if device is None:
+            device = _device()
+        t0 = time.perf_counter()
+        preload = upload_csr(problem.matrix, device)
+        t1 = time.perf_counter()
+        layout = layout_f.result()
+        timings["setup_preload_s"] = t1 - t0
+        timings["layout_wait_s"] = time.perf_counter() - t1
+    else:
+        host_f = None if banded else (_host_pool().submit(host_job) if HOST_OVERLAP else _Done(host_job()))
+        layout = layout_job()
     timings["layout_s"] = time.perf_counter() - t_start
     R, C = layout.topology.rows, layout.topology.cols
     if device is None:
@@ -251,14 +296,16 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
                              f"got {comm.world}")
     else:
         comm = VirtualGrid(R, C)
-    cnorm, bnorm, const = problem_scalars(problem) if not banded else (0.0, 0.0, 0.0)
-    probe = norm_probe_vector(int(problem.matrix.num_cols), cfg.seed) if not banded else None
-    opts = cfg.engine_options()
-    for k, v in (engine_overrides or {}).items():
-        setattr(opts, k, v)
-    engine = eng.PdhgEngine(problem, layout, opts, comm, ops_factory or CudaOps, device,
-                            cnorm, bnorm, const)
+    engine = eng.PdhgEngine(problem, layout, opts, comm, ops_factory or CudaOps, device, 0.0, 0.0, 0.0,
+                            preload=preload)
+    del preload
     timings.update(engine.timings)
+    probe = None
+    if not banded:
+        t0 = time.perf_counter()
+        (cnorm, bnorm, const), probe = host_f.result()
+        engine.cnorm, engine.bnorm, engine.const = cnorm, bnorm, const
+        timings["host_scalars_wait_s"] = time.perf_counter() - t0
     if banded:
         cnorm, bnorm = engine.band_scalars()
         engine.cnorm, engine.bnorm = cnorm, bnorm
@@ -288,8 +335,11 @@ def _solve(problem, cfg: SolverConfig, trace=None, force_1x1=False, ops_factory=
     leader = (not comm.local) or comm.local[0] == (0, 0)
     out = engine.run(eta, omega, trace=trace, log_hook=_log_pass if leader else None)
     timings.update(engine.timings)
-    xs, ys = engine.solution_blocks()
-    x, y = unpermute_solution(layout, xs, ys)
+    xy = engine.solution_original()
+    if xy is None:
+        xs, ys = engine.solution_blocks()
+        xy = unpermute_solution(layout, xs, ys)
+    x, y = xy
     if scaled is not None:
         x, y = scaled.unscale(x, y)
         problem = original

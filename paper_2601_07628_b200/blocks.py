@@ -11,6 +11,8 @@ rows (include/gridlp_b200.h, gridlp_csr_t).
 from __future__ import annotations
 
 import ctypes
+import os
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -343,6 +345,17 @@ def upload(a, dtype, device) -> torch.Tensor:
     return out
 
 
+def upload_csr(A, device):
+    """The user's CSR (row_offsets int64, col_indices -> int32, values f64)
+    into HBM; the device setup's input (it needs no layout, so the solver
+    starts it while the layout is computed)."""
+    nnz = int(len(A.values))
+    ptr = upload(A.row_offsets, np.int64, device)
+    col = upload(A.col_indices, np.int32, device) if nnz else torch.zeros(1, dtype=torch.int32, device=device)
+    val = upload(A.values, np.float64, device) if nnz else torch.zeros(1, dtype=torch.float64, device=device)
+    return ptr, col, val
+
+
 class DeviceSetup:
     """One-off device preprocessing through the C ABI (csrc/gridlp_setup.cu):
     the original CSR is uploaded once; every local block is then extracted
@@ -350,7 +363,7 @@ class DeviceSetup:
     out as SELL-32 on the device. Replaces the host permute/slice/transpose
     (partition.py:262-319, sparse_kernels.py:27-58)."""
 
-    def __init__(self, problem, layout, device):
+    def __init__(self, problem, layout, device, preload=None):
         self.lib = native.load()
         self.device = device
         self.layout = layout
@@ -364,20 +377,26 @@ class DeviceSetup:
         def t(a, dt):
             return upload(a, dt, device)
 
-        self.src_ptr = t(A.row_offsets, np.int64)
-        self.src_col = t(A.col_indices, np.int32) if nnz else torch.zeros(1, dtype=torch.int32, device=device)
-        self.src_val = t(A.values, np.float64) if nnz else torch.zeros(1, dtype=torch.float64, device=device)
-        self.inv_col = t(layout.perm.inverse_cols(), np.int32) if n else torch.zeros(1, dtype=torch.int32,
-                                                                                      device=device)
+        t0 = time.perf_counter()
+        self.src_ptr, self.src_col, self.src_val = preload if preload is not None else upload_csr(A, device)
+        t1 = time.perf_counter()
+        # the column permutation goes up once; its inverse is a device scatter
+        self.col_perm = t(layout.perm.col_perm, np.int32) if n else torch.zeros(1, dtype=torch.int32, device=device)
+        self.inv_col = torch.zeros(max(n, 1), dtype=torch.int32, device=device)
+        if n:
+            self.inv_col[self.col_perm.long()] = torch.arange(n, dtype=torch.int32, device=device)
         self.row_perm = t(layout.perm.row_perm, np.int64) if m else torch.zeros(1, dtype=torch.int64,
                                                                                  device=device)
+        t2 = time.perf_counter()
         items = max(nnz, m + n) + 64
         segs = (m + n) + (m + n) // 32 + 64
         wsb = int(self.lib._lib.gridlp_setup_workspace_bytes(items, segs))
         self.ws = torch.empty(wsb, dtype=torch.uint8, device=device)
         self.ws_bytes = wsb
+        self.times = {"setup_up_matrix_s": t1 - t0, "setup_up_perm_s": t2 - t1,
+                      "setup_ws_s": time.perf_counter() - t2}
         self.h2d_bytes = sum(x.numel() * x.element_size()
-                             for x in (self.src_ptr, self.src_col, self.src_val, self.inv_col, self.row_perm))
+                             for x in (self.src_ptr, self.src_col, self.src_val, self.col_perm, self.row_perm))
 
     def _stream(self):
         return torch.cuda.current_stream(self.device).cuda_stream
@@ -466,7 +485,7 @@ class DeviceSetup:
                     long_ptr=long_ptr[: nh + 1].clone(), long_cols=hcol, long_vals=hval)
 
     def release(self):
-        for name in ("src_ptr", "src_col", "src_val", "inv_col", "row_perm", "ws"):
+        for name in ("src_ptr", "src_col", "src_val", "col_perm", "inv_col", "row_perm", "ws"):
             setattr(self, name, None)
 
 

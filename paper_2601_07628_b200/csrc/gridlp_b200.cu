@@ -389,6 +389,19 @@ struct OpDiv {
   __device__ void row(int64_t r, double, const Data&, double*) const { out[r] = ddiv(in[r], divisor); }
 };
 
+struct OpDivNorm {
+  static constexpr int NRED = 0;
+  const double* in;
+  double* out;
+  const double* sumsq;
+  using Data = Empty;
+  __device__ void prepare() {}
+  __device__ Data load(int64_t) const { return {}; }
+  __device__ void row(int64_t r, double, const Data&, double*) const {
+    out[r] = ddiv(in[r], __dsqrt_rn(*sumsq));
+  }
+};
+
 struct OpInitPrimal {
   static constexpr int NRED = 0;
   double* x;
@@ -1025,6 +1038,12 @@ int gridlp_op_div(const double* in, double* out, int64_t n, double divisor, void
   if (n < 0 || (n > 0 && (!in || !out))) return fail(GRIDLP_ERR_ARG, "op_div: bad argument");
   gridlp_src_t src = rows_src(n);
   return launch_op(&src, OpDiv{in, out, divisor}, nullptr, stream, "op_div");
+}
+
+int gridlp_op_div_norm(const double* in, double* out, int64_t n, const double* sumsq, void* stream) {
+  if (n < 0 || !sumsq || (n > 0 && (!in || !out))) return fail(GRIDLP_ERR_ARG, "op_div_norm: bad argument");
+  gridlp_src_t src = rows_src(n);
+  return launch_op(&src, OpDivNorm{in, out, sumsq}, nullptr, stream, "op_div_norm");
 }
 
 int gridlp_op_init_primal(const gridlp_primal_t* pv, void* stream) {

@@ -175,7 +175,7 @@ class PdhgEngine:
     """Blocks, state and the main loop for the coords local to this process."""
 
     def __init__(self, problem, layout, opts: EngineOptions, comm, ops_factory, device,
-                 objective_norm: float, bound_norm: float, objective_constant: float):
+                 objective_norm: float, bound_norm: float, objective_constant: float, preload=None):
         self.opts = opts
         self.layout = layout
         self.comm = comm
@@ -185,7 +185,7 @@ class PdhgEngine:
         self.ledger = Ledger()
         self.timings = {}
         t0 = time.perf_counter()
-        self._build(problem)
+        self._build(problem, preload)
         if comm.kind == "peer":
             (i0, j0), = comm.local
             comm.setup_axes(self.rows[i0].m, self.cols[j0].n)
@@ -200,16 +200,17 @@ class PdhgEngine:
         self.iteration_events = None   # bench hook: list of (start, end, iterations)
 
     # ------------------------------------------------------------ setup
-    def _build(self, problem):
+    def _build(self, problem, preload=None):
         lay, dev = self.layout, self.device
         banded = hasattr(problem, "bands")       # blocks generated per device (synth.BandProblem)
         on_device = dev.type == "cuda" and (self.opts.device_setup or banded)
         tm = self.timings
         if on_device:
             t0 = time.perf_counter()
-            setup = BandSetup(problem, lay, dev) if banded else DeviceSetup(problem, lay, dev)
+            setup = BandSetup(problem, lay, dev) if banded else DeviceSetup(problem, lay, dev, preload)
             torch.cuda.synchronize(dev)
             tm["setup_upload_s"] = time.perf_counter() - t0
+            tm.update(getattr(setup, "times", {}))
             self.setup_h2d_bytes = setup.h2d_bytes
             host_blocks = None
         else:
@@ -226,7 +227,17 @@ class PdhgEngine:
         tm["setup_orders_s"] = time.perf_counter() - t0
         t0 = time.perf_counter()
         f64 = dict(dtype=torch.float64, device=dev)
-        if not banded:
+        # with the device setup the vectors go up in the user's order and one
+        # device gather per band applies layout permutation + internal order
+        # (the composed index is kept for the solution's way back)
+        dev_vec = on_device and not banded
+        self._col_idx, self._row_idx = {}, {}
+        if dev_vec:
+            cpd = setup.col_perm[:lay.num_cols].long()
+            rpd = setup.row_perm[:lay.num_rows]
+            obj, vlo, vhi, clo, chi = (upload(np.asarray(getattr(problem, k)), np.float64, dev) for k in
+                                       ("objective", "var_lower", "var_upper", "con_lower", "con_upper"))
+        elif not banded:
             obj = np.asarray(problem.objective, np.float64)[cp]
             vlo = np.asarray(problem.var_lower, np.float64)[cp]
             vhi = np.asarray(problem.var_upper, np.float64)[cp]
@@ -240,6 +251,12 @@ class PdhgEngine:
             c0, c1 = lay.col_range(j)
             n = c1 - c0
             t = lambda a: self._to_internal_col(j, a[c0:c1])  # noqa: E731
+            if dev_vec:
+                idx = cpd[c0:c1]
+                if self.sorted:
+                    idx = idx[self.col_order[j].long()]
+                self._col_idx[j] = idx
+                t = lambda a: a[idx]  # noqa: E731
             if banded:
                 cj, lj, hj, _ = problem.bands.col_data(c0, c1)
                 t = lambda a: a  # noqa: E731
@@ -252,6 +269,12 @@ class PdhgEngine:
             r0, r1 = lay.row_range(i)
             m = r1 - r0
             t = lambda a: self._to_internal_row(i, a[r0:r1])  # noqa: E731
+            if dev_vec:
+                idx = rpd[r0:r1]
+                if self.sorted:
+                    idx = idx[self.row_order[i].long()]
+                self._row_idx[i] = idx
+                t = lambda a: a[idx]  # noqa: E731
             if banded:
                 li, hi_, _ = problem.bands.row_data(r0, r1)
                 t = lambda a: a  # noqa: E731
@@ -344,7 +367,7 @@ class PdhgEngine:
             dev = self.device
             m, n = lay.num_rows, lay.num_cols
             row_len = (setup.src_ptr[1:] - setup.src_ptr[:-1])[setup.row_perm[:m]]
-            col_len = setup.col_counts_device()[upload(lay.perm.col_perm, np.int64, dev)] if n else row_len[:0]
+            col_len = setup.col_counts_device()[setup.col_perm[:n].long()] if n else row_len[:0]
             order, inverse = length_order_device, inverse_order_device
         else:
             A = problem.matrix
@@ -529,6 +552,8 @@ class PdhgEngine:
                                    torch.cuda.current_stream(self.device).cuda_stream)
                 continue
             col.v.copy_(self._to_internal_col(j, np.asarray(probe[c0:c1], dtype=np.float64)))
+        if self.comm.kind == "virtual" and self.R == 1 and self.C == 1 and self.device.type == "cuda":
+            return self._power_single_block(iters)
         est = 0.0
         for _ in range(iters):
             for i, row in self.rows.items():
@@ -565,6 +590,40 @@ class PdhgEngine:
             d = math.sqrt(s_sq)
             for col in self.cols.values():
                 ops.div(col.s, col.v, d)
+        return est
+
+    def _power_single_block(self, iters: int) -> float:
+        """power_estimate on a 1x1 grid without a host round trip per step:
+        v = s / sqrt(s_sq) takes s_sq from its reduction slot on the device
+        (gridlp_op_div_norm), each step's (u_sq, v_sq, s_sq) is copied to a
+        device history, and the reference's early exits are replayed on the
+        host from one read at the end. Steps after an early exit compute
+        garbage that is never read; the estimate, the ledger and v are those
+        of the step-by-step loop (v is only an internal probe)."""
+        ops = self.ops
+        row, col = self.rows[0], self.cols[0]
+        su, sv, ss = self.slot[("u", 0)], self.slot[("v", 0)], self.slot[("s", 0)]
+        pick = torch.tensor([su, sv, ss], dtype=torch.int64, device=self.device)
+        hist = torch.empty((iters, 3), dtype=torch.float64, device=self.device)
+        for k in range(iters):
+            ops.store(self._run_plan(self.plan_pow_u[0]), row.u, su)
+            ops.dot(col.v, col.v, sv)
+            ops.store(self._run_plan(self.plan_pow_s[0]), col.s, ss)
+            torch.index_select(ops.slots[:, 0], 0, pick, out=hist[k])
+            ops.div_norm(col.s, col.v, ss)
+        h = hist.cpu().numpy()
+        est = 0.0
+        for u_sq, v_sq, s_sq in h:
+            self.ledger.vec("C", "m")
+            self.ledger.scalar("G", 2)
+            u_sq, v_sq, s_sq = float(u_sq) / 1.0, float(v_sq) / 1.0, float(s_sq) / 1.0
+            if u_sq == 0.0 or v_sq == 0.0:
+                return 0.0
+            est = math.sqrt(u_sq / v_sq)
+            self.ledger.vec("R", "n")
+            self.ledger.scalar("G")
+            if s_sq == 0.0:
+                return est
         return est
 
     # -------------------------------------------------------- main loop
@@ -608,17 +667,21 @@ class PdhgEngine:
             self._launch_iterations(count)
             return
         if self._graph is None:
-            # warm every kernel once outside capture (module loading), then capture
+            # warm every kernel once outside capture (the launch loads the
+            # module), then capture while the GPU runs those iterations: no
+            # synchronize before capture (torch.cuda.graph's context manager
+            # would add one), so instantiation overlaps device work
             self._launch_iterations(g)
             count -= g
             stream = torch.cuda.Stream(self.device)
-            stream.wait_stream(torch.cuda.current_stream(self.device))
             graph = torch.cuda.CUDAGraph()
             before = getattr(self.ops, "launches", 0)
             with torch.cuda.stream(stream):
-                with torch.cuda.graph(graph, stream=stream):
+                graph.capture_begin()
+                try:
                     self._launch_iterations(g)
-            torch.cuda.current_stream(self.device).wait_stream(stream)
+                finally:
+                    graph.capture_end()
             self._graph_launches = getattr(self.ops, "launches", 0) - before
             if hasattr(self.ops, "launches"):
                 self.ops.launches = before     # capture records, it does not launch
@@ -820,6 +883,21 @@ class PdhgEngine:
     def count_iterations(self, n: int):
         self.ledger.vec("R", "n", n)
         self.ledger.vec("C", "m", n)
+
+    def solution_original(self):
+        """(x, y) as host arrays in the user's index order, by one device
+        scatter each through the composed (layout permutation, internal
+        order) index of the device setup; None when that index is not
+        available (host setup, band problems, one block per process)."""
+        if self.comm.kind != "virtual" or len(self._col_idx) != self.C or len(self._row_idx) != self.R:
+            return None
+        x = torch.empty(self.layout.num_cols, dtype=torch.float64, device=self.device)
+        y = torch.empty(self.layout.num_rows, dtype=torch.float64, device=self.device)
+        for j, idx in self._col_idx.items():
+            x[idx] = self.cols[j].x
+        for i, idx in self._row_idx.items():
+            y[idx] = self.rows[i].y
+        return x.cpu().numpy(), y.cpu().numpy()
 
     def solution_blocks(self):
         """x blocks of grid columns (from devices (0, j)) and y blocks of grid

@@ -95,6 +95,7 @@ SIGNATURES = {
     "gridlp_op_anchor": ([_P, _P, c_int64, POINTER(Red), _P], c_int),
     "gridlp_op_dot": ([_P, _P, c_int64, POINTER(Red), _P], c_int),
     "gridlp_op_div": ([_P, _P, c_int64, c_double, _P], c_int),
+    "gridlp_op_div_norm": ([_P, _P, c_int64, _P, _P], c_int),
     "gridlp_op_init_primal": ([POINTER(Primal), _P], c_int),
     "gridlp_op_step_advance": ([_P, c_int64, _P], c_int),
     "gridlp_pdhg_iterate": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32, c_uint32, _P],

@@ -185,6 +185,11 @@ class CudaOps:
         self.launches += 1
         self.lib.call("gridlp_op_div", _ptr(inp), _ptr(out), inp.numel(), float(divisor), self.stream())
 
+    def div_norm(self, inp, out, slot: int):
+        self.launches += 1
+        self.lib.call("gridlp_op_div_norm", _ptr(inp), _ptr(out), inp.numel(), self.slots[slot].data_ptr(),
+                      self.stream())
+
     def init_primal(self, col):
         self.launches += 1
         self.lib.call("gridlp_op_init_primal", self.primal_struct(col), self.stream())
