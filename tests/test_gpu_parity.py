@@ -180,6 +180,23 @@ class TestProducts:
         np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
+    def test_div_norm_equals_host_divisor(self, ops):
+        """gridlp_op_div_norm (divisor sqrt(s_sq) read from a reduction slot
+        on the device) == gridlp_op_div with the divisor computed on the host
+        by math.sqrt, bit for bit (power iteration, sparse_kernels.py:92)."""
+        rng = np.random.default_rng(11)
+        s = rng.standard_normal(5003) * 10.0 ** rng.integers(-6, 6, 5003)
+        src = dev(s)
+        for sq in (2.0, 3.0e-7, 1.2345678901234567e11, float(np.dot(s, s))):
+            ops.slots[5, 0] = sq
+            a = torch.empty_like(src)
+            b = torch.empty_like(src)
+            ops.div_norm(src, a, 5)
+            ops.div(src, b, math.sqrt(sq))
+            np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
+            np.testing.assert_array_equal(a.cpu().numpy(), s / math.sqrt(sq))
+
+
 def _edge_vectors(rng, n):
     v = rng.standard_normal(n) * 10.0 ** rng.integers(-3, 3, n)
     special = [0.0, -0.0, np.inf, -np.inf, 1e-300, -1e308, 5.0]
