@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_tma(const __grid_constant__ CUte
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ uint64_t bars[WARPS][STAGES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* wbuf = reinterpret_cast<double*>(sm) + (size_t)warp * STAGES * 256;
+  double* wbuf = reinterpret_cast<double*>(sm) + (size_t)warp * STAGES * 512;  // 128-B slot per lane (TMA dst alignment)
   if (lane == 0)
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[warp][s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_tma(const __grid_constant__ CUte
     if (lane == 0) mbar_expect_tx(&bars[warp][s], 32 * 64);
     __syncwarp();
     int4 c = idx[r * 32 + lane];
-    gather4(wbuf + s * 256 + lane * 8, &tm, &bars[warp][s], 0, c.x >> 1, c.y >> 1, c.z >> 1, c.w >> 1);
+    gather4(wbuf + s * 512 + lane * 16, &tm, &bars[warp][s], 0, c.x >> 1, c.y >> 1, c.z >> 1, c.w >> 1);
   };
   for (int s = 0; s < STAGES; ++s) {
     long r = gw + s * nw;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_tma(const __grid_constant__ CUte
       }
     }
     int4 c = idx[r * 32 + lane];
-    const double* b = wbuf + s * 256 + lane * 8;
+    const double* b = wbuf + s * 512 + lane * 16;
     acc += b[0 + (c.x & 1)] + b[2 + (c.y & 1)] + b[4 + (c.z & 1)] + b[6 + (c.w & 1)];
     __syncwarp();
     long rn = gw + (k + STAGES) * nw;
@@ -193,7 +193,7 @@ int main() {
       }
       // TMA gather4
       const int STAGES = 4;
-      size_t smem = (size_t)WARPS * STAGES * 256 * 8;
+      size_t smem = (size_t)WARPS * STAGES * 512 * 8;
       CK(cudaFuncSetAttribute(k_tma<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       for (int rep = 0; rep < 2; ++rep) {
         CK(cudaMemset(out, 0, 64L << 20));
