@@ -385,6 +385,8 @@ def run_ours(args, rank, world, local_rank):
         over["light_row_max"] = args.light_row_max
     if args.no_graphs:
         over["use_graphs"] = False
+    if args.natural_order:
+        over["sorted_order"] = False
     if args.graph_nccl:
         over["graph_nccl"] = True
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
@@ -436,6 +438,7 @@ def run_ours(args, rank, world, local_rank):
         tr = json.loads(tf.read_text()).get(args.config)
         traffic = tr["bytes_per_iteration"] if isinstance(tr, dict) else tr
     restarts = engine._s["epoch"]
+    choices = {k: v for k, v in engine.choices.items()}
     del engine
     torch.cuda.empty_cache()
     spmv = spmv_compare(p, dev) if world == 1 and not args.no_spmv and not hasattr(p, "bands") else None
@@ -485,7 +488,7 @@ def run_ours(args, rank, world, local_rank):
                    "block_nnz_max_over_mean": balance,
                    "l2": "inputs larger than L2 (A + A^T = "
                    f"{24 * nnz_total / 1e6:.0f} MB of 126 MB L2 per iteration, streamed evict-first)",
-                   "restarts_in_timed_region": restarts},
+                   "restarts_in_timed_region": restarts, "layout_choices": choices},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "fused PDHG iteration (K1 A^T y+primal/Halpern, K2 A x_bar+dual/Halpern)",
@@ -523,6 +526,7 @@ def main():
     ap.add_argument("--no-spmv", action="store_true", help="skip the SpMV-only comparison with cuSPARSE")
     ap.add_argument("--light-row-max", type=int, default=None, help="EngineOptions.light_row_max override")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches (the NCCL executor's path)")
+    ap.add_argument("--natural-order", action="store_true", help="EngineOptions.sorted_order=False (layout order)")
     ap.add_argument("--graph-nccl", action="store_true", help="capture NCCL iterations in CUDA graphs (opt-in)")
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")

@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, BandSetup, DeviceCsr, DeviceSetup, inverse_order,
+from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, LIGHT_ROW_CANDIDATES, BandSetup, DeviceCsr, DeviceSetup, inverse_order,
                      inverse_order_device, length_order, length_order_device, permute_csr, permute_matrix,
                      slice_blocks, transpose, upload)
 from . import native
@@ -69,8 +69,14 @@ class EngineOptions:
     omega_max: float = 1e6
     time_limit_seconds: float | None = None
     exact_row_max: int = DEFAULT_EXACT_ROW_MAX   # rows up to this length: sequential (bit-exact) sums
-    light_row_max: int = DEFAULT_LIGHT_ROW_MAX   # rows up to this length: SELL-32 lanes
-    sorted_order: bool = True    # internal length-sorted row/column order per band (CUDA only)
+    # rows up to this length: SELL-32 lanes; None = per block, the fastest of
+    # LIGHT_ROW_CANDIDATES by a timed product (device setup; every choice is
+    # bit-identical, only the kernel path of rows in (128, 512] changes)
+    light_row_max: int | None = None
+    # internal length-class row/column order per band (CUDA only); None = on the
+    # virtual grid, when the matrix has rows longer than the lightest class,
+    # the faster of sorted / layout order by a timed trial on block (0, 0)
+    sorted_order: bool | None = None
     device_setup: bool = True
     use_graphs: bool = True
     # capture the NCCL executor's iterations (kernels + NCCL allreduces) in a
@@ -184,6 +190,8 @@ class PdhgEngine:
         self.cnorm, self.bnorm, self.const = objective_norm, bound_norm, objective_constant
         self.ledger = Ledger()
         self.timings = {}
+        self._ops_factory = ops_factory
+        self.choices = {}
         t0 = time.perf_counter()
         self._build(problem, preload)
         if comm.kind == "peer":
@@ -222,9 +230,15 @@ class PdhgEngine:
         t0 = time.perf_counter()
         # a band problem's row lengths are only known per block, and ranks sharing
         # a band must agree on its order, so it keeps the layout order
-        self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order and not banded,
+        self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order is not False and not banded,
                               setup if on_device else None)
         tm["setup_orders_s"] = time.perf_counter() - t0
+        prebuilt = {}
+        if (on_device and not banded and self.sorted and self.opts.sorted_order is None
+                and self.comm.kind == "virtual" and (0, 0) in set(self.comm.local)):
+            t0 = time.perf_counter()
+            prebuilt = self._order_trial(setup)
+            tm["setup_order_trial_s"] = time.perf_counter() - t0
         t0 = time.perf_counter()
         f64 = dict(dtype=torch.float64, device=dev)
         # with the device setup the vectors go up in the user's order and one
@@ -281,11 +295,16 @@ class PdhgEngine:
                 clo, chi = li, hi_
             self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
-        kw = dict(exact_row_max=self.opts.exact_row_max, light_row_max=self.opts.light_row_max)
+        kw = dict(exact_row_max=self.opts.exact_row_max,
+                  light_row_max=self.opts.light_row_max if self.opts.light_row_max is not None
+                  else DEFAULT_LIGHT_ROW_MAX)
         tm["setup_vectors_s"] = time.perf_counter() - t0
         nnz_of = {}
         for (i, j) in local:
-            if on_device:
+            if (i, j) in prebuilt:
+                self.blocks[(i, j)] = prebuilt[(i, j)]
+                nnz_of[(i, j)] = self.blocks[(i, j)].A.nnz
+            elif on_device:
                 t0 = time.perf_counter()
                 a = setup.block(i, j)
                 torch.cuda.synchronize(dev)
@@ -303,19 +322,16 @@ class PdhgEngine:
                     at = setup.permute(at, d32(self.col_order[j]), d32(self.row_inv[i]))
                 torch.cuda.synchronize(dev)
                 t2 = time.perf_counter()
-                sa = setup.sell(a, self.opts.light_row_max)
-                sa["shape"] = (a.num_rows, a.num_cols, a.nnz)
-                st = setup.sell(at, self.opts.light_row_max)
-                st["shape"] = (at.num_rows, at.num_cols, at.nnz)
+                da = self._sell_auto(setup, a)
+                dt = self._sell_auto(setup, at)
                 torch.cuda.synchronize(dev)
                 t3 = time.perf_counter()
                 tm["setup_extract_s"] = tm.get("setup_extract_s", 0.0) + t1 - t0
                 tm["setup_transpose_s"] = tm.get("setup_transpose_s", 0.0) + t2 - t1
                 tm["setup_sell_s"] = tm.get("setup_sell_s", 0.0) + t3 - t2
                 del a, at
-                self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(sa, dev, **kw), DeviceCsr(st, dev, **kw))
+                self.blocks[(i, j)] = BlockState(i, j, da, dt)
                 nnz_of[(i, j)] = self.blocks[(i, j)].A.nnz
-                tm["setup_csr_s"] = tm.get("setup_csr_s", 0.0) + time.perf_counter() - t3
             else:
                 hb = host_blocks[(i, j)]
                 ht = transpose(hb)
@@ -336,6 +352,9 @@ class PdhgEngine:
                 tab = self.comm.table({c: np.array([float(v)]) for c, v in nnz_of.items()})
                 self.per_device_nnz = [int(tab[c][0]) for c in coords]
         del host_blocks
+        self.choices.setdefault("order", "sorted" if self.sorted else "layout")
+        self.choices["light_row_max"] = {f"{k}{i},{j}": getattr(b, k).light_row_max
+                                         for (i, j), b in self.blocks.items() for k in ("A", "AT")}
         tensors = [t for b in self.blocks.values() for d in (b.A, b.AT) for t in d.tensors()]
         tensors += [t for c in self.cols.values() for t in (c.c, c.lo, c.hi)]
         tensors += [t for r in self.rows.values() for t in (r.lo, r.hi)]
@@ -345,6 +364,97 @@ class PdhgEngine:
                 t.numel() * t.element_size() for c in self.cols.values() for t in (c.c, c.lo, c.hi))
                 + sum(t.numel() * t.element_size() for r in self.rows.values() for t in (r.lo, r.hi)))
         self.passes = 0
+
+    # ------------------------------------------------- layout choices
+    def _sell_csr(self, setup, arr, light: int) -> DeviceCsr:
+        d = setup.sell(arr, light)
+        d["shape"] = (arr.num_rows, arr.num_cols, arr.nnz)
+        return DeviceCsr(d, self.device, exact_row_max=self.opts.exact_row_max, light_row_max=light)
+
+    def _time_products(self, mats) -> float:
+        """Median device time of one product with each matrix (summed), on
+        random gather vectors: the cost model of the layout choices."""
+        dev = self.device
+        ops = self._ops_factory(dev, max(m.slots() for m in mats) + 8, 1)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(0)
+        xs = [torch.rand(max(m.num_cols, 1), dtype=torch.float64, device=dev, generator=gen)[:m.num_cols]
+              for m in mats]
+        outs = [torch.empty(m.num_rows, dtype=torch.float64, device=dev) for m in mats]
+
+        def run():
+            for m, x, o in zip(mats, xs, outs):
+                ops.store(Fused(m, x), o)
+        run()
+        times = []
+        for _ in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run()
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        return sorted(times)[1] * 1e-3
+
+    def _sell_auto(self, setup, arr) -> DeviceCsr:
+        """SELL-32 layout of one block (or transpose). With light_row_max set
+        it is used as is; otherwise rows of length (128, 512] may go to the
+        SELL lanes instead of the warp-per-row path when a timed product says
+        so (lanes walk consecutive rows, so when neighbouring rows gather
+        neighbouring columns — multi-commodity coupling rows — their gathers
+        coalesce; on power-law rows the warp-per-row path is faster)."""
+        if self.opts.light_row_max is not None:
+            return self._sell_csr(setup, arr, self.opts.light_row_max)
+        cands = [DEFAULT_LIGHT_ROW_MAX]
+        if arr.num_rows and arr.nnz:
+            lens = arr.ptr[1:] - arr.ptr[:-1]
+            for lo, hi in zip(LIGHT_ROW_CANDIDATES, LIGHT_ROW_CANDIDATES[1:]):
+                if bool(((lens > lo) & (lens <= hi)).any()):
+                    cands.append(hi)
+        if len(cands) == 1:
+            return self._sell_csr(setup, arr, cands[0])
+        best, best_t = None, None
+        for light in cands:
+            d = self._sell_csr(setup, arr, light)
+            t = self._time_products([d])
+            if best_t is None or t < 0.97 * best_t:
+                best, best_t = d, t
+            del d
+        return best
+
+    def _order_trial(self, setup) -> dict:
+        """sorted_order=None: when the matrix has rows longer than the
+        lightest SELL class (so the row order decides kernel paths and gather
+        locality, not just slice padding), build block (0, 0) in both the
+        length-class order and the layout order and keep the faster (A + Aᵀ
+        products). Block-structured matrices (MCF: one commodity's rows gather
+        one commodity's columns) keep their locality in the layout order;
+        random and power-law ones gain from the classes. Returns the winning
+        block for reuse; the other order's orders are dropped."""
+        ptr = setup.src_ptr
+        if ptr.numel() < 2 or int((ptr[1:] - ptr[:-1]).max().item()) <= DEFAULT_LIGHT_ROW_MAX:
+            self.choices["order"] = "sorted"
+            return {}
+        a = setup.block(0, 0)
+        at = setup.transpose(a)
+        nat = BlockState(0, 0, self._sell_auto(setup, a), self._sell_auto(setup, at))
+        t_nat = self._time_products([nat.A, nat.AT])
+        d32 = lambda o: o.to(torch.int32)  # noqa: E731
+        sa = setup.permute(a, d32(self.row_order[0]), d32(self.col_inv[0]))
+        sat = setup.permute(at, d32(self.col_order[0]), d32(self.row_inv[0]))
+        del a, at
+        srt = BlockState(0, 0, self._sell_auto(setup, sa), self._sell_auto(setup, sat))
+        del sa, sat
+        t_srt = self._time_products([srt.A, srt.AT])
+        self.choices["order_trial_s"] = {"layout": t_nat, "sorted": t_srt}
+        if t_nat < 0.97 * t_srt:
+            self.choices["order"] = "layout"
+            self.sorted = False
+            self.row_order, self.row_inv, self.col_order, self.col_inv = {}, {}, {}, {}
+            return {(0, 0): nat}
+        self.choices["order"] = "sorted"
+        return {(0, 0): srt}
 
     # ------------------------------------------------- internal order
     def _internal_orders(self, problem, enabled: bool, setup=None):

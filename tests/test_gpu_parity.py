@@ -140,7 +140,7 @@ class TestProducts:
         ssq = float(ops.read_slots(1)[0][0])
         assert abs(ssq - float(np.sum(outs[0] ** 2))) <= 1e-12 * float(np.sum(outs[0] ** 2))
 
-    @pytest.mark.parametrize("light,exact", [(64, 4096), (0, 4096), (8, 8), (1, 65536)])
+    @pytest.mark.parametrize("light,exact", [(64, 4096), (0, 4096), (8, 8), (1, 65536), (512, 4096), (2048, 4096)])
     def test_row_classes_bitwise(self, ops, light, exact):
         """Every row up to exact_row_max is the sequential +0.0-seeded sum
         whichever class sums it (SELL lane, warp per row), including

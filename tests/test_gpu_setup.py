@@ -139,3 +139,27 @@ def test_staged_upload_converts_and_matches():
     vals = rng.standard_normal(STAGING_BYTES // 8 + 7)
     np.testing.assert_array_equal(upload(vals, np.float64, DEV).cpu().numpy(), vals)
     assert upload(np.zeros(0), np.float64, DEV).numel() == 0
+
+
+def test_layout_autotune_choices_solve_identically():
+    """The engine's timed layout choices (light_row_max per block, sorted vs
+    layout order) change kernel paths only: a problem with rows in (128, 512]
+    and longer solves bit for bit like every fixed choice."""
+    from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate
+    from paper_2601_07628_b200.api import _solve
+    from paper_2601_07628_b200.synth import McfSpec, generate_mcf
+
+    p = generate_mcf(McfSpec(num_nodes=40, num_arcs=1200, num_commodities=300, seed=2),
+                     torch.device("cuda", 0)).to_problem("mcf_small")
+    cfg = SolverConfig(tolerance=1e-4, seed=1, max_iterations=640, permutation="none")
+    auto = _solve(p, cfg)
+    for over in ({"light_row_max": 128, "sorted_order": True}, {"light_row_max": 512, "sorted_order": False},
+                 {"light_row_max": 256, "sorted_order": True}):
+        r = _solve(p, cfg, engine_overrides=over)
+        assert (r.status, r.iterations, r.restarts) == (auto.status, auto.iterations, auto.restarts)
+        np.testing.assert_array_equal(r.x, auto.x)
+        np.testing.assert_array_equal(r.y, auto.y)
+    q = generate(GeneratorSpec(kind="uniform_random", num_rows=300, num_cols=500, nnz_target=3000, seed=4))
+    a = _solve(q, SolverConfig(tolerance=1e-6, seed=4))
+    b = _solve(q, SolverConfig(tolerance=1e-6, seed=4), engine_overrides={"light_row_max": 128, "sorted_order": True})
+    np.testing.assert_array_equal(a.x, b.x)
