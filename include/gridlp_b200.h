@@ -110,6 +110,15 @@ typedef struct gridlp_csr {
   int32_t* chunk_done;        /* [num_long_rows] scratch, zero-initialised */
   int32_t light_row_max;      /* <= GRIDLP_ROW_MAX_LIMIT */
   int32_t exact_row_max;      /* >= light_row_max, <= GRIDLP_ROW_MAX_LIMIT */
+  /* Column bands: a block whose gather vector exceeds L2 may be stored as K
+   * CSRs over consecutive column ranges (entries keep their row order, so a
+   * row's band-k entries are the next ones of its scipy add chain). Band
+   * k > 0 has carry = the row sums of bands < k (written by gridlp_op_store
+   * of band k - 1), and every exact row's sequential sum starts from
+   * carry[row] instead of 0.0: the result is the unbanded sum bit for bit.
+   * Chunked rows (> exact_row_max) must lie wholly in the last band (their
+   * carry is then 0 and ignored). NULL = start from 0.0. */
+  const double* carry;
 } gridlp_csr_t;
 
 /*
@@ -189,11 +198,17 @@ typedef struct gridlp_dual {
 } gridlp_dual_t;
 
 /* Reduction workspace: `partials` holds capacity * GRIDLP_MAX_RED doubles;
- * the op writes its final sums to out[0..k). */
+ * the op writes its final sums to out[0..k). With `terms` (>= rows * k
+ * doubles) a fused product stores each row's k reduction terms and they are
+ * summed in a fixed row order (the partial-sum path's order): the sums no
+ * longer depend on the block's layout (row classes, light_row_max, column
+ * bands). terms = NULL: per-CTA partials in layout order. */
 typedef struct gridlp_red {
   double* partials;
   int64_t capacity;
   double* out;
+  double* terms;
+  int64_t terms_capacity;
 } gridlp_red_t;
 
 /* flags */

@@ -300,6 +300,7 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
                             preload=preload)
     del preload
     timings.update(engine.timings)
+    timings["layout_order"] = engine.choices.get("order")
     probe = None
     if not banded:
         t0 = time.perf_counter()

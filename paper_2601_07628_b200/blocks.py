@@ -298,6 +298,73 @@ def parts_src(parts, num_rows: int) -> native.Src:
     return s
 
 
+class BandedCsr:
+    """A block stored as K column bands (include/gridlp_b200.h, gridlp_csr_t
+    .carry): band k holds each row's entries with columns in
+    [cuts[k], cuts[k+1]) in their original order, rows over the full block.
+    A product runs band by band — bands 0..K-2 store running row sums into
+    `acc`, band k > 0 continues every row's add chain from acc — so each
+    band's slice of the gather vector stays L2-resident and the sums are the
+    unbanded ones bit for bit. Chunked rows (> exact_row_max) sit wholly in
+    the last band. ops.CudaOps.src issues the leading bands."""
+
+    def __init__(self, bands, cuts, device):
+        if len(bands) < 2:
+            raise ValueError("a banded block needs >= 2 bands")
+        self.bands = list(bands)
+        self.cuts = list(cuts)
+        b0 = self.bands[0]
+        self.num_rows, self.num_cols = b0.num_rows, b0.num_cols
+        self.nnz = sum(b.nnz for b in self.bands)
+        self.light_row_max = self.bands[-1].light_row_max
+        self.acc = torch.zeros(max(self.num_rows, 1), dtype=torch.float64, device=device)
+        for b in self.bands[1:]:
+            b.struct.carry = self.acc.data_ptr()
+
+    def tensors(self):
+        return tuple(t for b in self.bands for t in b.tensors()) + (self.acc,)
+
+    def slots(self) -> int:
+        return max(b.slots() for b in self.bands)
+
+    def launches(self) -> int:
+        return sum(b.launches() for b in self.bands)
+
+    def src(self, gather):
+        return self.bands[-1].src(gather)
+
+
+def split_column_bands(arr, cuts, exact_row_max: int):
+    """DeviceCsrArrays -> one DeviceCsrArrays per column band (torch ops on
+    the device; entry order inside a row kept). Rows longer than
+    exact_row_max go wholly to the last band."""
+    dev = arr.col.device
+    m, nnz = arr.num_rows, arr.nnz
+    lens = (arr.ptr[1:] - arr.ptr[:-1]).long()
+    row_of = torch.repeat_interleave(torch.arange(m, device=dev), lens)
+    col = arr.col[:nnz]
+    val = arr.val[:nnz]
+    inner = torch.as_tensor(list(cuts[1:-1]), dtype=torch.int32, device=dev)
+    band = torch.bucketize(col, inner, right=True)
+    K = len(cuts) - 1
+    heavy = lens > exact_row_max
+    if bool(heavy.any()):
+        band[heavy[row_of]] = K - 1
+    out = []
+    for k in range(K):
+        sel = band == k
+        cnt = torch.bincount(row_of[sel], minlength=m)
+        ptr = torch.zeros(m + 1, dtype=torch.int32, device=dev)
+        ptr[1:] = torch.cumsum(cnt, 0).to(torch.int32)
+        nk = int(ptr[-1].item()) if m else 0
+        ck = torch.empty(nk + 8, dtype=torch.int32, device=dev)
+        vk = torch.empty(nk + 8, dtype=torch.float64, device=dev)
+        ck[:nk] = col[sel]
+        vk[:nk] = val[sel]
+        out.append(DeviceCsrArrays(m, arr.num_cols, nk, ptr, ck, vk))
+    return out
+
+
 @dataclass
 class DeviceCsrArrays:
     """A block (or its transpose) as int32 CSR in HBM — the output of the

@@ -453,11 +453,33 @@ constexpr int SELL_MINB = 32;        // 64 warps per SM at <= 32 registers
 #define LONG_U 2                     // long-row kernel: 64-entry blocks (registers -> occupancy)
 #endif
 
+// A product row's epilogue. With `terms` (canonical reductions, launch_op)
+// the row's reduction terms are stored per row (terms[q * n + r]) and summed
+// later in a fixed row order independent of which kernel / CTA owned the
+// row; otherwise they accumulate into the thread's partials.
+template <class Op>
+__device__ __forceinline__ void emit_row(const Op& op, int64_t r, double s, const typename Op::Data& d,
+                                         double* acc, double* __restrict__ terms, int64_t n) {
+  if constexpr (Op::NRED > 0) {
+    if (terms) {
+      double t[Op::NRED];
+#pragma unroll
+      for (int q = 0; q < Op::NRED; ++q) t[q] = 0.0;
+      op.row(r, s, d, t);
+#pragma unroll
+      for (int q = 0; q < Op::NRED; ++q) terms[(int64_t)q * n + r] = t[q];
+      return;
+    }
+  }
+  op.row(r, s, d, acc);
+}
+
 // Deterministic per-CTA reduction of a SELL_NT-thread CTA: warp tree, then
 // warps in order, one slot per CTA.
 template <class Op>
 __device__ __forceinline__ void cta_partials(double (&acc)[Op::NRED > 0 ? Op::NRED : 1], double* partials) {
   if constexpr (Op::NRED > 0) {
+    if (!partials) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ double rs[Op::NRED][SELL_WPB];
 #pragma unroll
@@ -484,7 +506,7 @@ __device__ __forceinline__ void cta_partials(double (&acc)[Op::NRED > 0 ? Op::NR
 // reduction partials occupy slots [0, num_chunks).
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
-                                                              double* __restrict__ partials) {
+                                                              double* __restrict__ partials, double* __restrict__ terms) {
   constexpr int U = SELL_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   pdl_launch_dependents();
@@ -543,7 +565,7 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
     if (last) {
       const int row = A.long_rows[h];
       const typename Op::Data d = op.load(row);
-      op.row(row, t, d, acc);
+      emit_row(op, row, t, d, acc, terms, A.num_rows);
     }
   }
   cta_partials<Op>(acc, partials);
@@ -562,7 +584,7 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
 // add latency per entry. Reduction partials follow the heavy kernel's.
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
-                                                           double* __restrict__ partials) {
+                                                           double* __restrict__ partials, double* __restrict__ terms) {
   constexpr int U = LONG_U;
   constexpr int B = 32 * U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
@@ -594,7 +616,7 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) x[u] = 32 * u + lane < len ? ld_gather(g + ca[u], pl) : 0.0;
-    double s = 0.0;
+    double s = A.carry ? A.carry[A.long_rows[h]] : 0.0;   // column bands: continue the chain
     for (int j0 = 0; j0 < len; j0 += B) {
       double p[U];
 #pragma unroll
@@ -622,7 +644,7 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
     if (lane == 0) {
       const int row = A.long_rows[h];
       const typename Op::Data d = op.load(row);
-      op.row(row, s, d, acc);
+      emit_row(op, row, s, d, acc, terms, A.num_rows);
     }
   }
   cta_partials<Op>(acc, partials);
@@ -637,7 +659,8 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
 // memory and no barrier on the light path.
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t A, const double* __restrict__ g,
-                                                                   Op op, double* __restrict__ partials) {
+                                                                   Op op, double* __restrict__ partials,
+                                                                   double* __restrict__ terms) {
   constexpr int U = SELL_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   double acc[NR];
@@ -658,7 +681,7 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
       const int64_t base = (int64_t)A.slice_off[slice] + lane;
       const int* __restrict__ cp = A.sell_cols + base;
       const double* __restrict__ vp = A.sell_vals + base;
-      double s = 0.0;
+      double s = A.carry ? A.carry[r] : 0.0;   // column bands: continue the chain
       for (int j = 0; j < len; j += U) {
         int c[U];
         double v[U], x[U];
@@ -677,7 +700,7 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
       // epilogue operands are loaded after the sums: issuing them first costs
       // registers (occupancy) and measured slower (profiles/r1, variant 10)
       const typename Op::Data d = op.load(r);
-      op.row(r, s, d, acc);
+      emit_row(op, r, s, d, acc, terms, A.num_rows);
     }
   }
   cta_partials<Op>(acc, partials);
@@ -757,6 +780,28 @@ __global__ void __launch_bounds__(TPB) reduce_kernel(const double* __restrict__ 
     for (int q = 0; q < nred; ++q) out[q] = acc[q];
 }
 
+// Canonical reduction of per-row terms (emit_row): the same grid-stride row
+// partition and tree as rows_kernel, so a fused product's reductions do not
+// depend on its layout (row classes, light_row_max, column bands) and equal
+// those of the partial-sum path for the same rows.
+template <int NR>
+__global__ void __launch_bounds__(TPB) terms_reduce_kernel(const double* __restrict__ terms, int64_t n,
+                                                           double* __restrict__ partials) {
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * TPB + threadIdx.x; r < n; r += (int64_t)gridDim.x * TPB) {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) acc[q] = dadd(acc[q], terms[(int64_t)q * n + r]);
+  }
+  __shared__ double scratch[NR][WARPS];
+  block_sum<NR>(acc, scratch);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NR; ++q) partials[(int64_t)blockIdx.x * GRIDLP_MAX_RED + q] = acc[q];
+  }
+}
+
 __global__ void step_advance_kernel(gridlp_step_t* st, int64_t delta) {
   if (threadIdx.x == 0 && blockIdx.x == 0) st->inner_k += delta;
 }
@@ -798,8 +843,9 @@ int64_t src_rows(const gridlp_src_t* src) { return src->A ? src->A->num_rows : s
 // Launch one of a product's kernels; `after_sibling` marks a programmatic
 // dependency on the previous kernel of the same product (see pdl_wait).
 template <class Op>
-cudaError_t launch_part(void (*kern)(gridlp_csr_t, const double*, Op, double*), int64_t blocks, bool after_sibling,
-                        cudaStream_t s, const gridlp_csr_t& M, const double* gather, Op op, double* partials) {
+cudaError_t launch_part(void (*kern)(gridlp_csr_t, const double*, Op, double*, double*), int64_t blocks,
+                        bool after_sibling, cudaStream_t s, const gridlp_csr_t& M, const double* gather, Op op,
+                        double* partials, double* terms) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3((unsigned)blocks);
@@ -811,7 +857,7 @@ cudaError_t launch_part(void (*kern)(gridlp_csr_t, const double*, Op, double*), 
     cfg.attrs = at;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, kern, M, gather, op, partials);
+  return cudaLaunchKernelEx(&cfg, kern, M, gather, op, partials, terms);
 }
 
 template <class Op>
@@ -841,15 +887,25 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
     slots = n > 0 ? rows_blocks(n) : 0;
   }
   double* partials = nullptr;
+  double* terms = nullptr;
+  int64_t red_slots = slots;
   if (Op::NRED > 0) {
     if (!red || !red->out) return fail(GRIDLP_ERR_ARG, std::string(name) + ": reduction output required");
-    if (slots > 0) {
+    // canonical reductions for fused products when the caller passes a
+    // per-row term buffer (see gridlp_red_t)
+    if (src->A && n > 0 && red->terms && red->terms_capacity >= n * Op::NRED && red->partials &&
+        red->capacity >= rows_blocks(n)) {
+      terms = red->terms;
+      red_slots = rows_blocks(n);
+      partials = red->partials;
+    } else if (slots > 0) {
       if (!red->partials || red->capacity < slots)
         return fail(GRIDLP_ERR_WORKSPACE, std::string(name) + ": reduction workspace too small (need " +
                                               std::to_string(slots) + " slots)");
       partials = red->partials;
     }
   }
+  double* kpartials = terms ? nullptr : partials;   // product kernels' CTA partials
   if (slots > 0) {
     if (src->A) {
       const gridlp_csr_t& M = *src->A;
@@ -858,17 +914,17 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
       bool prev = false;
       cudaError_t e = cudaSuccess;
       if (M.num_chunks > 0) {
-        e = launch_part(heavy_chunk_kernel<Op>, M.num_chunks, prev, s, M, src->gather, op, partials);
+        e = launch_part(heavy_chunk_kernel<Op>, M.num_chunks, prev, s, M, src->gather, op, kpartials, terms);
         prev = true;
       }
       if (e == cudaSuccess && nlong > 0) {
         e = launch_part(long_row_kernel<Op>, nlong, prev, s, M, src->gather, op,
-                        partials ? partials + M.num_chunks * GRIDLP_MAX_RED : nullptr);
+                        kpartials ? kpartials + M.num_chunks * GRIDLP_MAX_RED : nullptr, terms);
         prev = true;
       }
       if (e == cudaSuccess && nlight > 0)
         e = launch_part(sell32_kernel<Op>, nlight, prev, s, M, src->gather, op,
-                        partials ? partials + (M.num_chunks + nlong) * GRIDLP_MAX_RED : nullptr);
+                        kpartials ? kpartials + (M.num_chunks + nlong) * GRIDLP_MAX_RED : nullptr, terms);
       if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
     } else
       rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials,
@@ -877,7 +933,12 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
     if (rc) return rc;
   }
   if (Op::NRED > 0) {
-    reduce_kernel<<<1, TPB, 0, s>>>(partials, slots, Op::NRED, red->out);
+    if (terms) {
+      terms_reduce_kernel<(Op::NRED > 0 ? Op::NRED : 1)><<<(unsigned)red_slots, TPB, 0, s>>>(terms, n, partials);
+      int rc = check_launch(name);
+      if (rc) return rc;
+    }
+    reduce_kernel<<<1, TPB, 0, s>>>(partials, red_slots, Op::NRED, red->out);
     int rc = check_launch(name);
     if (rc) return rc;
   }

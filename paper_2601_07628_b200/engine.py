@@ -30,7 +30,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, LIGHT_ROW_CANDIDATES, BandSetup, DeviceCsr, DeviceSetup, inverse_order,
+from .blocks import (DEFAULT_EXACT_ROW_MAX, DEFAULT_LIGHT_ROW_MAX, LIGHT_ROW_CANDIDATES, BandedCsr,
+                     split_column_bands, BandSetup, DeviceCsr, DeviceSetup, inverse_order,
                      inverse_order_device, length_order, length_order_device, permute_csr, permute_matrix,
                      slice_blocks, transpose, upload)
 from . import native
@@ -47,6 +48,10 @@ NUMERICAL_FAILURE = "numerical_failure"
 # per-coord scalar table fields of one KKT pass
 F_RP2, F_PEN, F_RD2, F_CX, F_RCX, F_DX2, F_DY2, F_CROSS, F_TIME = range(9)
 NFIELDS = 9
+
+
+ORDER_WINDOW_ROWS = 4096      # locality window of _choose_order
+ORDER_LOCALITY_RATIO = 2.0    # layout order when its window span is <= 1/2 of the class order's
 
 
 @dataclass
@@ -70,13 +75,19 @@ class EngineOptions:
     time_limit_seconds: float | None = None
     exact_row_max: int = DEFAULT_EXACT_ROW_MAX   # rows up to this length: sequential (bit-exact) sums
     # rows up to this length: SELL-32 lanes; None = per block, the fastest of
-    # LIGHT_ROW_CANDIDATES by a timed product (device setup; every choice is
-    # bit-identical, only the kernel path of rows in (128, 512] changes)
+    # LIGHT_ROW_CANDIDATES by a timed product (device setup). Result-neutral:
+    # products are bit-identical and fused reductions are summed in a fixed
+    # row order (gridlp_red_t.terms), so the choice may vary between runs
     light_row_max: int | None = None
-    # internal length-class row/column order per band (CUDA only); None = on the
-    # virtual grid, when the matrix has rows longer than the lightest class,
-    # the faster of sorted / layout order by a timed trial on block (0, 0)
+    # internal length-class row/column order per band (CUDA only); None = the
+    # class order unless the layout order has 2x better gather locality
+    # (deterministic statistic, PdhgEngine._choose_order)
     sorted_order: bool | None = None
+    # column bands per block (BandedCsr): None = when the gather vector of a
+    # block exceeds band_bytes, ceil(bytes / band_bytes) bands if a timed
+    # product says so; an int forces that many (1 = never). Bit-identical.
+    column_bands: int | None = None
+    band_bytes: int = 48 << 20
     device_setup: bool = True
     use_graphs: bool = True
     # capture the NCCL executor's iterations (kernels + NCCL allreduces) in a
@@ -202,6 +213,10 @@ class PdhgEngine:
                   + [b.AT.slots() for b in self.blocks.values()] + [1184])
         self.nslots = self._assign_slots()
         self.ops = ops_factory(device, cap, self.nslots)
+        if hasattr(self.ops, "enable_terms"):
+            # reductions independent of the layout choices (row classes, bands)
+            self.ops.enable_terms(max([b.A.num_rows for b in self.blocks.values()]
+                                      + [b.AT.num_rows for b in self.blocks.values()] + [1]))
         self._plans()
         self._graph = None
         self._graph_launches = 0
@@ -233,12 +248,10 @@ class PdhgEngine:
         self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order is not False and not banded,
                               setup if on_device else None)
         tm["setup_orders_s"] = time.perf_counter() - t0
-        prebuilt = {}
-        if (on_device and not banded and self.sorted and self.opts.sorted_order is None
-                and self.comm.kind == "virtual" and (0, 0) in set(self.comm.local)):
+        if on_device and not banded and self.sorted and self.opts.sorted_order is None:
             t0 = time.perf_counter()
-            prebuilt = self._order_trial(setup)
-            tm["setup_order_trial_s"] = time.perf_counter() - t0
+            self._choose_order(setup)
+            tm["setup_order_choice_s"] = time.perf_counter() - t0
         t0 = time.perf_counter()
         f64 = dict(dtype=torch.float64, device=dev)
         # with the device setup the vectors go up in the user's order and one
@@ -301,10 +314,7 @@ class PdhgEngine:
         tm["setup_vectors_s"] = time.perf_counter() - t0
         nnz_of = {}
         for (i, j) in local:
-            if (i, j) in prebuilt:
-                self.blocks[(i, j)] = prebuilt[(i, j)]
-                nnz_of[(i, j)] = self.blocks[(i, j)].A.nnz
-            elif on_device:
+            if on_device:
                 t0 = time.perf_counter()
                 a = setup.block(i, j)
                 torch.cuda.synchronize(dev)
@@ -322,8 +332,8 @@ class PdhgEngine:
                     at = setup.permute(at, d32(self.col_order[j]), d32(self.row_inv[i]))
                 torch.cuda.synchronize(dev)
                 t2 = time.perf_counter()
-                da = self._sell_auto(setup, a)
-                dt = self._sell_auto(setup, at)
+                da = self._block_auto(setup, a, not self.sorted)
+                dt = self._block_auto(setup, at, not self.sorted)
                 torch.cuda.synchronize(dev)
                 t3 = time.perf_counter()
                 tm["setup_extract_s"] = tm.get("setup_extract_s", 0.0) + t1 - t0
@@ -355,6 +365,9 @@ class PdhgEngine:
         self.choices.setdefault("order", "sorted" if self.sorted else "layout")
         self.choices["light_row_max"] = {f"{k}{i},{j}": getattr(b, k).light_row_max
                                          for (i, j), b in self.blocks.items() for k in ("A", "AT")}
+        self.choices["column_bands"] = {f"{k}{i},{j}": len(getattr(getattr(b, k), "bands", [None]))
+                                        for (i, j), b in self.blocks.items() for k in ("A", "AT")}
+        self._banded = any(isinstance(m, BandedCsr) for b in self.blocks.values() for m in (b.A, b.AT))
         tensors = [t for b in self.blocks.values() for d in (b.A, b.AT) for t in d.tensors()]
         tensors += [t for c in self.cols.values() for t in (c.c, c.lo, c.hi)]
         tensors += [t for r in self.rows.values() for t in (r.lo, r.hi)]
@@ -423,38 +436,82 @@ class PdhgEngine:
             del d
         return best
 
-    def _order_trial(self, setup) -> dict:
-        """sorted_order=None: when the matrix has rows longer than the
-        lightest SELL class (so the row order decides kernel paths and gather
-        locality, not just slice padding), build block (0, 0) in both the
-        length-class order and the layout order and keep the faster (A + Aᵀ
-        products). Block-structured matrices (MCF: one commodity's rows gather
-        one commodity's columns) keep their locality in the layout order;
-        random and power-law ones gain from the classes. Returns the winning
-        block for reuse; the other order's orders are dropped."""
-        ptr = setup.src_ptr
-        if ptr.numel() < 2 or int((ptr[1:] - ptr[:-1]).max().item()) <= DEFAULT_LIGHT_ROW_MAX:
+    def _block_auto(self, setup, arr, allow_bands: bool):
+        """_sell_auto, then column bands (BandedCsr) when the block's gather
+        vector is larger than band_bytes and banding is measured faster (or
+        forced by column_bands): each band's slice of x̄ / y then stays in
+        L2 instead of every gather being a DRAM sector. Only in the layout
+        order (allow_bands): there every row's entries ascend in the gather
+        index, so a column band is a contiguous piece of the row's add chain;
+        the length-class column relabeling would break that."""
+        best = self._sell_auto(setup, arr)
+        o = self.opts
+        if not allow_bands:
+            K = 1
+        elif o.column_bands is not None:
+            K = int(o.column_bands)
+        elif arr.nnz and arr.num_cols * 8 > o.band_bytes:
+            K = min(16, -(-arr.num_cols * 8 // o.band_bytes))
+        else:
+            K = 1
+        K = min(K, max(arr.num_cols, 1))
+        if K <= 1:
+            return best
+        cuts = [(k * arr.num_cols) // K for k in range(K + 1)]
+        parts = split_column_bands(arr, cuts, o.exact_row_max)
+        banded = BandedCsr([self._sell_auto(setup, p) for p in parts], cuts, self.device)
+        del parts
+        if o.column_bands is not None:
+            return banded
+        if self._time_products([banded]) < 0.97 * self._time_products([best]):
+            return banded
+        return best
+
+    def _choose_order(self, setup):
+        """sorted_order=None: keep the length-class order unless the layout
+        order has much better gather locality — the median column span of
+        ORDER_WINDOW_ROWS consecutive rows (128 SELL slices, about what the
+        GPU works on at once) in the layout order is at most half the span in
+        the class order (random and power-law matrices: ratio ~1.0; MCF 2.7-7). Block-structured matrices (multi-commodity
+        flow: one commodity's rows and columns together) keep the layout
+        order; each length class would sweep all commodities, re-reading x̄
+        from DRAM once per class. A pure function of the matrix and layout,
+        so every run and every rank decides alike (the two orders differ in
+        reduction rounding, not in products)."""
+        lay = self.layout
+        m, nnz = lay.num_rows, setup.nnz
+        if m == 0 or nnz == 0:
             self.choices["order"] = "sorted"
-            return {}
-        a = setup.block(0, 0)
-        at = setup.transpose(a)
-        nat = BlockState(0, 0, self._sell_auto(setup, a), self._sell_auto(setup, at))
-        t_nat = self._time_products([nat.A, nat.AT])
-        d32 = lambda o: o.to(torch.int32)  # noqa: E731
-        sa = setup.permute(a, d32(self.row_order[0]), d32(self.col_inv[0]))
-        sat = setup.permute(at, d32(self.col_order[0]), d32(self.row_inv[0]))
-        del a, at
-        srt = BlockState(0, 0, self._sell_auto(setup, sa), self._sell_auto(setup, sat))
-        del sa, sat
-        t_srt = self._time_products([srt.A, srt.AT])
-        self.choices["order_trial_s"] = {"layout": t_nat, "sorted": t_srt}
-        if t_nat < 0.97 * t_srt:
+            return
+        dev = self.device
+        ptr = setup.src_ptr
+        lens = ptr[1:] - ptr[:-1]
+        rid = torch.repeat_interleave(torch.arange(m, device=dev), lens)
+        lc = setup.inv_col[setup.src_col[:nnz].long()].long()
+        big = lay.num_cols + 1
+        rmin = torch.full((m,), big, dtype=torch.int64, device=dev).scatter_reduce(0, rid, lc, "amin")
+        rmax = torch.full((m,), -1, dtype=torch.int64, device=dev).scatter_reduce(0, rid, lc, "amax")
+        del rid, lc
+
+        def median_span(seq, w=ORDER_WINDOW_ROWS):
+            pad = (-seq.numel()) % w
+            mn = torch.cat([rmin[seq], torch.full((pad,), big, dtype=torch.int64, device=dev)]).view(-1, w)
+            mx = torch.cat([rmax[seq], torch.full((pad,), -1, dtype=torch.int64, device=dev)]).view(-1, w)
+            smin, smax = mn.min(1).values, mx.max(1).values
+            ok = smax >= 0
+            return float((smax - smin)[ok].double().median().item()) if bool(ok.any()) else 0.0
+
+        layout_seq = setup.row_perm[:m]
+        sorted_seq = torch.cat([layout_seq[lay.row_range(i)[0]:lay.row_range(i)[1]][self.row_order[i].long()]
+                                for i in range(self.R)])
+        span_layout, span_sorted = median_span(layout_seq), median_span(sorted_seq)
+        self.choices["order_spans"] = {"layout": span_layout, "sorted": span_sorted}
+        if ORDER_LOCALITY_RATIO * span_layout <= span_sorted:
             self.choices["order"] = "layout"
             self.sorted = False
             self.row_order, self.row_inv, self.col_order, self.col_inv = {}, {}, {}, {}
-            return {(0, 0): nat}
-        self.choices["order"] = "sorted"
-        return {(0, 0): srt}
+        else:
+            self.choices["order"] = "sorted"
 
     # ------------------------------------------------- internal order
     def _internal_orders(self, problem, enabled: bool, setup=None):
@@ -739,7 +796,7 @@ class PdhgEngine:
     # -------------------------------------------------------- main loop
     def _launch_iterations(self, count: int):
         ops, h = self.ops, self.opts.halpern
-        if self.R == 1 and self.C == 1 and hasattr(ops, "iterate") and count > 0:
+        if self.R == 1 and self.C == 1 and hasattr(ops, "iterate") and count > 0 and not self._banded:
             # one block, fused sources: the whole chunk in one C-ABI call
             (j, col), = self.cols.items()
             (i, row), = self.rows.items()

@@ -43,7 +43,7 @@ class Csr(ctypes.Structure):
                 ("exact_long", c_void_p), ("num_exact_long", c_int64),
                 ("chunk_first", c_void_p), ("chunk_row", c_void_p), ("num_chunks", c_int64),
                 ("chunk_sums", c_void_p), ("chunk_done", c_void_p),
-                ("light_row_max", c_int32), ("exact_row_max", c_int32)]
+                ("light_row_max", c_int32), ("exact_row_max", c_int32), ("carry", c_void_p)]
 
 
 class Peer(ctypes.Structure):
@@ -73,8 +73,12 @@ class Dual(ctypes.Structure):
                 ("hi", c_void_p), ("m", c_int64)]
 
 
+TERMS_PER_ROW = 4      # the most reduction terms a fused product op emits per row (KKT columns)
+
+
 class Red(ctypes.Structure):
-    _fields_ = [("partials", c_void_p), ("capacity", c_int64), ("out", c_void_p)]
+    _fields_ = [("partials", c_void_p), ("capacity", c_int64), ("out", c_void_p), ("terms", c_void_p),
+                ("terms_capacity", c_int64)]
 
 
 _P = c_void_p

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import native
-from .blocks import DeviceCsr, parts_src
+from .blocks import BandedCsr, DeviceCsr, parts_src
 
 
 class Fused:
@@ -81,16 +81,34 @@ class CudaOps:
     def stream(self):
         return torch.cuda.current_stream(self.device).cuda_stream
 
+    def enable_terms(self, rows: int):
+        """Canonical (layout-independent) reductions for fused products of up
+        to `rows` rows: a per-row term buffer (gridlp_red_t.terms)."""
+        self.terms = torch.empty(max(int(rows), 1) * native.TERMS_PER_ROW, dtype=torch.float64, device=self.device)
+        self._red = {}
+
     def red(self, slot: int):
         r = self._red.get(slot)
         if r is None:
-            r = native.Red(self.partials.data_ptr(), self.capacity, self.slots[slot].data_ptr())
+            t = getattr(self, "terms", None)
+            r = native.Red(self.partials.data_ptr(), self.capacity, self.slots[slot].data_ptr(),
+                           t.data_ptr() if t is not None else None, t.numel() if t is not None else 0)
             self._red[slot] = r
         return ctypes.byref(r)
 
     def src(self, s):
         key = id(s)
         hit = self._srcs.get(key)
+        if isinstance(s, Fused) and isinstance(s.mat, BandedCsr):
+            # leading column bands: running row sums into the block's carry
+            # buffer (launched on every use, so graphs capture them too)
+            key2 = ("bands", key)
+            hit2 = self._srcs.get(key2)
+            if hit2 is None or hit2[0] is not s:
+                hit2 = (s, [b.src(s.gather) for b in s.mat.bands[:-1]])
+                self._srcs[key2] = hit2
+            for c in hit2[1]:
+                self.lib.call("gridlp_op_store", ctypes.byref(c), s.mat.acc.data_ptr(), 0, None, self.stream())
         if hit is not None and hit[0] is s:
             return ctypes.byref(hit[1])
         if isinstance(s, Fused):

@@ -169,6 +169,41 @@ class TestProducts:
         num = ok & ~np.isnan(want)         # NaN sign/payload is not IEEE-specified (x86 vs GPU default NaN)
         assert np.array_equal(np.signbit(got[num]), np.signbit(want[num]))
 
+    @pytest.mark.parametrize("K,light,exact", [(3, 64, 4096), (4, 8, 64), (2, 0, 16)])
+    def test_column_bands_bitwise(self, ops, K, light, exact):
+        """BandedCsr (column bands chained through the carry buffer) ==
+        the unbanded block bit for bit, with SELL, warp-per-row and chunked
+        rows (the latter kept whole in the last band) and empty rows."""
+        from paper_2601_07628_b200.blocks import BandedCsr, DeviceCsrArrays, split_column_bands
+
+        rng = np.random.default_rng(K * 100 + light)
+        m, n = 900, 5000
+        lens = rng.integers(0, 300, m)
+        lens[::5] = 0
+        lens[3] = 2000
+        ptr = np.concatenate([[0], np.cumsum(lens)])
+        col = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int64)
+        val = rng.standard_normal(len(col)) * 10.0 ** rng.integers(-8, 8, len(col))
+        x = rng.standard_normal(n)
+        h = host_csr(m, n, ptr, col, val)
+        whole = DeviceCsr(h, DEV, exact_row_max=exact, light_row_max=light)
+        want = torch.empty(m, dtype=torch.float64, device=DEV)
+        ops.store(Fused(whole, dev(x)), want)
+        arr = DeviceCsrArrays(m, n, len(col), torch.as_tensor(ptr.astype(np.int32), device=DEV),
+                              torch.as_tensor(np.concatenate([col, np.zeros(8, np.int64)]).astype(np.int32), device=DEV),
+                              dev(np.concatenate([val, np.zeros(8)])))
+        cuts = [(k * n) // K for k in range(K + 1)]
+        parts = split_column_bands(arr, cuts, exact)
+        assert sum(p.nnz for p in parts) == len(col)
+        bands = [DeviceCsr(host_csr(m, n, p.ptr.cpu().numpy(), p.col[:p.nnz].cpu().numpy(),
+                                    p.val[:p.nnz].cpu().numpy()), DEV, exact_row_max=exact, light_row_max=light)
+                 for p in parts]
+        banded = BandedCsr(bands, cuts, DEV)
+        cap = CudaOps(DEV, banded.slots() + whole.slots() + 8, 4)
+        got = torch.empty(m, dtype=torch.float64, device=DEV)
+        cap.store(Fused(banded, dev(x)), got)
+        np.testing.assert_array_equal(got.cpu().numpy(), want.cpu().numpy())
+
     def test_parts_sum_ascending(self, ops):
         rng = np.random.default_rng(3)
         parts = [rng.standard_normal(777) * 10.0 ** rng.integers(-8, 8, 777) for _ in range(5)]

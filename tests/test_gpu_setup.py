@@ -159,7 +159,29 @@ def test_layout_autotune_choices_solve_identically():
         assert (r.status, r.iterations, r.restarts) == (auto.status, auto.iterations, auto.restarts)
         np.testing.assert_array_equal(r.x, auto.x)
         np.testing.assert_array_equal(r.y, auto.y)
+        if over["sorted_order"] == (auto.timings.get("layout_order") == "sorted"):
+            assert r.report == auto.report      # canonical reductions: KKT sums independent of row classes
     q = generate(GeneratorSpec(kind="uniform_random", num_rows=300, num_cols=500, nnz_target=3000, seed=4))
     a = _solve(q, SolverConfig(tolerance=1e-6, seed=4))
     b = _solve(q, SolverConfig(tolerance=1e-6, seed=4), engine_overrides={"light_row_max": 128, "sorted_order": True})
     np.testing.assert_array_equal(a.x, b.x)
+
+
+@pytest.mark.parametrize("over", [{"column_bands": 3, "sorted_order": False},
+                                  {"column_bands": 2, "light_row_max": 8, "exact_row_max": 32, "sorted_order": False}])
+def test_column_bands_solve_identically(golden_cfg1, over):
+    """Column-banded blocks (forced) solve bit for bit like unbanded ones,
+    on the virtual grid and with row classes that put chunked rows in play."""
+    from paper_2601_07628_b200 import SolverConfig
+    from paper_2601_07628_b200.api import _solve
+
+    p = golden_problem(golden_cfg1)
+    base = {k: v for k, v in over.items() if k != "column_bands"}
+    for grid in ((1, 1), (2, 2)):
+        cfg = SolverConfig(tolerance=1e-6, seed=0, n_procs=grid[0] * grid[1], grid=grid, max_iterations=2048)
+        a = _solve(p, cfg, engine_overrides=dict(base, column_bands=1))
+        b = _solve(p, cfg, engine_overrides=over)
+        assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+        np.testing.assert_array_equal(a.x, b.x)
+        np.testing.assert_array_equal(a.y, b.y)
+        assert a.report == b.report
