@@ -157,3 +157,42 @@ def test_length_order_classes():
         ls = lens[o[s:s + 32]]
         if 8 < ls.min() and ls.max() < 1000:
             assert ls.max() <= 1.2 * ls.min() + 1
+
+
+@pytest.mark.parametrize("K,exact", [(2, 4096), (3, 50), (5, 8)])
+def test_column_band_split(K, exact):
+    """split_column_bands (torch ops, here on CPU tensors): every row's
+    entries are distributed over the bands by column range, each band keeps
+    the row's entry order, rows longer than exact_row_max go wholly to the
+    last band, and concatenating a row's band pieces in band order gives the
+    row back (so chaining the bands' sums reproduces the row's add chain)."""
+    import torch
+
+    from paper_2601_07628_b200.blocks import DeviceCsrArrays, split_column_bands
+
+    rng = np.random.default_rng(K + exact)
+    m, n = 300, 1000
+    lens = rng.integers(0, 80, m)
+    lens[::9] = 0
+    ptr = np.concatenate([[0], np.cumsum(lens)])
+    col = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int32)
+    val = rng.standard_normal(len(col))
+    arr = DeviceCsrArrays(m, n, len(col), torch.as_tensor(ptr.astype(np.int32)),
+                          torch.as_tensor(np.concatenate([col, np.zeros(8, np.int32)])),
+                          torch.as_tensor(np.concatenate([val, np.zeros(8)])))
+    cuts = [(k * n) // K for k in range(K + 1)]
+    bands = split_column_bands(arr, cuts, exact)
+    assert len(bands) == K and sum(b.nnz for b in bands) == len(col)
+    for r in range(m):
+        pieces_c, pieces_v = [], []
+        for k, b in enumerate(bands):
+            p0, p1 = int(b.ptr[r]), int(b.ptr[r + 1])
+            c = b.col[p0:p1].numpy()
+            if lens[r] > exact:
+                assert k == K - 1 or p1 == p0
+            elif p1 > p0:
+                assert c.min() >= cuts[k] and c.max() < cuts[k + 1]
+            pieces_c.append(c)
+            pieces_v.append(b.val[p0:p1].numpy())
+        np.testing.assert_array_equal(np.concatenate(pieces_c), col[ptr[r]:ptr[r + 1]])
+        np.testing.assert_array_equal(np.concatenate(pieces_v), val[ptr[r]:ptr[r + 1]])
