@@ -159,8 +159,9 @@ def test_length_order_classes():
             assert ls.max() <= 1.2 * ls.min() + 1
 
 
-@pytest.mark.parametrize("K,exact", [(2, 4096), (3, 50), (5, 8)])
-def test_column_band_split(K, exact):
+@pytest.mark.parametrize("K,exact,relabel", [(2, 4096, False), (3, 50, False), (5, 8, False), (3, 4096, True),
+                                             (4, 30, True)])
+def test_column_band_split(K, exact, relabel):
     """split_column_bands (torch ops, here on CPU tensors): every row's
     entries are distributed over the bands by column range, each band keeps
     the row's entry order, rows longer than exact_row_max go wholly to the
@@ -177,17 +178,27 @@ def test_column_band_split(K, exact):
     ptr = np.concatenate([[0], np.cumsum(lens)])
     col = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int32)
     val = rng.standard_normal(len(col))
+    # relabel: entries keep ascending LAYOUT columns but are stored under an
+    # internal relabeling (the engine's length-class order); to_layout maps back
+    to_layout = torch.as_tensor(rng.permutation(n).astype(np.int64)) if relabel else None
+    stored = col
+    if relabel:
+        inv = np.empty(n, np.int64)
+        inv[to_layout.numpy()] = np.arange(n)
+        stored = inv[col].astype(np.int32)
     arr = DeviceCsrArrays(m, n, len(col), torch.as_tensor(ptr.astype(np.int32)),
-                          torch.as_tensor(np.concatenate([col, np.zeros(8, np.int32)])),
+                          torch.as_tensor(np.concatenate([stored, np.zeros(8, np.int32)])),
                           torch.as_tensor(np.concatenate([val, np.zeros(8)])))
     cuts = [(k * n) // K for k in range(K + 1)]
-    bands = split_column_bands(arr, cuts, exact)
+    bands = split_column_bands(arr, cuts, exact, to_layout)
     assert len(bands) == K and sum(b.nnz for b in bands) == len(col)
     for r in range(m):
         pieces_c, pieces_v = [], []
         for k, b in enumerate(bands):
             p0, p1 = int(b.ptr[r]), int(b.ptr[r + 1])
             c = b.col[p0:p1].numpy()
+            if relabel:
+                c = to_layout.numpy()[c]
             if lens[r] > exact:
                 assert k == K - 1 or p1 == p0
             elif p1 > p0:
