@@ -334,10 +334,15 @@ class BandedCsr:
         return self.bands[-1].src(gather)
 
 
-def split_column_bands(arr, cuts, exact_row_max: int):
+def split_column_bands(arr, cuts, exact_row_max: int, to_layout=None):
     """DeviceCsrArrays -> one DeviceCsrArrays per column band (torch ops on
     the device; entry order inside a row kept). Rows longer than
-    exact_row_max go wholly to the last band."""
+    exact_row_max go wholly to the last band. Bands are ranges of the
+    LAYOUT column index, along which every row's entries ascend: with
+    `to_layout` (internal column -> layout column, the engine's length-class
+    order) the band of an entry is that of its layout column, so each band is
+    still a contiguous piece of every row's add chain; its internal columns
+    form one contiguous run per length class, a band's share of x̄."""
     dev = arr.col.device
     m, nnz = arr.num_rows, arr.nnz
     lens = (arr.ptr[1:] - arr.ptr[:-1]).long()
@@ -345,7 +350,8 @@ def split_column_bands(arr, cuts, exact_row_max: int):
     col = arr.col[:nnz]
     val = arr.val[:nnz]
     inner = torch.as_tensor(list(cuts[1:-1]), dtype=torch.int32, device=dev)
-    band = torch.bucketize(col, inner, right=True)
+    key = col if to_layout is None else to_layout[col.long()].to(torch.int32)
+    band = torch.bucketize(key, inner, right=True)
     K = len(cuts) - 1
     heavy = lens > exact_row_max
     if bool(heavy.any()):

@@ -332,8 +332,8 @@ class PdhgEngine:
                     at = setup.permute(at, d32(self.col_order[j]), d32(self.row_inv[i]))
                 torch.cuda.synchronize(dev)
                 t2 = time.perf_counter()
-                da = self._block_auto(setup, a, not self.sorted)
-                dt = self._block_auto(setup, at, not self.sorted)
+                da = self._block_auto(setup, a, self.col_order[j] if self.sorted else None)
+                dt = self._block_auto(setup, at, self.row_order[i] if self.sorted else None)
                 torch.cuda.synchronize(dev)
                 t3 = time.perf_counter()
                 tm["setup_extract_s"] = tm.get("setup_extract_s", 0.0) + t1 - t0
@@ -436,19 +436,17 @@ class PdhgEngine:
             del d
         return best
 
-    def _block_auto(self, setup, arr, allow_bands: bool):
+    def _block_auto(self, setup, arr, to_layout=None):
         """_sell_auto, then column bands (BandedCsr) when the block's gather
         vector is larger than band_bytes and banding is measured faster (or
         forced by column_bands): each band's slice of x̄ / y then stays in
-        L2 instead of every gather being a DRAM sector. Only in the layout
-        order (allow_bands): there every row's entries ascend in the gather
-        index, so a column band is a contiguous piece of the row's add chain;
-        the length-class column relabeling would break that."""
+        L2 instead of every gather being a DRAM sector. Bands are layout
+        column ranges (`to_layout` maps the length-class order back), along
+        which every row's entries ascend, so a band is a contiguous piece of
+        each row's add chain."""
         best = self._sell_auto(setup, arr)
         o = self.opts
-        if not allow_bands:
-            K = 1
-        elif o.column_bands is not None:
+        if o.column_bands is not None:
             K = int(o.column_bands)
         elif arr.nnz and arr.num_cols * 8 > o.band_bytes:
             K = min(16, -(-arr.num_cols * 8 // o.band_bytes))
@@ -458,7 +456,7 @@ class PdhgEngine:
         if K <= 1:
             return best
         cuts = [(k * arr.num_cols) // K for k in range(K + 1)]
-        parts = split_column_bands(arr, cuts, o.exact_row_max)
+        parts = split_column_bands(arr, cuts, o.exact_row_max, to_layout)
         banded = BandedCsr([self._sell_auto(setup, p) for p in parts], cuts, self.device)
         del parts
         if o.column_bands is not None:

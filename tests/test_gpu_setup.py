@@ -168,7 +168,9 @@ def test_layout_autotune_choices_solve_identically():
 
 
 @pytest.mark.parametrize("over", [{"column_bands": 3, "sorted_order": False},
-                                  {"column_bands": 2, "light_row_max": 8, "exact_row_max": 32, "sorted_order": False}])
+                                  {"column_bands": 3, "sorted_order": True},
+                                  {"column_bands": 2, "light_row_max": 8, "exact_row_max": 32, "sorted_order": False},
+                                  {"column_bands": 4, "light_row_max": 8, "exact_row_max": 32, "sorted_order": True}])
 def test_column_bands_solve_identically(golden_cfg1, over):
     """Column-banded blocks (forced) solve bit for bit like unbanded ones,
     on the virtual grid and with row classes that put chunked rows in play."""
