@@ -362,6 +362,7 @@ class PdhgEngine:
                 tab = self.comm.table({c: np.array([float(v)]) for c, v in nnz_of.items()})
                 self.per_device_nnz = [int(tab[c][0]) for c in coords]
         del host_blocks
+        self._trial_ops = None
         self.choices.setdefault("order", "sorted" if self.sorted else "layout")
         self.choices["light_row_max"] = {f"{k}{i},{j}": getattr(b, k).light_row_max
                                          for (i, j), b in self.blocks.items() for k in ("A", "AT")}
@@ -388,7 +389,10 @@ class PdhgEngine:
         """Median device time of one product with each matrix (summed), on
         random gather vectors: the cost model of the layout choices."""
         dev = self.device
-        ops = self._ops_factory(dev, max(m.slots() for m in mats) + 8, 1)
+        need = max(m.slots() for m in mats) + 8
+        ops = getattr(self, "_trial_ops", None)
+        if ops is None or ops.capacity < need:
+            ops = self._trial_ops = self._ops_factory(dev, max(need, 4096), 1)
         gen = torch.Generator(device=dev)
         gen.manual_seed(0)
         xs = [torch.rand(max(m.num_cols, 1), dtype=torch.float64, device=dev, generator=gen)[:m.num_cols]
