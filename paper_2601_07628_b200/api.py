@@ -193,6 +193,14 @@ _HOST_POOL = []
 HOST_OVERLAP = True
 
 
+class _Pair:
+    def __init__(self, a, b):
+        self.a, self.b = a, b
+
+    def result(self):
+        return self.a.result(), self.b.result()
+
+
 class _Done:
     def __init__(self, value):
         self.value = value
@@ -203,7 +211,7 @@ class _Done:
 
 def _host_pool():
     if not _HOST_POOL:
-        _HOST_POOL.append(ThreadPoolExecutor(2, thread_name_prefix="gridlp-host"))
+        _HOST_POOL.append(ThreadPoolExecutor(3, thread_name_prefix="gridlp-host"))
     return _HOST_POOL[0]
 
 
@@ -273,7 +281,9 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
     if (HOST_OVERLAP and not banded and opts.device_setup and torch.cuda.is_available()
             and (device is None or device.type == "cuda")):
         layout_f = _host_pool().submit(layout_job)
-        host_f = _host_pool().submit(host_job)
+        scal_f = _host_pool().submit(problem_scalars, problem)
+        probe_f = _host_pool().submit(norm_probe_vector, int(problem.matrix.num_cols), cfg.seed)
+        host_f = _Pair(scal_f, probe_f)
         if device is None:
             device = _device()
         t0 = time.perf_counter()
