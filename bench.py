@@ -406,6 +406,8 @@ def run_ours(args, rank, world, local_rank):
         over["sorted_order"] = False
     if args.column_bands is not None:
         over["column_bands"] = args.column_bands
+    if args.band_mb is not None:
+        over["band_bytes"] = int(args.band_mb) << 20
     if args.graph_nccl:
         over["graph_nccl"] = True
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
@@ -547,6 +549,7 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="eager launches (the NCCL executor's path)")
     ap.add_argument("--natural-order", action="store_true", help="EngineOptions.sorted_order=False (layout order)")
     ap.add_argument("--column-bands", type=int, default=None, help="EngineOptions.column_bands (1 = off)")
+    ap.add_argument("--band-mb", type=int, default=None, help="EngineOptions.band_bytes in MiB")
     ap.add_argument("--graph-nccl", action="store_true", help="capture NCCL iterations in CUDA graphs (opt-in)")
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")

@@ -214,6 +214,7 @@ typedef struct gridlp_red {
 /* flags */
 #define GRIDLP_F_HALPERN 1u   /* EngineConfig.halpern (pdhg_engine.py:396-399) */
 #define GRIDLP_F_SUMSQ 2u     /* op_store: also reduce sum of squares */
+#define GRIDLP_F_STREAM 4u    /* op_store: streaming (evict-first) output, e.g. column-band carries */
 
 /* --- library / device ---------------------------------------------------- */
 int gridlp_abi_version(void);

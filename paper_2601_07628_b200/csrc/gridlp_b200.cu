@@ -107,6 +107,12 @@ __device__ __forceinline__ int ld_stream(const int* p, uint64_t pol) {
                : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+// column-band carry: coherent (the kernel may rewrite the row), first to leave L2
+__device__ __forceinline__ double ld_carry(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
   double v;
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
@@ -157,7 +163,7 @@ __device__ __forceinline__ void block_sum(double (&acc)[NR], double (*scratch)[W
 
 struct Empty {};
 
-template <bool SUMSQ>
+template <bool SUMSQ, bool STREAM = false>
 struct OpStore {
   static constexpr int NRED = SUMSQ ? 1 : 0;
   double* out;
@@ -165,7 +171,10 @@ struct OpStore {
   __device__ void prepare() {}
   __device__ Data load(int64_t) const { return {}; }
   __device__ void row(int64_t r, double s, const Data&, double* acc) const {
-    out[r] = s;
+    if (STREAM)
+      __stcs(out + r, s);   // running sums of a column band: read once by the next band
+    else
+      out[r] = s;
     if (SUMSQ) acc[0] = dadd(acc[0], dmul(s, s));
   }
 };
@@ -616,7 +625,7 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) x[u] = 32 * u + lane < len ? ld_gather(g + ca[u], pl) : 0.0;
-    double s = A.carry ? A.carry[A.long_rows[h]] : 0.0;   // column bands: continue the chain
+    double s = A.carry ? ld_carry(A.carry + A.long_rows[h], pf) : 0.0;   // column bands: continue the chain
     for (int j0 = 0; j0 < len; j0 += B) {
       double p[U];
 #pragma unroll
@@ -681,7 +690,7 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
       const int64_t base = (int64_t)A.slice_off[slice] + lane;
       const int* __restrict__ cp = A.sell_cols + base;
       const double* __restrict__ vp = A.sell_vals + base;
-      double s = A.carry ? A.carry[r] : 0.0;   // column bands: continue the chain
+      double s = A.carry ? ld_carry(A.carry + r, pf) : 0.0;   // column bands: continue the chain
       for (int j = 0; j < len; j += U) {
         int c[U];
         double v[U], x[U];
@@ -1008,6 +1017,7 @@ int gridlp_op_store(const gridlp_src_t* src, double* out, uint32_t flags, const 
   if (!src) return fail(GRIDLP_ERR_ARG, "op_store: null source");
   if (!out && src_rows(src) > 0) return fail(GRIDLP_ERR_ARG, "op_store: null output");
   if (flags & GRIDLP_F_SUMSQ) return launch_op(src, OpStore<true>{out}, red, stream, "op_store");
+  if (flags & GRIDLP_F_STREAM) return launch_op(src, OpStore<false, true>{out}, red, stream, "op_store");
   return launch_op(src, OpStore<false>{out}, red, stream, "op_store");
 }
 

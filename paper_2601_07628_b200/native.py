@@ -26,6 +26,7 @@ HEAVY_CHUNK = 2048
 ROW_MAX_LIMIT = 65536
 F_HALPERN = 1
 F_SUMSQ = 2
+F_STREAM = 4
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -108,7 +108,8 @@ class CudaOps:
                 hit2 = (s, [b.src(s.gather) for b in s.mat.bands[:-1]])
                 self._srcs[key2] = hit2
             for c in hit2[1]:
-                self.lib.call("gridlp_op_store", ctypes.byref(c), s.mat.acc.data_ptr(), 0, None, self.stream())
+                self.lib.call("gridlp_op_store", ctypes.byref(c), s.mat.acc.data_ptr(), native.F_STREAM, None,
+                              self.stream())
         if hit is not None and hit[0] is s:
             return ctypes.byref(hit[1])
         if isinstance(s, Fused):
