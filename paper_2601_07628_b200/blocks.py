@@ -11,7 +11,6 @@ rows (include/gridlp_b200.h, gridlp_csr_t).
 from __future__ import annotations
 
 import ctypes
-import os
 import time
 from dataclasses import dataclass
 
