@@ -187,3 +187,23 @@ def test_column_bands_solve_identically(golden_cfg1, over):
         np.testing.assert_array_equal(a.x, b.x)
         np.testing.assert_array_equal(a.y, b.y)
         assert a.report == b.report
+
+
+def test_order_choice_is_deterministic_and_structural():
+    """sorted_order=None picks the order from the matrix alone: the same
+    choice on every prepare; random rows keep the length-class order, a
+    block-structured multi-commodity flow LP keeps its layout order."""
+    from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate
+    from paper_2601_07628_b200.api import prepare
+    from paper_2601_07628_b200.synth import McfSpec, generate_mcf
+
+    mcf = generate_mcf(McfSpec(num_nodes=200, num_arcs=4000, num_commodities=60, seed=3),
+                       torch.device("cuda", 0)).to_problem("mcf")
+    rnd = generate(GeneratorSpec(kind="uniform_random", num_rows=20000, num_cols=40000, nnz_target=200000, seed=3))
+    cfg = SolverConfig(tolerance=1e-4, seed=0, permutation="none")
+    picks = {}
+    for name, p in (("mcf", mcf), ("random", rnd)):
+        got = [prepare(p, cfg)[0].choices["order"] for _ in range(2)]
+        assert got[0] == got[1], name
+        picks[name] = got[0]
+    assert picks == {"mcf": "layout", "random": "sorted"}
