@@ -20,7 +20,7 @@ import torch
 from . import native
 
 DEFAULT_LIGHT_ROW_MAX = 128     # SELL-32 lanes (one lane per row); sweep in profiles/r1/row_classes.md
-LIGHT_ROW_CANDIDATES = (128, 256, 512)   # the engine's per-block choices (profiles/r1/layout_autotune.md)
+LIGHT_ROW_CANDIDATES = (128, 256, 512, 1024, 2048)   # the engine's per-block choices (profiles/r1/layout_autotune.md)
 DEFAULT_EXACT_ROW_MAX = 4096    # one warp per row, still sequential sums; longer rows are chunked
 
 

@@ -416,7 +416,7 @@ class PdhgEngine:
 
     def _sell_auto(self, setup, arr) -> DeviceCsr:
         """SELL-32 layout of one block (or transpose). With light_row_max set
-        it is used as is; otherwise rows of length (128, 512] may go to the
+        it is used as is; otherwise rows of length (128, 2048] may go to the
         SELL lanes instead of the warp-per-row path when a timed product says
         so (lanes walk consecutive rows, so when neighbouring rows gather
         neighbouring columns — multi-commodity coupling rows — their gathers
