@@ -14,6 +14,7 @@ from .api import (
     StepSizes,
     reference_solve,
     solve,
+    warmup,
 )
 from .generators import GeneratorSpec, box_lp_optimum, generate
 from .layout import (
@@ -38,5 +39,5 @@ __all__ = [
     "Permutation", "SolveResult", "SolverConfig", "SparseMatrix", "StepSizes",
     "block_random_permutation", "box_lp_optimum", "build_layout", "generate",
     "layout_summary", "load_mps", "nnz_balanced_cuts", "objective_value", "parse_mps", "reference_solve",
-    "reported_objective", "select_grid", "solve", "uniform_cuts", "unpermute_solution", "write_mps",
+    "reported_objective", "select_grid", "solve", "uniform_cuts", "unpermute_solution", "warmup", "write_mps",
 ]

@@ -376,6 +376,23 @@ def _solve(problem, cfg: SolverConfig, trace=None, force_1x1=False, ops_factory=
     )
 
 
+def warmup() -> None:
+    """Optional, once per process before the first timed solve: loads the
+    sm_100a kernels (CUDA loads each kernel lazily at its first launch), the
+    device-setup kernels and allocator pools, the pinned staging buffers and
+    the host helper threads, by solving a small LP. The first solve of a
+    process otherwise pays ~0.4 s for these (profiles/r1/e2e_host.md)."""
+    from .blocks import upload
+    from .generators import GeneratorSpec, generate
+
+    dev = _device()
+    upload(np.zeros(1 << 18), np.float64, dev)        # > 1 MB: allocates the pinned staging pair
+    p = generate(GeneratorSpec(kind="uniform_random", num_rows=3000, num_cols=5000, nnz_target=40000,
+                               inequality_fraction=0.3, seed=0))
+    _solve(p, SolverConfig(tolerance=1e-4, max_iterations=256))
+    torch.cuda.synchronize(dev)
+
+
 def solve(problem, cfg: SolverConfig | None = None) -> SolveResult:
     """Solve on the device grid; deterministic for fixed (problem, cfg, seed)
     (solver_driver.py:193-272)."""

@@ -141,3 +141,13 @@ def test_pass_log_line(caplog):
         solve(rand_lp(14, m=8, n=10, nnz=40), SolverConfig(tolerance=1e-300, max_iterations=128, kkt_interval=64))
     lines = [r.getMessage() for r in caplog.records if r.name == "gridlp.solver"]
     assert [int(pat.match(x).group(1)) for x in lines] == [64, 128]
+
+
+def test_warmup_then_solve():
+    """warmup() (optional, once per process) solves a small LP on the device;
+    later solves are unaffected."""
+    from paper_2601_07628_b200 import warmup
+
+    warmup()
+    r = solve(rand_lp(21, m=12, n=16, nnz=90), SolverConfig(tolerance=1e-6))
+    assert r.status == "optimal"

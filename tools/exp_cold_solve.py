@@ -17,8 +17,15 @@ from paper_2601_07628_b200 import SolverConfig, solve  # noqa: E402
 
 
 def main():
-    p = bench.make_problem(sys.argv[1] if len(sys.argv) > 1 else "cfg2")
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    p = bench.make_problem(args[0] if args else "cfg2")
     torch.cuda.synchronize()
+    if "--warmup" in sys.argv:
+        from paper_2601_07628_b200 import warmup
+
+        t0 = time.perf_counter()
+        warmup()
+        print(f"warmup() {time.perf_counter() - t0:.3f}s", flush=True)
     for k in range(3):
         t0 = time.perf_counter()
         r = solve(p, SolverConfig(tolerance=1e-4, seed=0))
