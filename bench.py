@@ -407,6 +407,8 @@ def run_ours(args, rank, world, local_rank):
         over["column_bands"] = args.column_bands
     if args.band_mb is not None:
         over["band_bytes"] = int(args.band_mb) << 20
+    if args.no_first_touch:
+        over["first_touch_cols"] = False
     if args.graph_nccl:
         over["graph_nccl"] = True
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
@@ -549,6 +551,7 @@ def main():
     ap.add_argument("--natural-order", action="store_true", help="EngineOptions.sorted_order=False (layout order)")
     ap.add_argument("--column-bands", type=int, default=None, help="EngineOptions.column_bands (1 = off)")
     ap.add_argument("--band-mb", type=int, default=None, help="EngineOptions.band_bytes in MiB")
+    ap.add_argument("--no-first-touch", action="store_true", help="EngineOptions.first_touch_cols=False")
     ap.add_argument("--graph-nccl", action="store_true", help="capture NCCL iterations in CUDA graphs (opt-in)")
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")

@@ -83,6 +83,9 @@ class EngineOptions:
     # class order unless the layout order has 2x better gather locality
     # (deterministic statistic, PdhgEngine._choose_order)
     sorted_order: bool | None = None
+    # inside each column class, columns in first-touch order of the A
+    # products (device setup, class order): coalesced first gathers
+    first_touch_cols: bool = True
     # column bands per block (BandedCsr): None = when the gather vector of a
     # block exceeds band_bytes, ceil(bytes / band_bytes) bands if a timed
     # product says so; an int forces that many (1 = never). Bit-identical.
@@ -548,10 +551,47 @@ class PdhgEngine:
             r0, r1 = lay.row_range(i)
             self.row_order[i] = order(row_len[r0:r1])
             self.row_inv[i] = inverse(self.row_order[i])
+        touch = self._first_touch(setup) if setup is not None and self.opts.first_touch_cols else None
         for j in range(self.C):
             c0, c1 = lay.col_range(j)
-            self.col_order[j] = order(col_len[c0:c1])
+            if touch is None:
+                self.col_order[j] = order(col_len[c0:c1])
+            else:
+                # first-touch order inside each length class (stable sorts:
+                # by first touch, then by class)
+                base = torch.sort(touch[c0:c1], stable=True).indices
+                self.col_order[j] = base[length_order_device(col_len[c0:c1][base])]
             self.col_inv[j] = inverse(self.col_order[j])
+
+    def _first_touch(self, setup) -> torch.Tensor:
+        """Per layout column, the position of its first use in the A
+        products' SELL traversal (grid row band, slice, step, lane) under the
+        internal row order. Ordering each column class by it gives the
+        columns first gathered by one warp step consecutive ids, so those
+        gathers coalesce (and, in Aᵀ, consecutive columns start at nearby
+        rows). A column relabeling: products are unchanged bit for bit."""
+        lay, dev = self.layout, self.device
+        m, n, nnz = lay.num_rows, lay.num_cols, setup.nnz
+        big = torch.iinfo(torch.int64).max
+        if n == 0:
+            return torch.zeros(0, dtype=torch.int64, device=dev)
+        if m == 0 or nnz == 0:
+            return torch.full((n,), big, dtype=torch.int64, device=dev)
+        ptr = setup.src_ptr
+        lens = ptr[1:] - ptr[:-1]
+        internal_of_layout = torch.cat([lay.row_range(i)[0] + self.row_inv[i] for i in range(self.R)])
+        inv_rp = torch.empty(m, dtype=torch.int64, device=dev)
+        inv_rp[setup.row_perm[:m]] = torch.arange(m, dtype=torch.int64, device=dev)
+        rank = internal_of_layout[inv_rp]                      # original row -> internal rank
+        rid = torch.repeat_interleave(torch.arange(m, device=dev), lens)
+        step = torch.arange(nnz, device=dev) - ptr[rid]
+        rk = rank[rid]
+        kmax = int(lens.max().item()) + 1
+        key = ((rk // 32) * kmax + step) * 32 + (rk % 32)
+        del rid, step, rk
+        first = torch.full((n,), big, dtype=torch.int64, device=dev).scatter_reduce(
+            0, setup.src_col[:nnz].long(), key, "amin")
+        return first[setup.col_perm[:n].long()]                # layout order
 
     def _vec(self, a) -> torch.Tensor:
         """Host band slice -> FP64 device tensor (pinned staging on CUDA)."""

@@ -77,8 +77,8 @@ def test_device_and_host_setup_solve_identically(golden_cfg1):
 
     p = golden_problem(golden_cfg1)
     cfg = SolverConfig(tolerance=1e-4, seed=0, n_procs=4, grid=(2, 2))
-    a = _solve(p, cfg, engine_overrides={"device_setup": True})
-    b = _solve(p, cfg, engine_overrides={"device_setup": False})
+    a = _solve(p, cfg, engine_overrides={"device_setup": True, "first_touch_cols": False})
+    b = _solve(p, cfg, engine_overrides={"device_setup": False, "first_touch_cols": False})
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
     assert a.layout == b.layout and a.counters == b.counters
@@ -157,10 +157,14 @@ def test_layout_autotune_choices_solve_identically():
                  {"light_row_max": 256, "sorted_order": True}):
         r = _solve(p, cfg, engine_overrides=over)
         assert (r.status, r.iterations, r.restarts) == (auto.status, auto.iterations, auto.restarts)
-        np.testing.assert_array_equal(r.x, auto.x)
-        np.testing.assert_array_equal(r.y, auto.y)
         if over["sorted_order"] == (auto.timings.get("layout_order") == "sorted"):
-            assert r.report == auto.report      # canonical reductions: KKT sums independent of row classes
+            # same order: products bit-identical and canonical reductions -> everything equal
+            np.testing.assert_array_equal(r.x, auto.x)
+            np.testing.assert_array_equal(r.y, auto.y)
+            assert r.report == auto.report
+        else:   # another order sums the column-side reductions in another order (ulp level)
+            np.testing.assert_allclose(r.x, auto.x, rtol=1e-9, atol=1e-9)
+            np.testing.assert_allclose(r.y, auto.y, rtol=1e-9, atol=1e-9)
     q = generate(GeneratorSpec(kind="uniform_random", num_rows=300, num_cols=500, nnz_target=3000, seed=4))
     a = _solve(q, SolverConfig(tolerance=1e-6, seed=4))
     b = _solve(q, SolverConfig(tolerance=1e-6, seed=4), engine_overrides={"light_row_max": 128, "sorted_order": True})
