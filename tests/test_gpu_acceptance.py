@@ -8,7 +8,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, reference_solve, solve  # noqa: E402
+from oracle import pdhg_oracle  # noqa: E402  (the checker: CPU restatement pinned to the reference)
+from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, solve  # noqa: E402
 
 GRIDS = [(1, 1), (1, 2), (2, 1), (2, 2)]
 
@@ -24,16 +25,25 @@ def test_criterion_1_oracle_equivalence_across_grids():
         p = rand_lp(seed)
         res = {g: solve(p, SolverConfig(tolerance=1e-8, n_procs=g[0] * g[1], grid=g, seed=seed,
                                         max_iterations=300_000)) for g in GRIDS}
-        ref = reference_solve(p, SolverConfig(tolerance=1e-8, seed=seed, max_iterations=300_000))
+        # the CPU oracle (reference algorithm, pinned bitwise to the reference's
+        # own solves) on the 1x1 grid: test_acceptance.py:44-80 compares the
+        # grids with an independent oracle, not with one of themselves
+        ref = pdhg_oracle.oracle_solve(p, tolerance=1e-8, seed=seed, max_iterations=300_000)
         assert ref.status == "optimal" and all(r.status == "optimal" for r in res.values()), seed
         obj = [r.objective for r in res.values()] + [ref.objective]
         spread = (max(obj) - min(obj)) / max(1.0, max(abs(v) for v in obj))
         worst = max(worst, spread)
         assert spread <= 1e-6, (seed, spread)
-        solo = res[(1, 1)]
-        np.testing.assert_array_equal(solo.x, ref.x)
-        np.testing.assert_array_equal(solo.y, ref.y)
-        assert solo.iterations == ref.iterations and solo.report == ref.report
+        for g, r in res.items():
+            want = pdhg_oracle.oracle_solve(p, tolerance=1e-8, seed=seed, max_iterations=300_000,
+                                            n_procs=g[0] * g[1], grid=g)
+            assert (r.iterations, r.restarts) == (want.iterations, want.restarts), (seed, g)
+            # only the norm/dot reduction order differs (tree vs OpenBLAS ddot)
+            np.testing.assert_allclose(r.x, want.x, rtol=1e-9, atol=1e-12)
+            np.testing.assert_allclose(r.y, want.y, rtol=1e-9, atol=1e-12)
+            for key in ("r_primal", "r_dual", "r_gap", "obj_primal", "obj_dual"):
+                a, b = getattr(r.report, key), getattr(want, key)
+                assert abs(a - b) <= 1e-6 * max(abs(b), 1e-12) or abs(a - b) <= 1e-14, (seed, g, key)
 
 
 def test_criterion_3_communication_ledger():
