@@ -171,6 +171,13 @@ def make_problem(name):
     return p
 
 
+def kernel_tuning() -> dict:
+    from paper_2601_07628_b200 import native
+
+    lib = native.load()
+    return {k: lib.get_tuning(k) for k in ("sell_variant", "tma_ctas_per_sm", "chain_products")}
+
+
 def workload_name(cfg: str) -> str:
     c = CONFIGS[cfg]
     return WORKLOADS[c.get("gen") or c["kind"]]
@@ -411,6 +418,8 @@ def run_ours(args, rank, world, local_rank):
         over["first_touch_cols"] = False
     if args.graph_nccl:
         over["graph_nccl"] = True
+    if args.hot_mb is not None:
+        over["hot_gather_bytes"] = int(args.hot_mb) << 20
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
     log(f"[bench] rank {rank}: setup {time.perf_counter() - t0:.1f}s {tim}")
     R, C = layout.topology.rows, layout.topology.cols
@@ -510,7 +519,9 @@ def run_ours(args, rank, world, local_rank):
                    "block_nnz_max_over_mean": balance,
                    "l2": "inputs larger than L2 (A + A^T = "
                    f"{24 * nnz_total / 1e6:.0f} MB of 126 MB L2 per iteration, streamed evict-first)",
-                   "restarts_in_timed_region": restarts, "layout_choices": choices},
+                   "restarts_in_timed_region": restarts, "layout_choices": choices,
+                   "kernel_tuning": kernel_tuning(),
+                   "ranks_share_gpus": world > 1 and args.dist_backend == "gloo"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "fused PDHG iteration (K1 A^T y+primal/Halpern, K2 A x_bar+dual/Halpern)",
@@ -535,6 +546,35 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` without torchrun: start N copies of this script
+    with RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* set (what torchrun
+    exports), one per GPU; rank 0 prints the JSON line. With fewer GPUs than
+    N the ranks share devices over gloo (an orchestration run: the line says
+    ranks_share_gpus, and its time is not a scaling number)."""
+    import socket
+    import subprocess
+
+    import torch
+
+    ngpu = torch.cuda.device_count()
+    share = ngpu < args.gpus
+    if share:
+        log(f"[bench] --gpus {args.gpus} on {ngpu} visible GPU(s): ranks share devices over gloo")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        if share:
+            env["GRIDLP_SHARE_GPUS"] = "1"
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve())] + sys.argv[1:], env=env))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -552,7 +592,8 @@ def main():
     ap.add_argument("--column-bands", type=int, default=None, help="EngineOptions.column_bands (1 = off)")
     ap.add_argument("--band-mb", type=int, default=None, help="EngineOptions.band_bytes in MiB")
     ap.add_argument("--no-first-touch", action="store_true", help="EngineOptions.first_touch_cols=False")
-    ap.add_argument("--graph-nccl", action="store_true", help="capture NCCL iterations in CUDA graphs (opt-in)")
+    ap.add_argument("--graph-nccl", action="store_true", help="capture NCCL iterations in CUDA graphs (default now)")
+    ap.add_argument("--hot-mb", type=int, default=None, help="EngineOptions.hot_gather_bytes in MiB (0 = off)")
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")
     ap.add_argument("--partitioning", default=None, help="SolverConfig.partitioning override")
@@ -562,15 +603,27 @@ def main():
                     help="multi-GPU vector sums: NCCL allreduce (default) or in-kernel peer-memory exchange")
     ap.add_argument("--force-nccl", action="store_true",
                     help="run the NCCL executor even at world size 1 (exercises the multi-GPU path on one GPU)")
+    ap.add_argument("--tuning", action="append", default=[],
+                    help="KEY=VALUE kernel knob (gridlp_set_tuning: sell_variant, tma_ctas_per_sm, chain_products)")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)
     ap.add_argument("--ref-sample-iters", type=int, default=4)
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")
         args.warmup = 3
+    if "WORLD_SIZE" in os.environ:
+        world_env = int(os.environ["WORLD_SIZE"])
+        if world_env != args.gpus and not (args.gpus == 1 and world_env == 1):
+            raise SystemExit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}: launch one rank per GPU")
+    elif args.gpus > 1:
+        # no launcher: spawn the N ranks ourselves (torchrun's environment)
+        raise SystemExit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if (args.impl == "ours" and world > 1 and args.dist_backend == "nccl"
+            and os.environ.get("GRIDLP_SHARE_GPUS") == "1"):
+        args.dist_backend = "gloo"
     if args.dist_backend == "gloo":
         # orchestration check on fewer GPUs than ranks: ranks share devices
         import torch
@@ -593,6 +646,12 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.tuning:
+        from paper_2601_07628_b200 import native
+
+        for kv in args.tuning:
+            k, v = kv.split("=", 1)
+            native.load().set_tuning(k, int(v))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

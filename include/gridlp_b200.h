@@ -119,6 +119,12 @@ typedef struct gridlp_csr {
    * Chunked rows (> exact_row_max) must lie wholly in the last band (their
    * carry is then 0 and ignored). NULL = start from 0.0. */
   const double* carry;
+  /* L2 residency of the gathered vector: entries [0, hot_cols) are gathered
+   * with L2 evict_last, the rest with evict_first, so that when the vector
+   * is larger than L2 its most-used prefix stays resident (the engine's
+   * length-class order puts the highest-degree columns first). <= 0: every
+   * gather evict_last. Picks a cache policy, never a value. */
+  int64_t hot_cols;
 } gridlp_csr_t;
 
 /*
@@ -145,6 +151,7 @@ typedef struct gridlp_peer {
   int32_t group_size;
   int32_t my_slot;
   int64_t len;
+  int64_t timeout_ns;                /* consumer wait bound (collective_timeout_seconds); 0 = 120 s */
 } gridlp_peer_t;
 
 /*
@@ -226,6 +233,19 @@ int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes);
 int gridlp_enable_peer_access(int peer_device);
 /* Upper bound on the CTAs (reduction slots) an op over `src` launches. */
 int64_t gridlp_op_slots(const gridlp_src_t* src);
+/* Process-wide kernel knobs (no reference counterpart; results are
+ * bit-identical for every value — they pick kernels, not arithmetic):
+ *   "sell_variant"    0 = SELL lanes with LSU streams (one slice per warp,
+ *                     default), 1..4 = TMA-staged streams, persistent warps
+ *                     (stages x depth 8x2, 8x3, 16x2, 4x4), 5 = LSU streams
+ *                     issued one step block ahead of the gathers
+ *   "tma_ctas_per_sm" cap on resident CTAs of the TMA kernel (0 = occupancy)
+ *   "chain_products"  gridlp_pdhg_iterate chains its products by
+ *                     programmatic dependent launch (default 1)
+ * Unknown key or out-of-range value: GRIDLP_ERR_ARG. get returns -1 for an
+ * unknown key. */
+int gridlp_set_tuning(const char* key, int64_t value);
+int64_t gridlp_get_tuning(const char* key);
 
 /* --- products ------------------------------------------------------------ */
 /* out = sums(src). Replaces spmv (sparse_kernels.py:18-24) and

@@ -16,6 +16,7 @@ from .api import (
     solve,
     warmup,
 )
+from .comm import CollectiveError, CollectiveMismatch, CollectiveTimeout, WorkerError
 from .generators import GeneratorSpec, box_lp_optimum, generate
 from .layout import (
     GridTopology,
@@ -35,6 +36,7 @@ from .problem import LpProblem, SparseMatrix, objective_value, reported_objectiv
 __version__ = "0.1.0"
 
 __all__ = [
+    "CollectiveError", "CollectiveMismatch", "CollectiveTimeout", "WorkerError",
     "GeneratorSpec", "GridTopology", "KktReport", "LpProblem", "MpsParseError", "PartitionLayout",
     "Permutation", "SolveResult", "SolverConfig", "SparseMatrix", "StepSizes",
     "block_random_permutation", "box_lp_optimum", "build_layout", "generate",

@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import engine as eng
-from .comm import Ledger, NcclGrid, PeerGrid, VirtualGrid
+from .comm import CollectiveError, Ledger, NcclGrid, PeerGrid, VirtualGrid, WorkerError
 from .blocks import upload_csr
 from .layout import GridTopology, build_layout, layout_summary, unpermute_solution
 from .ops import CudaOps
@@ -300,14 +300,15 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
     if device is None:
         device = _device()
     if cfg.comm_backend in ("nccl", "peer") and not force_1x1:
-        comm = (PeerGrid if cfg.comm_backend == "peer" else NcclGrid)(R, C, device)
+        comm = (PeerGrid if cfg.comm_backend == "peer" else NcclGrid)(R, C, device, cfg.collective_timeout_seconds)
         if comm.world != R * C:
             raise ValueError(f"{cfg.comm_backend} backend needs world size == grid devices ({R * C}), "
                              f"got {comm.world}")
     else:
         comm = VirtualGrid(R, C)
-    engine = eng.PdhgEngine(problem, layout, opts, comm, ops_factory or CudaOps, device, 0.0, 0.0, 0.0,
-                            preload=preload)
+    with eng.nvtx_range("gridlp.setup_blocks"):
+        engine = eng.PdhgEngine(problem, layout, opts, comm, ops_factory or CudaOps, device, 0.0, 0.0, 0.0,
+                                preload=preload)
     del preload
     timings.update(engine.timings)
     timings["layout_order"] = engine.choices.get("order")
@@ -321,7 +322,8 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
         cnorm, bnorm = engine.band_scalars()
         engine.cnorm, engine.bnorm = cnorm, bnorm
     t0 = time.perf_counter()
-    estimate = engine.power_estimate(cfg.power_iterations, probe, cfg.seed)
+    with eng.nvtx_range("gridlp.power_iteration"):
+        estimate = engine.power_estimate(cfg.power_iterations, probe, cfg.seed)
     timings["power_s"] = time.perf_counter() - t0
     timings["estimate"] = estimate
     eta = eta_from_estimate(cfg, estimate)
@@ -344,7 +346,17 @@ def _solve(problem, cfg: SolverConfig, trace=None, force_1x1=False, ops_factory=
     comm = engine.comm
     setup_events = engine.ledger.snapshot()
     leader = (not comm.local) or comm.local[0] == (0, 0)
-    out = engine.run(eta, omega, trace=trace, log_hook=_log_pass if leader else None)
+    try:
+        out = engine.run(eta, omega, trace=trace, log_hook=_log_pass if leader else None)
+    except CollectiveError:
+        raise
+    except Exception as exc:
+        if comm.kind in ("nccl", "peer"):
+            # a device worker failed (reference solver_driver.py:215, comm.py:219-221)
+            raise WorkerError(f"device {comm.local} failed: {exc}") from exc
+        raise
+    if comm.kind in ("nccl", "peer"):
+        comm.agree(out["status"], "statuses")       # solver_driver.py:242-244
     timings.update(engine.timings)
     xy = engine.solution_original()
     if xy is None:

@@ -21,12 +21,32 @@ Executors:
 
 from __future__ import annotations
 
+import datetime
 from collections import Counter
 
 import numpy as np
 import torch
 
 AXES = ("R", "C", "G")
+
+
+class CollectiveError(RuntimeError):
+    """comm.py:45 of the reference."""
+
+
+class CollectiveTimeout(CollectiveError):
+    """A collective did not complete within collective_timeout_seconds
+    (reference comm.py:49, :125-132)."""
+
+
+class CollectiveMismatch(CollectiveError):
+    """Devices issued different collective sequences (reference comm.py:53,
+    the lockstep check :87-91, :309-320)."""
+
+
+class WorkerError(RuntimeError):
+    """A device worker raised; the original exception is chained
+    (reference comm.py:57, :219-221)."""
 
 
 class Ledger:
@@ -119,12 +139,15 @@ class NcclGrid:
 
     kind = "nccl"
 
-    def __init__(self, rows: int, cols: int, device):
+    def __init__(self, rows: int, cols: int, device, timeout: float = 120.0):
         import torch.distributed as dist
 
         if not dist.is_initialized():
             raise RuntimeError("NcclGrid needs an initialised torch.distributed process group")
         self.dist = dist
+        self.timeout = float(timeout)
+        self._td = datetime.timedelta(seconds=self.timeout)
+        self._seq = 0                  # host collectives issued (lockstep tag)
         self.rows, self.cols = rows, cols
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
@@ -134,10 +157,27 @@ class NcclGrid:
         self.active = self.rank < rows * cols
         self.coord = (self.rank // cols, self.rank % cols) if self.active else None
         self.local = [self.coord] if self.active else []
-        # every rank must create every group, in the same order
-        self.col_groups = [dist.new_group([i * cols + j for i in range(rows)]) for j in range(cols)]
-        self.row_groups = [dist.new_group([i * cols + j for j in range(cols)]) for i in range(rows)]
-        self.active_group = dist.new_group(list(range(rows * cols)))
+        # every rank must create every group, in the same order; the groups'
+        # own timeout bounds the device-side vector collectives (NCCL watchdog)
+        td = self._td
+        self.col_groups = [dist.new_group([i * cols + j for i in range(rows)], timeout=td) for j in range(cols)]
+        self.row_groups = [dist.new_group([i * cols + j for j in range(cols)], timeout=td) for i in range(rows)]
+        self.active_group = dist.new_group(list(range(rows * cols)), timeout=td)
+        # NCCL collectives can be captured in CUDA graphs; gloo (ranks sharing
+        # a GPU in tests, CPU runs) cannot
+        self.graph_safe = dist.get_backend() == "nccl"
+
+    def _wait(self, work, what: str):
+        """Host-side wait on a collective, bounded by collective_timeout_seconds:
+        a rank that died or stopped issuing collectives surfaces here as the
+        reference's CollectiveTimeout instead of a hang."""
+        try:
+            ok = work.wait(timeout=self._td)
+        except Exception as exc:   # torch raises on timeout / a failed peer
+            raise CollectiveTimeout(f"collective {what} timed out after {self.timeout}s or failed on a peer: "
+                                    f"{exc}") from exc
+        if ok is False:
+            raise CollectiveTimeout(f"collective {what} timed out after {self.timeout}s")
 
     def reduce(self, axis, index, partials, scratch=None):
         (p,) = partials
@@ -147,15 +187,71 @@ class NcclGrid:
             self.dist.all_reduce(buf, group=group)
         return [buf]
 
+    def _axis_group(self, axis, index):
+        return self.col_groups[index] if axis == "R" else self.row_groups[index]
+
+    def _gloo_cuda(self, group, t) -> bool:
+        return t.is_cuda and self.dist.get_backend(group) == "gloo"
+
+    def exchange(self, axis, index, partial, recv):
+        """Ordered reduce-scatter, first half: recv[q*S:(q+1)*S] = member q's
+        partial of this rank's shard (all-to-all over the axis group; the
+        consuming epilogue adds the slices in ascending q)."""
+        group = self._axis_group(axis, index)
+        if self._gloo_cuda(group, partial):
+            # gloo has no all-to-all on CUDA tensors (ranks sharing one GPU in
+            # tests): all-gather the full partials and keep this rank's shard
+            G = self.rows if axis == "R" else self.cols
+            me = self.coord[0] if axis == "R" else self.coord[1]
+            S = partial.numel() // G
+            outs = [torch.empty_like(partial) for _ in range(G)]
+            self.dist.all_gather(outs, partial, group=group)
+            for q in range(G):
+                recv[q * S:(q + 1) * S].copy_(outs[q][me * S:(me + 1) * S])
+            return
+        self.dist.all_to_all_single(recv, partial, group=group)
+
+    def gather_shard(self, axis, index, vec, me, S):
+        """All-gather this rank's shard [me*S, (me+1)*S) of `vec` (a view of
+        storage padded to G*S) into every member's copy, in place."""
+        group = self._axis_group(axis, index)
+        G = self.rows if axis == "R" else self.cols
+        full = torch.as_strided(vec, (G * S,), (1,))      # the padded storage behind the view
+        mine = full[me * S:(me + 1) * S]
+        if self._gloo_cuda(group, full):
+            outs = [torch.empty_like(mine) for _ in range(G)]
+            self.dist.all_gather(outs, mine.contiguous(), group=group)
+            for q in range(G):
+                if q != me:
+                    full[q * S:(q + 1) * S].copy_(outs[q])
+            return
+        self.dist.all_gather_into_tensor(full, mine, group=group)
+
     def table(self, local_rows: dict) -> dict:
-        """All-gather each active rank's scalar row over the active group."""
+        """All-gather each active rank's scalar row over the active group.
+        Each row carries this rank's host-collective sequence number and row
+        width; ranks that disagree issued different collective sequences
+        (CollectiveMismatch, the reference's lockstep check)."""
         (coord, row), = local_rows.items()
         row = np.asarray(row, dtype=np.float64)
-        t = torch.as_tensor(row, device=self.device)
+        self._seq += 1
+        tagged = np.concatenate([[float(self._seq), float(len(row))], row])
+        t = torch.as_tensor(tagged, device=self.device)
         outs = [torch.empty_like(t) for _ in range(self.rows * self.cols)]
-        self.dist.all_gather(outs, t, group=self.active_group)
+        self._wait(self.dist.all_gather(outs, t, group=self.active_group, async_op=True), f"table#{self._seq}")
         full = torch.stack(outs).cpu().numpy()
-        return {(r // self.cols, r % self.cols): full[r] for r in range(self.rows * self.cols)}
+        if not (np.all(full[:, 0] == full[0, 0]) and np.all(full[:, 1] == full[0, 1])):
+            raise CollectiveMismatch(f"collective sequences diverged: (seq, width) per rank "
+                                     f"{[(int(a), int(b)) for a, b in full[:, :2]]}")
+        return {(r // self.cols, r % self.cols): full[r, 2:] for r in range(self.rows * self.cols)}
+
+    def agree(self, value: str, what: str) -> None:
+        """Raise RuntimeError when ranks hold different values of a replicated
+        decision (solver_driver.py:242-244: diverged device statuses)."""
+        got = [None] * (self.rows * self.cols)
+        self.dist.all_gather_object(got, value, group=self.active_group)
+        if len(set(got)) != 1:
+            raise RuntimeError(f"device {what} diverged: {set(got)}")
 
     def gather_vectors(self, local: dict, lengths: dict, device) -> dict:
         """{coord: tensor} of every active rank (padded all_gather)."""
@@ -164,7 +260,7 @@ class NcclGrid:
         buf = torch.zeros(width, dtype=torch.float64, device=self.device)
         buf[: vec.numel()] = vec
         outs = [torch.empty_like(buf) for _ in range(self.rows * self.cols)]
-        self.dist.all_gather(outs, buf, group=self.active_group)
+        self._wait(self.dist.all_gather(outs, buf, group=self.active_group, async_op=True), "gather_vectors")
         return {(r // self.cols, r % self.cols): outs[r][: lengths[(r // self.cols, r % self.cols)]]
                 for r in range(self.rows * self.cols)}
 
@@ -178,7 +274,7 @@ class PeerAxis:
     scratch, plus the IPC mappings of every group member's buffer and
     counter, packed as the C struct gridlp_peer_t."""
 
-    def __init__(self, dist, group, members: list, my_slot: int, length: int, device):
+    def __init__(self, dist, group, members: list, my_slot: int, length: int, device, timeout: float = 120.0):
         from torch.multiprocessing.reductions import reduce_tensor
 
         from . import native
@@ -207,6 +303,7 @@ class PeerAxis:
         c.recv, c.my_flag = self.recv.data_ptr(), self.flag.data_ptr()
         c.epoch, c.cta_count = self.epoch.data_ptr(), self.cta_count.data_ptr()
         c.group_size, c.my_slot, c.len = G, my_slot, length
+        c.timeout_ns = int(timeout * 1e9)
         self.struct = c
         self.length = length
 
@@ -218,8 +315,8 @@ class PeerGrid(NcclGrid):
 
     kind = "peer"
 
-    def __init__(self, rows: int, cols: int, device):
-        super().__init__(rows, cols, device)
+    def __init__(self, rows: int, cols: int, device, timeout: float = 120.0):
+        super().__init__(rows, cols, device, timeout)
         self.axes = {}
 
     def setup_axes(self, row_len: int, col_len: int):
@@ -232,11 +329,13 @@ class PeerGrid(NcclGrid):
         for ii in range(self.rows):
             members = [ii * self.cols + jj for jj in range(self.cols)]
             if ii == i:
-                self.axes["C"] = PeerAxis(self.dist, self.row_groups[ii], members, j, row_len, self.device)
+                self.axes["C"] = PeerAxis(self.dist, self.row_groups[ii], members, j, row_len, self.device,
+                                          self.timeout)
         for jj in range(self.cols):
             members = [ii * self.cols + jj for ii in range(self.rows)]
             if jj == j:
-                self.axes["R"] = PeerAxis(self.dist, self.col_groups[jj], members, i, col_len, self.device)
+                self.axes["R"] = PeerAxis(self.dist, self.col_groups[jj], members, i, col_len, self.device,
+                                          self.timeout)
 
     def reduce(self, axis, index, partials, scratch=None):
         raise RuntimeError("PeerGrid sums inside the kernels; reduce() is never called")

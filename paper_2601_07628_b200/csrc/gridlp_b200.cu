@@ -119,6 +119,23 @@ __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
   return v;
 }
 
+// coherent read-once load (the thread rewrites the element later), first to leave L2
+__device__ __forceinline__ double ld_once(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+// gather policy of column c: the hot prefix [0, hot) stays in L2
+__device__ __forceinline__ uint64_t gather_policy(int64_t c, int64_t hot, uint64_t pl, uint64_t pf) {
+  return c < hot ? pl : pf;
+}
+__device__ __forceinline__ int64_t hot_limit(const gridlp_csr_t& A) {
+  return A.hot_cols > 0 ? A.hot_cols : (int64_t)0x7fffffffffffffffLL;
+}
+
 // ------------------------------------------- programmatic dependent launch
 // The heavy-chunk, long-row and SELL kernels of one product touch disjoint
 // rows, so each lets the next one start as soon as SM slots free up
@@ -220,22 +237,28 @@ struct OpPrimal {
   int32_t iter;
   bool halpern;
   double tau, gamma, wm, wa;
+  uint64_t pf;
   struct Data { double x, c, lo, hi, x0; };
   __device__ void prepare() {
     tau = step->tau;
     gamma = step->gamma;
     halpern_weights(gamma, step->inner_k + iter, wm, wa);
+    pf = policy_evict_first();
   }
+  // read-once operands and the x rewrite leave L2 first (the gathered
+  // vectors' hot prefix stays); x_bar keeps the normal policy: it is the
+  // next product's gather vector
   __device__ Data load(int64_t r) const {
     Data d;
-    d.x = x[r]; d.c = c[r]; d.lo = lo[r]; d.hi = hi[r];
-    d.x0 = halpern ? x0[r] : 0.0;
+    d.x = ld_once(x + r, pf); d.c = ld_stream(c + r, pf); d.lo = ld_stream(lo + r, pf);
+    d.hi = ld_stream(hi + r, pf);
+    d.x0 = halpern ? ld_stream(x0 + r, pf) : 0.0;
     return d;
   }
   __device__ void row(int64_t r, double aty, const Data& d, double*) const {
     const double xh = np_clip(dsub(d.x, dmul(tau, dsub(d.c, aty))), d.lo, d.hi);
     xbar[r] = dsub(dmul(2.0, xh), d.x);
-    x[r] = halpern ? halpern_mix(xh, d.x, d.x0, wm, gamma, wa) : xh;
+    st_hint(x + r, halpern ? halpern_mix(xh, d.x, d.x0, wm, gamma, wa) : xh, pf);
   }
 };
 
@@ -255,16 +278,20 @@ struct OpDual {
   int32_t iter;
   bool halpern;
   double sigma, gamma, wm, wa;
+  uint64_t pf;
   struct Data { double y, lo, hi, y0; };
   __device__ void prepare() {
     sigma = step->sigma;
     gamma = step->gamma;
     halpern_weights(gamma, step->inner_k + iter, wm, wa);
+    pf = policy_evict_first();
   }
+  // y is the next product's gather vector (normal policy); bounds and
+  // anchor are read once
   __device__ Data load(int64_t r) const {
     Data d;
-    d.y = y[r]; d.lo = lo[r]; d.hi = hi[r];
-    d.y0 = halpern ? y0[r] : 0.0;
+    d.y = y[r]; d.lo = ld_stream(lo + r, pf); d.hi = ld_stream(hi + r, pf);
+    d.y0 = halpern ? ld_stream(y0 + r, pf) : 0.0;
     return d;
   }
   __device__ void row(int64_t r, double z, const Data& d, double*) const {
@@ -451,9 +478,14 @@ __device__ __forceinline__ void product_cta_done(const Op& op) {
   if constexpr (HasCtaDone<Op>::value) op.cta_done();
 }
 
-#ifndef GRIDLP_PEER_WAIT_CYCLES
-#define GRIDLP_PEER_WAIT_CYCLES (60LL * 2000000000LL)   // ~60 s at 2 GHz
+#ifndef GRIDLP_PEER_WAIT_NS
+#define GRIDLP_PEER_WAIT_NS (120ull * 1000000000ull)   // default peer-wait bound: 120 s
 #endif
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int SELL_WPB = 2;          // warps (slices) per CTA
 constexpr int SELL_NT = SELL_WPB * 32;
 constexpr int SELL_U = 4;            // steps in flight per lane
@@ -483,14 +515,14 @@ __device__ __forceinline__ void emit_row(const Op& op, int64_t r, double s, cons
   op.row(r, s, d, acc);
 }
 
-// Deterministic per-CTA reduction of a SELL_NT-thread CTA: warp tree, then
-// warps in order, one slot per CTA.
-template <class Op>
-__device__ __forceinline__ void cta_partials(double (&acc)[Op::NRED > 0 ? Op::NRED : 1], double* partials) {
+// Deterministic per-CTA reduction of a WPB-warp CTA: warp tree, then warps
+// in order, one slot per CTA.
+template <class Op, int WPB>
+__device__ __forceinline__ void cta_partials_n(double (&acc)[Op::NRED > 0 ? Op::NRED : 1], double* partials) {
   if constexpr (Op::NRED > 0) {
     if (!partials) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ double rs[Op::NRED][SELL_WPB];
+    __shared__ double rs[Op::NRED][WPB];
 #pragma unroll
     for (int q = 0; q < Op::NRED; ++q) {
       const double v = warp_sum(acc[q]);
@@ -501,11 +533,15 @@ __device__ __forceinline__ void cta_partials(double (&acc)[Op::NRED > 0 ? Op::NR
 #pragma unroll
       for (int q = 0; q < Op::NRED; ++q) {
         double t = rs[q][0];
-        for (int w = 1; w < SELL_WPB; ++w) t = dadd(t, rs[q][w]);
+        for (int w = 1; w < WPB; ++w) t = dadd(t, rs[q][w]);
         partials[(int64_t)blockIdx.x * GRIDLP_MAX_RED + q] = t;
       }
     }
   }
+}
+template <class Op>
+__device__ __forceinline__ void cta_partials(double (&acc)[Op::NRED > 0 ? Op::NRED : 1], double* partials) {
+  cta_partials_n<Op, SELL_WPB>(acc, partials);
 }
 
 // Heavy rows, one CTA per chunk of GRIDLP_HEAVY_CHUNK entries: strided
@@ -515,9 +551,11 @@ __device__ __forceinline__ void cta_partials(double (&acc)[Op::NRED > 0 ? Op::NR
 // reduction partials occupy slots [0, num_chunks).
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
-                                                              double* __restrict__ partials, double* __restrict__ terms) {
+                                                              double* __restrict__ partials, double* __restrict__ terms,
+                                                              int cross_wait) {
   constexpr int U = SELL_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  if (cross_wait) pdl_wait();     // chained to the previous product (see launch_op)
   pdl_launch_dependents();
   double acc[NR];
 #pragma unroll
@@ -525,6 +563,7 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
+  const int64_t hot = hot_limit(A);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int64_t c = blockIdx.x;
@@ -545,7 +584,8 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
       vv[u] = k < p1 ? ld_stream(A.long_vals + k, pf) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) xx[u] = k0 + (int64_t)u * SELL_NT < p1 ? ld_gather(g + cc[u], pl) : 0.0;
+    for (int u = 0; u < U; ++u)
+      xx[u] = k0 + (int64_t)u * SELL_NT < p1 ? ld_gather(g + cc[u], gather_policy(cc[u], hot, pl, pf)) : 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k0 + (int64_t)u * SELL_NT < p1) s = dadd(s, dmul(vv[u], xx[u]));
@@ -593,11 +633,13 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
 // add latency per entry. Reduction partials follow the heavy kernel's.
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
-                                                           double* __restrict__ partials, double* __restrict__ terms) {
+                                                           double* __restrict__ partials, double* __restrict__ terms,
+                                                           int cross_wait) {
   constexpr int U = LONG_U;
   constexpr int B = 32 * U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   __shared__ double prod[SELL_WPB][B];
+  if (cross_wait) pdl_wait();
   pdl_launch_dependents();
   double acc[NR];
 #pragma unroll
@@ -605,6 +647,7 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
+  const int64_t hot = hot_limit(A);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t q = (int64_t)blockIdx.x * SELL_WPB + warp;
   if (q < A.num_exact_long) {
@@ -624,7 +667,8 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
       vb[u] = k2 < len ? ld_stream(vp + k2, pf) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) x[u] = 32 * u + lane < len ? ld_gather(g + ca[u], pl) : 0.0;
+    for (int u = 0; u < U; ++u)
+      x[u] = 32 * u + lane < len ? ld_gather(g + ca[u], gather_policy(ca[u], hot, pl, pf)) : 0.0;
     double s = A.carry ? ld_carry(A.carry + A.long_rows[h], pf) : 0.0;   // column bands: continue the chain
     for (int j0 = 0; j0 < len; j0 += B) {
       double p[U];
@@ -637,7 +681,7 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
       // in flight during the add chain: gathers of block j0+B, streams of block j0+2B
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        x[u] = j0 + B + 32 * u + lane < len ? ld_gather(g + cb[u], pl) : 0.0;
+        x[u] = j0 + B + 32 * u + lane < len ? ld_gather(g + cb[u], gather_policy(cb[u], hot, pl, pf)) : 0.0;
         ca[u] = cb[u];
         va[u] = vb[u];
         const int k = j0 + 2 * B + 32 * u + lane;
@@ -669,9 +713,13 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t A, const double* __restrict__ g,
                                                                    Op op, double* __restrict__ partials,
-                                                                   double* __restrict__ terms) {
+                                                                   double* __restrict__ terms, int cross_wait) {
   constexpr int U = SELL_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  if (cross_wait) pdl_wait();
+  // the next product's first kernel may start on SM slots this one frees; it
+  // waits for this grid's completion before touching anything it writes
+  pdl_launch_dependents();
   double acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
@@ -680,6 +728,7 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
+  const int64_t hot = hot_limit(A);
   const int64_t slice = (int64_t)blockIdx.x * SELL_WPB + warp;
   if (slice < A.num_slices) {
     // lane = row & 31 (sell_plan): the lane's sum is its own row's
@@ -701,7 +750,8 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
           v[u] = ok ? ld_stream(vp + 32 * (j + u), pf) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = (j + u < len) ? ld_gather(g + c[u], pl) : 0.0;
+        for (int u = 0; u < U; ++u)
+        x[u] = (j + u < len) ? ld_gather(g + c[u], gather_policy(c[u], hot, pl, pf)) : 0.0;
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
@@ -711,6 +761,85 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
       const typename Op::Data d = op.load(r);
       emit_row(op, r, s, d, acc, terms, A.num_rows);
     }
+  }
+  cta_partials<Op>(acc, partials);
+  product_cta_done(op);
+  pdl_wait();
+}
+
+// Software-pipelined SELL lanes: the same lane-owns-row sum as
+// sell32_kernel, but the column/value streams of step block j+U are issued
+// before the gathers of block j are consumed, so each block costs one memory
+// round trip (the gathers) instead of two (streams, then the gathers that
+// depend on them). More registers (fewer warps per SM): it pays on long
+// lanes whose streams miss L2 (power-law rows), not on short ones.
+constexpr int PIPE_MINB = 20;        // 40 warps per SM at <= 51 registers
+template <class Op>
+__global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
+                                                                        Op op, double* __restrict__ partials,
+                                                                        double* __restrict__ terms, int cross_wait) {
+  constexpr int U = SELL_U;
+  constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t slice = (int64_t)blockIdx.x * SELL_WPB + warp;
+  const uint64_t pf = policy_evict_first();
+  int info = -1, len = 0;
+  const int* __restrict__ cp = nullptr;
+  const double* __restrict__ vp = nullptr;
+  int c[U];
+  double v[U];
+  if (slice < A.num_slices) {
+    info = A.lane_info[slice * 32 + lane];
+    len = info >= 0 ? info >> 8 : 0;
+    const int64_t base = (int64_t)A.slice_off[slice] + lane;
+    cp = A.sell_cols + base;
+    vp = A.sell_vals + base;
+  }
+  // the first block's streams are constant matrix data: issued before the
+  // wait on a chained predecessor product
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool ok = u < len;
+    c[u] = ok ? ld_stream(cp + 32 * u, pf) : 0;
+    v[u] = ok ? ld_stream(vp + 32 * u, pf) : 0.0;
+  }
+  if (cross_wait) pdl_wait();
+  pdl_launch_dependents();
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+  op.prepare();
+  const uint64_t pl = policy_evict_last();
+  const int64_t hot = hot_limit(A);
+  if (info >= 0) {
+    const int64_t r = slice * 32 + lane;
+    double s = A.carry ? ld_carry(A.carry + r, pf) : 0.0;   // column bands: continue the chain
+    for (int j = 0; j < len; j += U) {
+      double x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        x[u] = (j + u < len) ? ld_gather(g + c[u], gather_policy(c[u], hot, pl, pf)) : 0.0;
+      int cn[U];
+      double vn[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = j + U + u;
+        const bool ok = k < len;
+        cn[u] = ok ? ld_stream(cp + 32 * k, pf) : 0;
+        vn[u] = ok ? ld_stream(vp + 32 * k, pf) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        c[u] = cn[u];
+        v[u] = vn[u];
+      }
+    }
+    const typename Op::Data d = op.load(r);
+    emit_row(op, r, s, d, acc, terms, A.num_rows);
   }
   cta_partials<Op>(acc, partials);
   product_cta_done(op);
@@ -732,14 +861,16 @@ __global__ void __launch_bounds__(TPB) rows_kernel(gridlp_src_t src, int64_t n, 
     const uint32_t e = *pe.epoch;
     if (threadIdx.x == 0) {
       const uint32_t target = (e + 1u) * (uint32_t)pe.group_size;
-      const long long t0 = clock64();
+      const uint64_t limit = pe.timeout_ns > 0 ? (uint64_t)pe.timeout_ns : GRIDLP_PEER_WAIT_NS;
+      const uint64_t t0 = global_ns();
       uint32_t v;
       while (true) {
         asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(pe.my_flag) : "memory");
         if ((int32_t)(v - target) >= 0) break;
-        // a member that never arrives is a bug or a dead peer: fail the launch
-        // (cudaErrorLaunchFailure) instead of hanging the device
-        if (clock64() - t0 > GRIDLP_PEER_WAIT_CYCLES) __trap();
+        // a member that never arrives within collective_timeout_seconds is a
+        // dead or diverged peer: fail the launch (cudaErrorLaunchFailure, the
+        // host maps it to CollectiveTimeout) instead of hanging the device
+        if (global_ns() - t0 > limit) __trap();
         __nanosleep(256);
       }
     }
@@ -843,35 +974,64 @@ int check_csr(const gridlp_csr_t* A) {
 
 int64_t long_blocks(const gridlp_csr_t* A) { return (A->num_exact_long + SELL_WPB - 1) / SELL_WPB; }
 
+// ---- light-row kernel variant (gridlp_set_tuning "sell_variant"):
+//  0 = sell32_kernel, 1 = sell32_pipe_kernel (streams one step block ahead).
+// (TMA-staged streams with persistent warps were measured 1.9-2.3x slower on
+// cfg2 / cfg3 and removed: profiles/r2/ncu_cfg2_tma_8x2_dual_rejected.md.)
+int g_sell_variant = 1;
+int g_chain_products = 1;           // pdhg_iterate: programmatic launch between products
+
+int64_t light_blocks(const gridlp_csr_t* A) {
+  return A->num_slices > 0 ? (A->num_slices + SELL_WPB - 1) / SELL_WPB : 0;
+}
+
+// CTAs (= reduction slots) of one product
 int64_t sell_blocks(const gridlp_csr_t* A) {
-  return A->num_rows > 0 ? A->num_chunks + long_blocks(A) + (A->num_slices + SELL_WPB - 1) / SELL_WPB : 0;
+  return A->num_rows > 0 ? A->num_chunks + long_blocks(A) + light_blocks(A) : 0;
 }
 
 int64_t src_rows(const gridlp_src_t* src) { return src->A ? src->A->num_rows : src->num_rows; }
 
-// Launch one of a product's kernels; `after_sibling` marks a programmatic
-// dependency on the previous kernel of the same product (see pdl_wait).
-template <class Op>
-cudaError_t launch_part(void (*kern)(gridlp_csr_t, const double*, Op, double*, double*), int64_t blocks,
-                        bool after_sibling, cudaStream_t s, const gridlp_csr_t& M, const double* gather, Op op,
-                        double* partials, double* terms) {
+// Launch one of a product's kernels. `programmatic` marks a programmatic
+// dependency on the previous kernel in the stream: a sibling of the same
+// product (disjoint rows; the kernel waits for it only at its end), or —
+// with cross_wait — the last kernel of the previous product, which the
+// kernel waits for before its first dependent access.
+template <class K, class Op>
+cudaError_t launch_part(K kern, int64_t blocks, int threads, int smem, bool programmatic, int cross_wait,
+                        cudaStream_t s, const gridlp_csr_t& M, const double* gather, Op op, double* partials,
+                        double* terms) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3((unsigned)blocks);
-  cfg.blockDim = dim3(SELL_NT);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  if (after_sibling) {
+  if (programmatic) {
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, kern, M, gather, op, partials, terms);
+  return cudaLaunchKernelEx(&cfg, kern, M, gather, op, partials, terms, cross_wait);
 }
 
 template <class Op>
+cudaError_t launch_light(int64_t blocks, bool programmatic, int cross_wait, cudaStream_t s, const gridlp_csr_t& M,
+                         const double* gather, Op op, double* partials, double* terms) {
+  if (g_sell_variant == 1)
+    return launch_part(&sell32_pipe_kernel<Op>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
+                       partials, terms);
+  return launch_part(&sell32_kernel<Op>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op, partials,
+                     terms);
+}
+
+// One op. `cross`: the product's first kernel is chained to the previous
+// product on the stream by programmatic dependent launch (pdhg_iterate only:
+// there the previous kernel is always the last kernel of a product).
+template <class Op>
 int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* stream,
-              const char* name) {
+              const char* name, bool cross = false) {
   if (!src) return fail(GRIDLP_ERR_ARG, std::string(name) + ": null source");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n = src_rows(src);
@@ -920,20 +1080,24 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
       const gridlp_csr_t& M = *src->A;
       const int64_t nlong = long_blocks(&M);
       const int64_t nlight = slots - M.num_chunks - nlong;
-      bool prev = false;
+      bool prev = cross;           // programmatic edge to the previous kernel
+      int cw = cross ? 1 : 0;      // the first kernel launched waits for the previous product
       cudaError_t e = cudaSuccess;
       if (M.num_chunks > 0) {
-        e = launch_part(heavy_chunk_kernel<Op>, M.num_chunks, prev, s, M, src->gather, op, kpartials, terms);
+        e = launch_part(&heavy_chunk_kernel<Op>, M.num_chunks, SELL_NT, 0, prev, cw, s, M, src->gather, op,
+                        kpartials, terms);
         prev = true;
+        cw = 0;
       }
       if (e == cudaSuccess && nlong > 0) {
-        e = launch_part(long_row_kernel<Op>, nlong, prev, s, M, src->gather, op,
+        e = launch_part(&long_row_kernel<Op>, nlong, SELL_NT, 0, prev, cw, s, M, src->gather, op,
                         kpartials ? kpartials + M.num_chunks * GRIDLP_MAX_RED : nullptr, terms);
         prev = true;
+        cw = 0;
       }
       if (e == cudaSuccess && nlight > 0)
-        e = launch_part(sell32_kernel<Op>, nlight, prev, s, M, src->gather, op,
-                        kpartials ? kpartials + (M.num_chunks + nlong) * GRIDLP_MAX_RED : nullptr, terms);
+        e = launch_light(nlight, prev, cw, s, M, src->gather, op,
+                         kpartials ? kpartials + (M.num_chunks + nlong) * GRIDLP_MAX_RED : nullptr, terms);
       if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
     } else
       rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials,
@@ -1006,6 +1170,28 @@ int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes) {
   return GRIDLP_OK;
 }
 
+int gridlp_set_tuning(const char* key, int64_t value) {
+  if (!key) return fail(GRIDLP_ERR_ARG, "set_tuning: null key");
+  const std::string k(key);
+  if (k == "sell_variant") {
+    if (value < 0 || value > 1) return fail(GRIDLP_ERR_ARG, "set_tuning: sell_variant must be 0 or 1");
+    g_sell_variant = (int)value;
+  } else if (k == "chain_products") {
+    g_chain_products = value != 0;
+  } else {
+    return fail(GRIDLP_ERR_ARG, "set_tuning: unknown key " + k);
+  }
+  return GRIDLP_OK;
+}
+
+int64_t gridlp_get_tuning(const char* key) {
+  if (!key) return -1;
+  const std::string k(key);
+  if (k == "sell_variant") return g_sell_variant;
+  if (k == "chain_products") return g_chain_products;
+  return -1;
+}
+
 int64_t gridlp_op_slots(const gridlp_src_t* src) {
   if (!src) return 0;
   if (src->A) return sell_blocks(src->A);
@@ -1040,24 +1226,40 @@ int gridlp_op_store_peer(const gridlp_src_t* src, const gridlp_peer_t* peer, dou
   return launch_op(src, op, nullptr, stream, "op_store_peer");
 }
 
-int gridlp_op_primal(const gridlp_src_t* src, const gridlp_primal_t* pv, const gridlp_step_t* d_step,
-                     int32_t iter, uint32_t flags, void* stream) {
+}  // extern "C"
+
+namespace {
+int op_primal(const gridlp_src_t* src, const gridlp_primal_t* pv, const gridlp_step_t* d_step, int32_t iter,
+              uint32_t flags, void* stream, bool cross) {
   if (!pv || !d_step) return fail(GRIDLP_ERR_ARG, "op_primal: null argument");
   if (src && src_rows(src) != pv->n) return fail(GRIDLP_ERR_ARG, "op_primal: length mismatch");
   OpPrimal op{};
   op.x = pv->x; op.xbar = pv->x_bar; op.x0 = pv->x_anchor; op.c = pv->c; op.lo = pv->lo; op.hi = pv->hi;
   op.step = d_step; op.iter = iter; op.halpern = (flags & GRIDLP_F_HALPERN) != 0;
-  return launch_op(src, op, nullptr, stream, "op_primal");
+  return launch_op(src, op, nullptr, stream, "op_primal", cross);
 }
 
-int gridlp_op_dual(const gridlp_src_t* src, const gridlp_dual_t* dv, const gridlp_step_t* d_step,
-                   int32_t iter, uint32_t flags, void* stream) {
+int op_dual(const gridlp_src_t* src, const gridlp_dual_t* dv, const gridlp_step_t* d_step, int32_t iter,
+            uint32_t flags, void* stream, bool cross) {
   if (!dv || !d_step) return fail(GRIDLP_ERR_ARG, "op_dual: null argument");
   if (src && src_rows(src) != dv->m) return fail(GRIDLP_ERR_ARG, "op_dual: length mismatch");
   OpDual op{};
   op.y = dv->y; op.y0 = dv->y_anchor; op.lo = dv->lo; op.hi = dv->hi;
   op.step = d_step; op.iter = iter; op.halpern = (flags & GRIDLP_F_HALPERN) != 0;
-  return launch_op(src, op, nullptr, stream, "op_dual");
+  return launch_op(src, op, nullptr, stream, "op_dual", cross);
+}
+}  // namespace
+
+extern "C" {
+
+int gridlp_op_primal(const gridlp_src_t* src, const gridlp_primal_t* pv, const gridlp_step_t* d_step,
+                     int32_t iter, uint32_t flags, void* stream) {
+  return op_primal(src, pv, d_step, iter, flags, stream, false);
+}
+
+int gridlp_op_dual(const gridlp_src_t* src, const gridlp_dual_t* dv, const gridlp_step_t* d_step,
+                   int32_t iter, uint32_t flags, void* stream) {
+  return op_dual(src, dv, d_step, iter, flags, stream, false);
 }
 
 int gridlp_op_kkt_rows(const gridlp_src_t* src, const gridlp_dual_t* dv, double* ax,
@@ -1137,10 +1339,16 @@ int gridlp_pdhg_iterate(const gridlp_src_t* primal_src, const gridlp_primal_t* p
     return fail(GRIDLP_ERR_ARG, "pdhg_iterate: bad argument");
   if (!primal_src->A || !dual_src->A)
     return fail(GRIDLP_ERR_ARG, "pdhg_iterate: needs fused sources (single-block axes)");
+  // every product after the first is chained to its predecessor by
+  // programmatic dependent launch (launch_op `cross`): its CTAs take SM slots
+  // as the predecessor's tail frees them, stage their matrix streams, and
+  // wait for the predecessor's completion before the first gather
+  const bool chain = g_chain_products && primal_src->A->num_rows > 0 && primal_src->A->nnz > 0 &&
+                     dual_src->A->num_rows > 0 && dual_src->A->nnz > 0;
   for (int32_t t = 0; t < n_iters; ++t) {
-    int rc = gridlp_op_primal(primal_src, pv, d_step, t, flags, stream);
+    int rc = op_primal(primal_src, pv, d_step, t, flags, stream, chain && t > 0);
     if (rc) return rc;
-    rc = gridlp_op_dual(dual_src, dv, d_step, t, flags, stream);
+    rc = op_dual(dual_src, dv, d_step, t, flags, stream, chain);
     if (rc) return rc;
   }
   return n_iters > 0 ? gridlp_op_step_advance(d_step, n_iters, stream) : GRIDLP_OK;

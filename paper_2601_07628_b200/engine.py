@@ -22,6 +22,7 @@ pdhg_engine.py:405-462 does, with the same collective ledger.
 
 from __future__ import annotations
 
+import dataclasses
 import logging
 import math
 import time
@@ -92,12 +93,25 @@ class EngineOptions:
     column_bands: int | None = None
     band_bytes: int = 48 << 20
     device_setup: bool = True
+    # gathered vectors larger than this many bytes keep only their first
+    # hot_gather_bytes (the highest-degree columns / longest rows in the
+    # length-class order) at L2 evict_last; the rest is gathered evict_first
+    # (gridlp_csr_t.hot_cols). 0 = every gather evict_last. Cache policy
+    # only: results are unchanged.
+    hot_gather_bytes: int = 64 << 20
     use_graphs: bool = True
-    # capture the NCCL executor's iterations (kernels + NCCL allreduces) in a
-    # CUDA graph too; opt-in until it has run on a multi-GPU box (this round
-    # had one GPU): the eager path is the default there
-    graph_nccl: bool = False
+    # capture the NCCL executor's iterations (kernels + NCCL collectives) in
+    # a CUDA graph too, as the single-GPU and peer executors do
+    graph_nccl: bool = True
     graph_chunk: int = 128
+    # NCCL executor, main loop: each axis sum is an ordered reduce-scatter
+    # (all-to-all of the partial shards, then the epilogue adds the G member
+    # slices in ascending order — the reference's order, comm.py:75-84) and
+    # the epilogue runs on this rank's 1/G shard only; the updated x_bar / y
+    # shard is all-gathered. Same NVLink bytes as an allreduce, 1/G of the
+    # epilogue bytes, bit-identical to the virtual grid. False: allreduce
+    # (NCCL's order) + replicated epilogue.
+    nccl_sharded: bool = True
 
 
 @dataclass
@@ -129,6 +143,22 @@ class RowState:
 
 
 @dataclass
+class ShardPlan:
+    """One axis sum of the sharded NCCL executor (PdhgEngine._shard_plan)."""
+
+    axis: str
+    index: int
+    src: object          # Fused product of the local block
+    partial: torch.Tensor
+    recv: torch.Tensor
+    final: object        # Parts over the G received slices of this rank's shard
+    state: object        # ColState / RowState view of the shard
+    me: int
+    S: int
+    G: int
+
+
+@dataclass
 class BlockState:
     i: int
     j: int
@@ -148,6 +178,25 @@ class Report:
     @property
     def overall(self) -> float:
         return max(self.r_primal, self.r_dual, self.r_gap)
+
+
+class nvtx_range:
+    """NVTX range around a solve phase (setup, power iteration, iterations,
+    KKT pass), visible to ncu --nvtx / nsys; nothing when CUDA is absent."""
+
+    def __init__(self, name: str):
+        self.name = name
+        self.on = torch.cuda.is_available()
+
+    def __enter__(self):
+        if self.on:
+            torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            torch.cuda.nvtx.range_pop()
+        return False
 
 
 def gap_residual(p: float, d: float) -> float:
@@ -276,6 +325,16 @@ class PdhgEngine:
         local = self.comm.local
         self.local_cols = sorted({j for _, j in local})
         self.local_rows = sorted({i for i, _ in local})
+        self.sharded = (self.comm.kind == "nccl" and self.opts.nccl_sharded and hasattr(self.comm, "exchange")
+                        and (self.R > 1 or self.C > 1))
+
+        def padded(length, group):
+            """zeros(length) as a view of storage padded to group * ceil(length / group)
+            (the all-gather of the shards writes into it in place)"""
+            if not self.sharded or group <= 1:
+                return torch.zeros(length, **f64)
+            S = -(-length // group)
+            return torch.zeros(max(group * S, 1), **f64)[:length]
         self.cols, self.rows, self.blocks = {}, {}, {}
         for j in self.local_cols:
             c0, c1 = lay.col_range(j)
@@ -291,8 +350,8 @@ class PdhgEngine:
                 cj, lj, hj, _ = problem.bands.col_data(c0, c1)
                 t = lambda a: a  # noqa: E731
                 obj, vlo, vhi = cj, lj, hj
-            self.cols[j] = ColState(j, n, t(obj), t(vlo), t(vhi), torch.zeros(n, **f64),
-                                    torch.zeros(n, **f64), torch.zeros(n, **f64),
+            self.cols[j] = ColState(j, n, t(obj), t(vlo), t(vhi), padded(n, self.R),
+                                    padded(n, self.R), torch.zeros(n, **f64),
                                     torch.zeros(n, **f64), torch.zeros(n, **f64),
                                     torch.zeros(n, **f64))
         for i in self.local_rows:
@@ -309,7 +368,7 @@ class PdhgEngine:
                 li, hi_, _ = problem.bands.row_data(r0, r1)
                 t = lambda a: a  # noqa: E731
                 clo, chi = li, hi_
-            self.rows[i] = RowState(i, m, t(clo), t(chi), torch.zeros(m, **f64), torch.zeros(m, **f64),
+            self.rows[i] = RowState(i, m, t(clo), t(chi), padded(m, self.C), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
         kw = dict(exact_row_max=self.opts.exact_row_max,
                   light_row_max=self.opts.light_row_max if self.opts.light_row_max is not None
@@ -372,6 +431,12 @@ class PdhgEngine:
         self.choices["column_bands"] = {f"{k}{i},{j}": len(getattr(getattr(b, k), "bands", [None]))
                                         for (i, j), b in self.blocks.items() for k in ("A", "AT")}
         self._banded = any(isinstance(m, BandedCsr) for b in self.blocks.values() for m in (b.A, b.AT))
+        hot = int(self.opts.hot_gather_bytes) // 8
+        for b in self.blocks.values():
+            for m in (b.A, b.AT):
+                if isinstance(m, DeviceCsr) and self.sorted and hot > 0 and m.num_cols > hot:
+                    m.struct.hot_cols = hot
+        self.choices["hot_gather_bytes"] = int(self.opts.hot_gather_bytes) if self.sorted else 0
         tensors = [t for b in self.blocks.values() for d in (b.A, b.AT) for t in d.tensors()]
         tensors += [t for c in self.cols.values() for t in (c.c, c.lo, c.hi)]
         tensors += [t for r in self.rows.values() for t in (r.lo, r.hi)]
@@ -415,6 +480,11 @@ class PdhgEngine:
             e1.record()
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
+        # the trial ops cache one C source per Fused object (matrix + gather
+        # vector): drop them, so a losing candidate's HBM is freed as soon as
+        # the caller lets go of it
+        ops._srcs.clear()
+        del xs, outs
         return sorted(times)[2] * 1e-3
 
     def _sell_auto(self, setup, arr) -> DeviceCsr:
@@ -681,6 +751,30 @@ class PdhgEngine:
         target = scratch if keep else bufs[0]
         return pre, (axis, index, bufs, scratch), Parts([target], length)
 
+    def _shard_plan(self, axis, index, items, vec_state, length):
+        """Main-loop plan of the sharded NCCL executor on an axis of G > 1
+        members (see EngineOptions.nccl_sharded): the block's partial product
+        goes into a buffer padded to G * S, the all-to-all hands member q's
+        slice of this rank's shard to recv[q], and the epilogue runs over the
+        shard view of the vectors, adding the G slices in ascending order."""
+        (blk, orient, g), = items
+        G = self.R if axis == "R" else self.C
+        me = self.comm.coord[0] if axis == "R" else self.comm.coord[1]
+        S = -(-length // G)
+        partial = self._buf(blk, f"sh_{axis}", G * S)
+        recv = self._buf(blk, f"shr_{axis}", G * S)
+        a = min(me * S, length)
+        b = min(a + S, length)
+        fields = [f.name for f in dataclasses.fields(vec_state)]
+        view = {}
+        for k in fields:
+            v = getattr(vec_state, k)
+            view[k] = v[a:b] if isinstance(v, torch.Tensor) else v
+        view["n" if axis == "R" else "m"] = b - a
+        shard_state = type(vec_state)(**view)
+        return ShardPlan(axis, index, Fused(blk.A if orient == "A" else blk.AT, g), partial, recv,
+                         Parts([recv[q * S:q * S + (b - a)] for q in range(G)], b - a), shard_state, me, S, G)
+
     def _plans(self):
         cols, rows, blocks = self.cols, self.rows, self.blocks
         col_items = lambda j, vec: [(blocks[(i, j)], "T", vec(i)) for i in self.local_rows if (i, j) in blocks]  # noqa: E731
@@ -699,6 +793,15 @@ class PdhgEngine:
                            for i in self.local_rows}
         self.plan_pow_s = {j: self._axis_plan("R", j, col_items(j, lambda i: rows[i].u), cols[j].n, False, "pT")
                            for j in self.local_cols}
+        self.shard_primal, self.shard_dual = {}, {}
+        if self.sharded:
+            if self.R > 1:
+                self.shard_primal = {j: self._shard_plan("R", j, col_items(j, lambda i: rows[i].y), cols[j],
+                                                         cols[j].n) for j in self.local_cols}
+            if self.C > 1:
+                self.shard_dual = {i: self._shard_plan("C", i, row_items(i, lambda j: cols[j].xbar), rows[i],
+                                                       rows[i].m) for i in self.local_rows}
+        self._stale_x = False
 
     def _run_plan(self, plan):
         pre, red, final = plan
@@ -845,17 +948,46 @@ class PdhgEngine:
             (i, row), = self.rows.items()
             ops.iterate(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h)
             return
+        comm = self.comm
         for t in range(count):
             for j, col in self.cols.items():
-                ops.primal(self._run_plan(self.plan_primal[j]), col, t, h)
+                sp_ = self.shard_primal.get(j)
+                if sp_ is None:
+                    ops.primal(self._run_plan(self.plan_primal[j]), col, t, h)
+                    continue
+                ops.store(sp_.src, sp_.partial)
+                comm.exchange(sp_.axis, j, sp_.partial, sp_.recv)
+                ops.primal(sp_.final, sp_.state, t, h)
+                comm.gather_shard(sp_.axis, j, col.xbar, sp_.me, sp_.S)
+                self._stale_x = True        # x is current on this rank's shard only
             for i, row in self.rows.items():
-                ops.dual(self._run_plan(self.plan_dual[i]), row, t, h)
+                sd = self.shard_dual.get(i)
+                if sd is None:
+                    ops.dual(self._run_plan(self.plan_dual[i]), row, t, h)
+                    continue
+                ops.store(sd.src, sd.partial)
+                comm.exchange(sd.axis, i, sd.partial, sd.recv)
+                ops.dual(sd.final, sd.state, t, h)
+                comm.gather_shard(sd.axis, i, row.y, sd.me, sd.S)
         ops.step_advance(count)
+
+    def _sync_shards(self):
+        """Sharded NCCL executor: all-gather x (updated on this rank's shard
+        only during the main loop) before anything reads all of it — the KKT
+        pass, a trace snapshot, the solution."""
+        if not self._stale_x:
+            return
+        for j, col in self.cols.items():
+            sp_ = self.shard_primal.get(j)
+            if sp_ is not None:
+                self.comm.gather_shard(sp_.axis, j, col.x, sp_.me, sp_.S)
+        self._stale_x = False
 
     def _graphable(self) -> bool:
         if not (self.opts.use_graphs and self.device.type == "cuda"):
             return False
-        return self.comm.kind in ("virtual", "peer") or (self.comm.kind == "nccl" and self.opts.graph_nccl)
+        return self.comm.kind in ("virtual", "peer") or (self.comm.kind == "nccl" and self.opts.graph_nccl
+                                                          and getattr(self.comm, "graph_safe", False))
 
     def _run_iterations(self, count: int):
         if count <= 0:
@@ -908,6 +1040,7 @@ class PdhgEngine:
         """One evaluation pass (+ the speculative restart probe). Returns
         (report, pieces) with host scalars reduced in the reference order."""
         ops = self.ops
+        self._sync_shards()
         for i, row in self.rows.items():
             src = self._run_plan(self.plan_kkt_ax[i])
             fused = isinstance(src, Fused)
@@ -977,6 +1110,7 @@ class PdhgEngine:
         return self._g_sum(tab, 0, self.R), self._g_sum(tab, 1, self.C)
 
     def _snapshot_xy(self):
+        self._sync_shards()
         xs = {j: self._from_internal_col(j, c.x.detach()).copy() for j, c in self.cols.items()}
         ys = {i: self._from_internal_row(i, r.y.detach()).copy() for i, r in self.rows.items()}
         return xs, ys
@@ -1014,7 +1148,8 @@ class PdhgEngine:
         self.count_iterations(target - total)
         trace = st["trace"]
         if trace is None:
-            self._run_iterations(target - total)
+            with nvtx_range("gridlp.iterations"):
+                self._run_iterations(target - total)
             st["inner_k"] += target - total
             total = target
         else:
@@ -1029,7 +1164,8 @@ class PdhgEngine:
         st["total"] = total
         if total % K != 0:
             return False
-        report, tab = self._kkt(tau, o.restarts)
+        with nvtx_range("gridlp.kkt_pass"):
+            report, tab = self._kkt(tau, o.restarts)
         self.passes += 1
         st["report"], st["report_at"] = report, total
         if st["log_hook"] is not None:
@@ -1077,6 +1213,7 @@ class PdhgEngine:
             report, _ = self._kkt(eta / omega, False)
             if status != NUMERICAL_FAILURE and _broken(report):
                 status = NUMERICAL_FAILURE
+        self._sync_shards()
         if self.device.type == "cuda":
             torch.cuda.synchronize(self.device)
         self.timings["main_loop_s"] = time.perf_counter() - self._t_loop

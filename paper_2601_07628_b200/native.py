@@ -44,13 +44,14 @@ class Csr(ctypes.Structure):
                 ("exact_long", c_void_p), ("num_exact_long", c_int64),
                 ("chunk_first", c_void_p), ("chunk_row", c_void_p), ("num_chunks", c_int64),
                 ("chunk_sums", c_void_p), ("chunk_done", c_void_p),
-                ("light_row_max", c_int32), ("exact_row_max", c_int32), ("carry", c_void_p)]
+                ("light_row_max", c_int32), ("exact_row_max", c_int32), ("carry", c_void_p),
+                ("hot_cols", c_int64)]
 
 
 class Peer(ctypes.Structure):
     _fields_ = [("dst", c_void_p * MAX_PARTS), ("flag", c_void_p * MAX_PARTS), ("recv", c_void_p),
                 ("my_flag", c_void_p), ("epoch", c_void_p), ("cta_count", c_void_p), ("group_size", c_int32),
-                ("my_slot", c_int32), ("len", c_int64)]
+                ("my_slot", c_int32), ("len", c_int64), ("timeout_ns", c_int64)]
 
 
 class Src(ctypes.Structure):
@@ -89,6 +90,8 @@ SIGNATURES = {
     "gridlp_device_info": ([c_int, POINTER(c_int32), POINTER(c_int64)], c_int),
     "gridlp_enable_peer_access": ([c_int], c_int),
     "gridlp_op_slots": ([POINTER(Src)], c_int64),
+    "gridlp_set_tuning": ([ctypes.c_char_p, c_int64], c_int),
+    "gridlp_get_tuning": ([ctypes.c_char_p], c_int64),
     "gridlp_op_store": ([POINTER(Src), _P, c_uint32, POINTER(Red), _P], c_int),
     "gridlp_op_store_peer": ([POINTER(Src), POINTER(Peer), _P, _P], c_int),
     "gridlp_op_primal": ([POINTER(Src), POINTER(Primal), _P, c_int32, c_uint32, _P], c_int),
@@ -197,6 +200,13 @@ class Library:
 
     def slots(self, src: Src) -> int:
         return int(self._lib.gridlp_op_slots(ctypes.byref(src)))
+
+    def set_tuning(self, key: str, value: int) -> None:
+        """gridlp_set_tuning: kernel choice knobs (bit-identical results)."""
+        self.call("gridlp_set_tuning", key.encode(), int(value))
+
+    def get_tuning(self, key: str) -> int:
+        return int(self._lib.gridlp_get_tuning(key.encode()))
 
     def device_info(self, device: int = 0):
         sm = c_int32(0)

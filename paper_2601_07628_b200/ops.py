@@ -140,10 +140,18 @@ class CudaOps:
         return ctypes.byref(c)
 
     def set_step(self, tau: float, sigma: float, gamma: float, inner_k: int):
+        # the pinned staging buffer may still be read by the previous async
+        # copy (e.g. finish() right after a partial chunk): wait for it first
+        ev = getattr(self, "_step_ev", None)
+        if ev is not None:
+            ev.synchronize()
         h = self.step_host
         h[0], h[1], h[2] = tau, sigma, gamma
         h.view(torch.int64)[3] = int(inner_k)
         self.step.copy_(h, non_blocking=True)
+        if ev is None:
+            ev = self._step_ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
 
     def read_slots(self, n: int) -> np.ndarray:
         self.slots_host[:n].copy_(self.slots[:n], non_blocking=True)
