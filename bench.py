@@ -61,6 +61,10 @@ CONFIGS = {
     # ~8B nnz (A + A^T > 180 GB, needs >= 4 GPUs); cfg5s is a 1/20 one-GPU cut
     "cfg5": dict(gen="planted", num_rows=250_000_000, num_cols=400_000_000, draws_per_row=32, seed=0),
     "cfg5s": dict(gen="planted", num_rows=12_500_000, num_cols=20_000_000, draws_per_row=32, seed=0),
+    # one grid block of cfg5 on a 2x2 grid (4 GPUs): 125M x 200M, ~2B nnz
+    # (16 of each row's 32 draws fall in a column half) — the single-GPU
+    # readiness run for the sharded oversized solve
+    "cfg5q": dict(gen="planted", num_rows=125_000_000, num_cols=200_000_000, draws_per_row=16, seed=0),
 }
 WORKLOADS = {
     "uniform_random": "reference generator uniform_random LP",
@@ -169,6 +173,82 @@ def make_problem(name):
     log(f"[bench] generated {name}: m={p.num_constraints} n={p.num_variables} "
         f"nnz={p.matrix.nnz} in {time.perf_counter() - t0:.1f}s")
     return p
+
+
+def measure_config(name: str, dev, steps: int = 3) -> dict:
+    """Device µs per fused iteration and the HBM roofline fraction of another
+    BASELINE config on this GPU (the same measurement as the main line, a
+    few steps): recorded as an extra key so every driver bench run carries
+    the power-law (cfg3) number next to the cfg2 headline."""
+    import torch
+
+    from paper_2601_07628_b200 import SolverConfig
+    from paper_2601_07628_b200.api import prepare
+
+    p = make_problem(name)
+    cfg = SolverConfig(tolerance=1e-300, max_iterations=10**12, seed=0)
+    engine, layout, eta, omega, tim = prepare(p, cfg, device=dev)
+    engine.start(eta, omega)
+    for _ in range(3):
+        engine.step()
+    torch.cuda.synchronize()
+    engine.iteration_events = []
+    for _ in range(steps):
+        engine.step()
+    torch.cuda.synchronize()
+    ev = engine.iteration_events
+    t_iter = sum(a.elapsed_time(b) for a, b, _ in ev) * 1e-3 / max(sum(n for _, _, n in ev), 1)
+    b = iteration_bytes(engine)
+    peak, _ = measured_peak()
+    out = {"workload": f"{name}: {workload_name(name)}, m={p.num_constraints} n={p.num_variables} "
+                       f"nnz={sum(v for v in engine.per_device_nnz if v >= 0)}",
+           "us_per_iteration": t_iter * 1e6, "iterations_per_s": 1.0 / t_iter,
+           "bytes_per_iteration": b["iteration"], "achieved_GBs": b["iteration"] / t_iter / 1e9,
+           "frac": b["iteration"] / t_iter / 1e9 / peak, "layout_choices": dict(engine.choices)}
+    del engine, p
+    torch.cuda.empty_cache()
+    return out
+
+
+def cfg1_latency(dev, runs: int = 3) -> dict:
+    """BASELINE configs[0] (the reference's own CPU-runnable case, 2k x 4k,
+    20k nnz): time to 1e-4 through the public solve() from host arrays
+    (median of `runs` complete solves after one warm solve) and the device
+    µs per iteration of its main loop. This size is launch bound (two
+    products of 20k nonzeros per iteration): CUDA graphs of 64 iterations
+    with programmatic chaining between the products."""
+    import torch
+
+    from paper_2601_07628_b200 import GeneratorSpec, SolverConfig, generate, solve
+    from paper_2601_07628_b200.api import prepare
+
+    p = generate(GeneratorSpec(**CONFIGS["cfg1"]))
+    cfg = SolverConfig(tolerance=1e-4, seed=0)
+    solve(p, cfg)
+    walls = []
+    for _ in range(runs):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = solve(p, cfg)
+        walls.append(time.perf_counter() - t0)
+    engine, layout, eta, omega, tim = prepare(p, SolverConfig(tolerance=1e-300, max_iterations=10**12, seed=0),
+                                              device=dev)
+    engine.start(eta, omega)
+    for _ in range(3):
+        engine.step()
+    torch.cuda.synchronize()
+    engine.iteration_events = []
+    for _ in range(20):
+        engine.step()
+    torch.cuda.synchronize()
+    ev = engine.iteration_events
+    t_iter = sum(a.elapsed_time(b) for a, b, _ in ev) * 1e-3 / max(sum(n for _, _, n in ev), 1)
+    del engine
+    return {"workload": "cfg1: reference generator uniform_random LP m=2000 n=4000 nnz=20000 ineq=0.3 seed=0",
+            "time_to_tol_s": statistics.median(walls), "runs_s": walls, "status": res.status,
+            "iterations": res.iterations, "restarts": res.restarts, "objective": res.objective,
+            "us_per_iteration": t_iter * 1e6,
+            "reference_cpu_time_to_tol_s": "2.09-2.55 (BASELINE.md section 4, reference CPU PDHG)"}
 
 
 def kernel_tuning() -> dict:
@@ -473,6 +553,10 @@ def run_ours(args, rank, world, local_rank):
     del engine
     torch.cuda.empty_cache()
     spmv = spmv_compare(p, dev) if world == 1 and not args.no_spmv and not hasattr(p, "bands") else None
+    extra = {}
+    if world == 1 and args.config == "cfg2" and not args.no_extra:
+        extra["cfg1_latency"] = cfg1_latency(dev)
+        extra["cfg3"] = measure_config("cfg3", dev)
 
     # e2e through the public API, host arrays in, host arrays out
     e2e = None
@@ -538,6 +622,7 @@ def run_ours(args, rank, world, local_rank):
         "kernels": {k: {"seconds": ktimes[k], "bytes": bytes_[k], "GB/s": bytes_[k] / ktimes[k] / 1e9}
                     for k in ktimes},
         "spmv": spmv,
+        "extra_configs": extra or None,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -586,6 +671,7 @@ def main():
     ap.add_argument("--e2e-runs", type=int, default=3, help="complete solves timed for e2e (median reported)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmv", action="store_true", help="skip the SpMV-only comparison with cuSPARSE")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 latency / cfg3 extra keys")
     ap.add_argument("--light-row-max", type=int, default=None, help="EngineOptions.light_row_max override")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches (the NCCL executor's path)")
     ap.add_argument("--natural-order", action="store_true", help="EngineOptions.sorted_order=False (layout order)")

@@ -90,10 +90,10 @@ enum gridlp_status {
 typedef struct gridlp_csr {
   int64_t num_rows;
   int64_t num_cols;
-  int64_t nnz;                /* < 2^31 per block */
+  int64_t nnz;                /* < 2^31 per block (int32 row pointers in the setup); SELL offsets are int64 */
   const double* sell_vals;    /* [slice_off[num_slices]] */
   const int32_t* sell_cols;
-  const int32_t* slice_off;   /* [num_slices + 1] */
+  const int64_t* slice_off;   /* [num_slices + 1] (int64: padded SELL entries may pass 2^31) */
   const int32_t* lane_info;   /* [32 * num_slices] */
   int64_t num_slices;         /* ceil(num_rows / 32) */
   const int32_t* long_rows;   /* [num_long_rows] ascending */
@@ -193,6 +193,11 @@ typedef struct gridlp_primal {
   const double* lo;
   const double* hi;
   int64_t n;
+  /* Column scale Dc of a diagonally scaled LP (scaling.py: A~ = Dr A Dc,
+   * x = Dc x~), NULL when unscaled. When set, gridlp_op_kkt_cols evaluates
+   * the KKT terms of the ORIGINAL LP at x = Dc x~ (the restart terms stay
+   * in the scaled space); every other op ignores it. */
+  const double* scale;
 } gridlp_primal_t;
 
 /* Dual-side vectors of one grid row i (length m). */
@@ -202,6 +207,9 @@ typedef struct gridlp_dual {
   const double* lo;   /* con_lower */
   const double* hi;   /* con_upper */
   int64_t m;
+  /* Row scale Dr (y = Dr y~), NULL when unscaled: gridlp_op_kkt_rows then
+   * reports the original LP's range violation and bound penalty. */
+  const double* scale;
 } gridlp_dual_t;
 
 /* Reduction workspace: `partials` holds capacity * GRIDLP_MAX_RED doubles;
@@ -400,12 +408,12 @@ int gridlp_csr_permute(const int32_t* ptr, const int32_t* col, const double* val
  * longer rows go to long_rows [nrows] / long_ptr [nrows+1]; sizes (device
  * int64[3]) = {SELL elements, long rows, long-row nonzeros}. */
 int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t light_row_max, int32_t* lane_info,
-                     int32_t* slice_off, int32_t* rank_of, int32_t* long_rows, int32_t* long_ptr,
+                     int64_t* slice_off, int32_t* rank_of, int32_t* long_rows, int32_t* long_ptr,
                      int64_t* sizes, void* ws, size_t ws_bytes, void* stream);
 
 /* SELL-32 fill from a CSR and its plan (padding zeroed). */
 int gridlp_sell_fill(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows,
-                     int32_t light_row_max, const int32_t* slice_off, const int32_t* rank_of,
+                     int32_t light_row_max, const int64_t* slice_off, const int32_t* rank_of,
                      const int32_t* long_rows, const int32_t* long_ptr, int64_t num_long,
                      int32_t* sell_col, double* sell_val, int64_t sell_elems, int32_t* long_col,
                      double* long_val, void* stream);

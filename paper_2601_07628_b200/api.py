@@ -119,8 +119,10 @@ class SolverConfig:
     # B200 extensions (not in the reference; defaults keep its behaviour):
     # on-device diagonal preconditioning (scaling.py) — "none", "ruiz",
     # "pock_chambolle" or "ruiz+pock_chambolle". With scaling the iteration,
-    # restart and termination tests run on the scaled LP (report fields refer
-    # to it); x, y and the objective are returned in the original space.
+    # the iteration and the restart tests run on the scaled LP; the KKT
+    # report (termination, log, SolveResult.report) is evaluated on the
+    # ORIGINAL LP at the unscaled iterate; x, y and the objective are
+    # returned in the original space.
     scaling: str = "none"
     ruiz_iterations: int = 10
 
@@ -255,7 +257,7 @@ def _device():
 
 
 def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, device=None,
-            engine_overrides=None):
+            engine_overrides=None, scaled=None):
     """Layout + blocks in HBM + step sizes: everything before the main loop
     (solver_driver.py:199-227). Returns (engine, layout, eta, omega, timings)."""
     t_start = time.perf_counter()
@@ -278,7 +280,14 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
     for k, v in (engine_overrides or {}).items():
         setattr(opts, k, v)
     preload = None
-    if (HOST_OVERLAP and not banded and opts.device_setup and torch.cuda.is_available()
+    if scaled is not None:
+        # diagonally scaled LP: its CSR is already in HBM (scaling.py)
+        if device is None:
+            device = _device()
+        preload = scaled.device_csr
+        host_f = _host_pool().submit(host_job) if HOST_OVERLAP else _Done(host_job())
+        layout = layout_job()
+    elif (HOST_OVERLAP and not banded and opts.device_setup and torch.cuda.is_available()
             and (device is None or device.type == "cuda")):
         layout_f = _host_pool().submit(layout_job)
         scal_f = _host_pool().submit(problem_scalars, problem)
@@ -308,7 +317,9 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
         comm = VirtualGrid(R, C)
     with eng.nvtx_range("gridlp.setup_blocks"):
         engine = eng.PdhgEngine(problem, layout, opts, comm, ops_factory or CudaOps, device, 0.0, 0.0, 0.0,
-                                preload=preload)
+                                preload=preload,
+                                kkt_scale=None if scaled is None else (scaled.row_scale_device,
+                                                                       scaled.col_scale_device))
     del preload
     timings.update(engine.timings)
     timings["layout_order"] = engine.choices.get("order")
@@ -317,6 +328,10 @@ def prepare(problem, cfg: SolverConfig, force_1x1=False, ops_factory=None, devic
         t0 = time.perf_counter()
         (cnorm, bnorm, const), probe = host_f.result()
         engine.cnorm, engine.bnorm, engine.const = cnorm, bnorm, const
+        if scaled is not None:
+            # KKT is reported on the original LP: its norms normalise the
+            # residuals; the scaled norms (above) set the initial primal weight
+            engine.cnorm, engine.bnorm, _ = problem_scalars(scaled.original)
         timings["host_scalars_wait_s"] = time.perf_counter() - t0
     if banded:
         cnorm, bnorm = engine.band_scalars()
@@ -337,10 +352,13 @@ def _solve(problem, cfg: SolverConfig, trace=None, force_1x1=False, ops_factory=
     t_start = time.perf_counter()
     scaled = None
     if cfg.scaling != "none":
+        if hasattr(problem, "bands"):
+            raise ValueError("scaling is not supported for band problems (blocks generated per device)")
         scaled = scale_problem(problem, cfg.scaling, cfg.ruiz_iterations, device)
+        scaled.original = problem
         original, problem = problem, scaled.problem
     engine, layout, eta, omega, timings = prepare(problem, cfg, force_1x1, ops_factory, device,
-                                                  engine_overrides)
+                                                  engine_overrides, scaled=scaled)
     if scaled is not None:
         timings["scaling_s"] = scaled.seconds
     comm = engine.comm

@@ -159,8 +159,6 @@ def build_sell(host: HostCsr, light_row_max: int):
     slice_len = lane_len.reshape(-1, 32).max(axis=1) if ns else np.zeros(0, np.int64)
     slice_off = np.concatenate([[0], np.cumsum(32 * slice_len)]).astype(np.int64)
     total = int(slice_off[-1])
-    if total >= 2 ** 31 - 64:
-        raise ValueError("SELL block too large for int32 offsets")
     vals = np.zeros(total + 8, dtype=np.float64)
     cols = np.zeros(total + 8, dtype=np.int32)
     rows_l = order[pos]
@@ -183,7 +181,7 @@ def build_sell(host: HostCsr, light_row_max: int):
         hvals = np.concatenate([host.val[hsrc], np.zeros(4)])
     else:
         hcols, hvals = np.zeros(4, np.int32), np.zeros(4)
-    return dict(vals=vals, cols=cols, slice_off=slice_off.astype(np.int32),
+    return dict(vals=vals, cols=cols, slice_off=slice_off.astype(np.int64),
                 lane_info=info.astype(np.int32), num_slices=ns, long_rows=hrows.astype(np.int32),
                 long_ptr=hptr.astype(np.int32), long_cols=hcols, long_vals=hvals)
 
@@ -444,7 +442,7 @@ class DeviceSetup:
         m, n = int(A.num_rows), int(A.num_cols)
         if n >= 2 ** 31 - 1 or m >= 2 ** 31 - 1:
             raise ValueError("device setup needs < 2^31 rows and columns per matrix")
-        nnz = int(len(A.values))
+        nnz = int(np.asarray(A.row_offsets)[-1]) if m else 0       # (a scaled LP's values live on the device)
         self.nnz, self.n = nnz, n
 
         def t(a, dt):
@@ -536,7 +534,7 @@ class DeviceSetup:
         ns = (m + 31) // 32
         i32 = dict(dtype=torch.int32, device=dev)
         lane_info = torch.empty(max(ns * 32, 1), **i32)
-        slice_off = torch.empty(ns + 1, **i32)
+        slice_off = torch.empty(ns + 1, dtype=torch.int64, device=self.device)
         rank_of = torch.empty(max(m, 1), **i32)
         long_rows = torch.empty(max(m, 1), **i32)
         long_ptr = torch.empty(m + 1, **i32)

@@ -306,11 +306,21 @@ struct OpKktRows {
   const double* lo;
   const double* hi;
   double* ax;
+  const double* dr;        // row scale of a scaled LP (NULL: unscaled)
   struct Data { double y, lo, hi; };
   __device__ void prepare() {}
   __device__ Data load(int64_t r) const { return {y[r], lo[r], hi[r]}; }
-  __device__ void row(int64_t r, double s, const Data& d, double* acc) const {
+  __device__ void row(int64_t r, double s, const Data& ds, double* acc) const {
     if (ax) ax[r] = s;
+    Data d = ds;
+    if (dr) {
+      // original LP: A x = s / Dr, bounds / Dr, y = Dr y~
+      const double w = dr[r];
+      s = ddiv(s, w);
+      d.lo = ddiv(d.lo, w);
+      d.hi = ddiv(d.hi, w);
+      d.y = dmul(d.y, w);
+    }
     // range_violation (pdhg_engine.py:206-208)
     const double rv = dsub(np_maximum(dsub(s, d.hi), 0.0), np_maximum(dsub(d.lo, s), 0.0));
     acc[0] = dadd(acc[0], dmul(rv, rv));
@@ -334,6 +344,7 @@ struct OpKktCols {
   const double* hi;
   double* xpb;
   const gridlp_step_t* step;
+  const double* dc;        // column scale of a scaled LP (NULL: unscaled)
   double tau;
   struct Data { double x, c, lo, hi; };
   __device__ void prepare() { tau = step->tau; }
@@ -342,12 +353,27 @@ struct OpKktCols {
     // pdhg_engine.py:325-336
     const double shifted = dsub(d.x, dmul(tau, dsub(d.c, aty)));
     const double xp = np_clip(shifted, d.lo, d.hi);
-    const double rd = ddiv(dsub(xp, d.x), tau);
-    const double rc = ddiv(dsub(xp, shifted), tau);
     const double dx = dsub(d.x, xp);
-    acc[0] = dadd(acc[0], dmul(rd, rd));
-    acc[1] = dadd(acc[1], dmul(d.c, d.x));
-    acc[2] = dadd(acc[2], dmul(rc, d.x));
+    if (!dc) {
+      const double rd = ddiv(dsub(xp, d.x), tau);
+      const double rc = ddiv(dsub(xp, shifted), tau);
+      acc[0] = dadd(acc[0], dmul(rd, rd));
+      acc[1] = dadd(acc[1], dmul(d.c, d.x));
+      acc[2] = dadd(acc[2], dmul(rc, d.x));
+    } else {
+      // the same evaluation on the ORIGINAL LP at x = Dc x~ (A^T y = aty / Dc,
+      // c = c~ / Dc, bounds * Dc), same step tau; restart terms below stay scaled
+      const double w = dc[r];
+      const double xo = dmul(d.x, w);
+      const double co = ddiv(d.c, w);
+      const double sh = dsub(xo, dmul(tau, dsub(co, ddiv(aty, w))));
+      const double xpo = np_clip(sh, dmul(d.lo, w), dmul(d.hi, w));
+      const double rd = ddiv(dsub(xpo, xo), tau);
+      const double rc = ddiv(dsub(xpo, sh), tau);
+      acc[0] = dadd(acc[0], dmul(rd, rd));
+      acc[1] = dadd(acc[1], dmul(co, xo));
+      acc[2] = dadd(acc[2], dmul(rc, xo));
+    }
     acc[3] = dadd(acc[3], dmul(dx, dx));
     if (xpb) xpb[r] = dsub(dmul(2.0, xp), d.x);
   }
@@ -736,7 +762,7 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
     const int info = A.lane_info[slice * 32 + lane];
     if (info >= 0) {
       const int len = info >> 8;
-      const int64_t base = (int64_t)A.slice_off[slice] + lane;
+      const int64_t base = A.slice_off[slice] + lane;
       const int* __restrict__ cp = A.sell_cols + base;
       const double* __restrict__ vp = A.sell_vals + base;
       double s = A.carry ? ld_carry(A.carry + r, pf) : 0.0;   // column bands: continue the chain
@@ -792,7 +818,7 @@ __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_
   if (slice < A.num_slices) {
     info = A.lane_info[slice * 32 + lane];
     len = info >= 0 ? info >> 8 : 0;
-    const int64_t base = (int64_t)A.slice_off[slice] + lane;
+    const int64_t base = A.slice_off[slice] + lane;
     cp = A.sell_cols + base;
     vp = A.sell_vals + base;
   }
@@ -1266,7 +1292,7 @@ int gridlp_op_kkt_rows(const gridlp_src_t* src, const gridlp_dual_t* dv, double*
                        const gridlp_red_t* red, void* stream) {
   if (!dv) return fail(GRIDLP_ERR_ARG, "op_kkt_rows: null argument");
   if (src && src_rows(src) != dv->m) return fail(GRIDLP_ERR_ARG, "op_kkt_rows: length mismatch");
-  OpKktRows op{dv->y, dv->lo, dv->hi, ax};
+  OpKktRows op{dv->y, dv->lo, dv->hi, ax, dv->scale};
   return launch_op(src, op, red, stream, "op_kkt_rows");
 }
 
@@ -1276,6 +1302,7 @@ int gridlp_op_kkt_cols(const gridlp_src_t* src, const gridlp_primal_t* pv, doubl
   if (src && src_rows(src) != pv->n) return fail(GRIDLP_ERR_ARG, "op_kkt_cols: length mismatch");
   OpKktCols op{};
   op.x = pv->x; op.c = pv->c; op.lo = pv->lo; op.hi = pv->hi; op.xpb = x_probe_bar; op.step = d_step;
+  op.dc = pv->scale;
   return launch_op(src, op, red, stream, "op_kkt_cols");
 }
 

@@ -225,7 +225,7 @@ __global__ void gather_len_kernel(const int32_t* __restrict__ long_rows, const i
     hlen[i] = i < n ? ptr[long_rows[i] + 1] - ptr[long_rows[i]] : 0;
 }
 
-__global__ void sizes_kernel(const int32_t* __restrict__ slice_off, int64_t nslices, const int64_t* __restrict__ nh,
+__global__ void sizes_kernel(const int64_t* __restrict__ slice_off, int64_t nslices, const int64_t* __restrict__ nh,
                              const int32_t* __restrict__ long_ptr, int64_t* __restrict__ sizes) {
   sizes[0] = slice_off[nslices];
   sizes[1] = *nh;
@@ -235,13 +235,13 @@ __global__ void sizes_kernel(const int32_t* __restrict__ slice_off, int64_t nsli
 // SELL fill: one thread per light row writes its entries column-major.
 __global__ void sell_fill_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                                  const double* __restrict__ val, int64_t nrows, int32_t light_row_max,
-                                 const int32_t* __restrict__ slice_off, const int32_t* __restrict__ rank_of,
+                                 const int64_t* __restrict__ slice_off, const int32_t* __restrict__ rank_of,
                                  int32_t* __restrict__ sell_col, double* __restrict__ sell_val) {
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= nrows) return;
   const int32_t a = ptr[row], b = ptr[row + 1];
   if (b - a > light_row_max) return;
-  const int64_t base = (int64_t)slice_off[row >> 5] + rank_of[row];
+  const int64_t base = slice_off[row >> 5] + rank_of[row];
   for (int32_t k = a; k < b; ++k) {
     sell_col[base + 32 * (int64_t)(k - a)] = col[k];
     sell_val[base + 32 * (int64_t)(k - a)] = val[k];
@@ -363,7 +363,7 @@ int gridlp_csr_permute(const int32_t* ptr, const int32_t* col, const double* val
 }
 
 int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t light_row_max, int32_t* lane_info,
-                     int32_t* slice_off, int32_t* rank_of, int32_t* long_rows, int32_t* long_ptr,
+                     int64_t* slice_off, int32_t* rank_of, int32_t* long_rows, int32_t* long_ptr,
                      int64_t* sizes, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t nslices = (nrows + 31) / 32;
@@ -404,7 +404,7 @@ int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t light_row_max, i
 }
 
 int gridlp_sell_fill(const int32_t* ptr, const int32_t* col, const double* val, int64_t nrows, int32_t light_row_max,
-                     const int32_t* slice_off, const int32_t* rank_of, const int32_t* long_rows,
+                     const int64_t* slice_off, const int32_t* rank_of, const int32_t* long_rows,
                      const int32_t* long_ptr, int64_t num_long, int32_t* sell_col, double* sell_val,
                      int64_t sell_elems, int32_t* long_col, double* long_val, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -98,7 +98,7 @@ class EngineOptions:
     # length-class order) at L2 evict_last; the rest is gathered evict_first
     # (gridlp_csr_t.hot_cols). 0 = every gather evict_last. Cache policy
     # only: results are unchanged.
-    hot_gather_bytes: int = 64 << 20
+    hot_gather_bytes: int = 0
     use_graphs: bool = True
     # capture the NCCL executor's iterations (kernels + NCCL collectives) in
     # a CUDA graph too, as the single-GPU and peer executors do
@@ -127,6 +127,7 @@ class ColState:
     xpb: torch.Tensor
     v: torch.Tensor
     s: torch.Tensor
+    scale: torch.Tensor | None = None     # Dc of a scaled LP (KKT on the original LP)
 
 
 @dataclass
@@ -140,6 +141,7 @@ class RowState:
     ax: torch.Tensor
     dy: torch.Tensor
     u: torch.Tensor
+    scale: torch.Tensor | None = None     # Dr of a scaled LP
 
 
 @dataclass
@@ -244,7 +246,8 @@ class PdhgEngine:
     """Blocks, state and the main loop for the coords local to this process."""
 
     def __init__(self, problem, layout, opts: EngineOptions, comm, ops_factory, device,
-                 objective_norm: float, bound_norm: float, objective_constant: float, preload=None):
+                 objective_norm: float, bound_norm: float, objective_constant: float, preload=None,
+                 kkt_scale=None):
         self.opts = opts
         self.layout = layout
         self.comm = comm
@@ -256,6 +259,7 @@ class PdhgEngine:
         self._ops_factory = ops_factory
         self.choices = {}
         t0 = time.perf_counter()
+        self._kkt_scale = kkt_scale      # (Dr, Dc) user-order device vectors of a scaled LP, or None
         self._build(problem, preload)
         if comm.kind == "peer":
             (i0, j0), = comm.local
@@ -353,7 +357,9 @@ class PdhgEngine:
             self.cols[j] = ColState(j, n, t(obj), t(vlo), t(vhi), padded(n, self.R),
                                     padded(n, self.R), torch.zeros(n, **f64),
                                     torch.zeros(n, **f64), torch.zeros(n, **f64),
-                                    torch.zeros(n, **f64))
+                                    torch.zeros(n, **f64),
+                                    t(self._kkt_scale[1] if dev_vec else self._kkt_scale[1].cpu().numpy())
+                                    if self._kkt_scale is not None else None)
         for i in self.local_rows:
             r0, r1 = lay.row_range(i)
             m = r1 - r0
@@ -369,7 +375,9 @@ class PdhgEngine:
                 t = lambda a: a  # noqa: E731
                 clo, chi = li, hi_
             self.rows[i] = RowState(i, m, t(clo), t(chi), padded(m, self.C), torch.zeros(m, **f64),
-                                    torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64))
+                                    torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64),
+                                    t(self._kkt_scale[0] if dev_vec else self._kkt_scale[0].cpu().numpy())
+                                    if self._kkt_scale is not None else None)
         kw = dict(exact_row_max=self.opts.exact_row_max,
                   light_row_max=self.opts.light_row_max if self.opts.light_row_max is not None
                   else DEFAULT_LIGHT_ROW_MAX)
@@ -523,16 +531,10 @@ class PdhgEngine:
         each row's add chain."""
         best = self._sell_auto(setup, arr)
         o = self.opts
-        if o.column_bands is not None:
-            K = int(o.column_bands)
-        elif arr.nnz and arr.num_cols * 8 > o.band_bytes:
-            K = min(16, -(-arr.num_cols * 8 // o.band_bytes))
-        else:
-            K = 1
-        K = min(K, max(arr.num_cols, 1))
+        cuts = self._band_cuts(arr.num_cols) if arr.nnz or o.column_bands is not None else [0, arr.num_cols]
+        K = len(cuts) - 1
         if K <= 1:
             return best
-        cuts = [(k * arr.num_cols) // K for k in range(K + 1)]
         parts = split_column_bands(arr, cuts, o.exact_row_max, to_layout)
         banded = BandedCsr([self._sell_auto(setup, p) for p in parts], cuts, self.device)
         del parts
@@ -617,21 +619,54 @@ class PdhgEngine:
             row_len = np.diff(np.asarray(A.row_offsets, np.int64))[lay.perm.row_perm]
             col_len = np.bincount(A.col_indices, minlength=int(A.num_cols))[lay.perm.col_perm]
             order, inverse = length_order, inverse_order
+        def banded(length, piece):
+            """Band-major order: the ranges a gather vector of `length`
+            entries would be cut into as column bands (_band_cuts) keep their
+            layout positions, and `piece(a, b)` orders each range inside —
+            so a band is one contiguous run of the gathered vector in HBM
+            (L2-resident while its band is multiplied) as well as a
+            contiguous piece of every row's add chain."""
+            cuts = self._band_cuts(length)
+            if len(cuts) == 2:
+                return piece(0, length)
+            parts = [a + piece(a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+            return torch.cat(parts) if isinstance(parts[0], torch.Tensor) else np.concatenate(parts)
+
         for i in range(self.R):
             r0, r1 = lay.row_range(i)
-            self.row_order[i] = order(row_len[r0:r1])
+            rl = row_len[r0:r1]
+            self.row_order[i] = banded(r1 - r0, lambda a, b: order(rl[a:b]))
             self.row_inv[i] = inverse(self.row_order[i])
         touch = self._first_touch(setup) if setup is not None and self.opts.first_touch_cols else None
         for j in range(self.C):
             c0, c1 = lay.col_range(j)
+            cl = col_len[c0:c1]
             if touch is None:
-                self.col_order[j] = order(col_len[c0:c1])
+                self.col_order[j] = banded(c1 - c0, lambda a, b: order(cl[a:b]))
             else:
                 # first-touch order inside each length class (stable sorts:
                 # by first touch, then by class)
-                base = torch.sort(touch[c0:c1], stable=True).indices
-                self.col_order[j] = base[length_order_device(col_len[c0:c1][base])]
+                tj = touch[c0:c1]
+
+                def piece(a, b):
+                    base = torch.sort(tj[a:b], stable=True).indices
+                    return base[length_order_device(cl[a:b][base])]
+                self.col_order[j] = banded(c1 - c0, piece)
             self.col_inv[j] = inverse(self.col_order[j])
+
+    def _band_cuts(self, length: int) -> list:
+        """Column-band cuts of a gather vector of `length` doubles: one band
+        unless it exceeds band_bytes (or column_bands forces a count); the
+        same cuts in the internal order (band-major) and in _block_auto."""
+        o = self.opts
+        if o.column_bands is not None:
+            K = int(o.column_bands)
+        elif length * 8 > o.band_bytes:
+            K = min(16, -(-length * 8 // o.band_bytes))
+        else:
+            K = 1
+        K = max(1, min(K, max(length, 1)))
+        return [(k * length) // K for k in range(K + 1)]
 
     def _first_touch(self, setup) -> torch.Tensor:
         """Per layout column, the position of its first use in the A

@@ -237,7 +237,7 @@ def layout_summary(problem, layout: PartitionLayout, per_device_nnz=None) -> dic
     R, C = layout.topology.rows, layout.topology.cols
     if per_device_nnz is None:
         A = problem.matrix
-        if len(A.values):
+        if int(np.asarray(A.row_offsets)[-1]) if int(A.num_rows) else 0:
             inv_r = layout.perm.inverse_rows()
             inv_c = layout.perm.inverse_cols()
             band_r = np.searchsorted(layout.row_cuts, inv_r, side="right") - 1

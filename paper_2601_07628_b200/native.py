@@ -67,12 +67,12 @@ class Step(ctypes.Structure):
 
 class Primal(ctypes.Structure):
     _fields_ = [("x", c_void_p), ("x_bar", c_void_p), ("x_anchor", c_void_p),
-                ("c", c_void_p), ("lo", c_void_p), ("hi", c_void_p), ("n", c_int64)]
+                ("c", c_void_p), ("lo", c_void_p), ("hi", c_void_p), ("n", c_int64), ("scale", c_void_p)]
 
 
 class Dual(ctypes.Structure):
     _fields_ = [("y", c_void_p), ("y_anchor", c_void_p), ("lo", c_void_p),
-                ("hi", c_void_p), ("m", c_int64)]
+                ("hi", c_void_p), ("m", c_int64), ("scale", c_void_p)]
 
 
 TERMS_PER_ROW = 4      # the most reduction terms a fused product op emits per row (KKT columns)

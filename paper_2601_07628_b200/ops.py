@@ -127,7 +127,7 @@ class CudaOps:
         c = getattr(col, "_cprimal", None)
         if c is None:
             c = native.Primal(_ptr(col.x), _ptr(col.xbar), _ptr(col.x0), _ptr(col.c),
-                              _ptr(col.lo), _ptr(col.hi), col.n)
+                              _ptr(col.lo), _ptr(col.hi), col.n, _ptr(getattr(col, "scale", None)))
             col._cprimal = c
         return ctypes.byref(c)
 
@@ -135,7 +135,8 @@ class CudaOps:
     def dual_struct(row):
         c = getattr(row, "_cdual", None)
         if c is None:
-            c = native.Dual(_ptr(row.y), _ptr(row.y0), _ptr(row.lo), _ptr(row.hi), row.m)
+            c = native.Dual(_ptr(row.y), _ptr(row.y0), _ptr(row.lo), _ptr(row.hi), row.m,
+                            _ptr(getattr(row, "scale", None)))
             row._cdual = c
         return ctypes.byref(c)
 

@@ -28,12 +28,41 @@ from .problem import LpProblem, SparseMatrix
 MODES = ("none", "ruiz", "pock_chambolle", "ruiz+pock_chambolle")
 
 
+class _ScaledMatrix:
+    """The scaled CSR as the solver sees it: the sparsity pattern on the host
+    (the layout needs only counts) and the scaled values on the device (the
+    device setup consumes them there). `values` downloads on first access
+    (nothing on the solve path reads it)."""
+
+    def __init__(self, A, dev_val, nnz):
+        self.num_rows, self.num_cols = int(A.num_rows), int(A.num_cols)
+        self.row_offsets, self.col_indices = A.row_offsets, A.col_indices
+        self._dev_val, self._nnz, self._host = dev_val, nnz, None
+
+    @property
+    def values(self):
+        if self._host is None:
+            self._host = self._dev_val[:self._nnz].cpu().numpy()
+        return self._host
+
+    @property
+    def nnz(self):
+        return self._nnz
+
+    @property
+    def shape(self):
+        return (self.num_rows, self.num_cols)
+
+
 @dataclass
 class ScaledProblem:
-    problem: LpProblem          # the scaled LP (host arrays, solve() input)
+    problem: LpProblem          # the scaled LP (solve() input; matrix values stay on the device)
     row_scale: np.ndarray       # Dr
     col_scale: np.ndarray       # Dc
     seconds: float = 0.0
+    device_csr: tuple | None = None     # (ptr int64, col int32, val f64) of the scaled A in HBM
+    row_scale_device: object = None
+    col_scale_device: object = None
 
     def unscale(self, x: np.ndarray, y: np.ndarray):
         return x * self.col_scale, y * self.row_scale
@@ -96,9 +125,14 @@ def scale_problem(problem, mode: str = "ruiz+pock_chambolle", ruiz_iterations: i
         if k:
             lib.call("gridlp_scale_vector", p(v), p(d), k, div, stream)
     h = lambda t: t.cpu().numpy()  # noqa: E731
-    scaled = LpProblem(SparseMatrix(m, n, A.row_offsets, A.col_indices, h(val)[:nnz], check=False),
+    scaled = LpProblem(SparseMatrix(m, n, A.row_offsets, A.col_indices, np.zeros(0), check=False),
                        h(c), h(lv), h(uv), h(lc), h(uc),
                        objective_constant=float(getattr(problem, "objective_constant", 0.0)),
                        maximize=bool(getattr(problem, "maximize", False)),
                        name=str(getattr(problem, "name", "")))
-    return ScaledProblem(scaled, h(dr), h(dc), time.perf_counter() - t0)
+    # the scaled values never leave the device: the engine's device setup
+    # takes the scaled CSR as its preloaded input
+    scaled.matrix = _ScaledMatrix(A, val, nnz)
+    torch.cuda.synchronize(dev)
+    return ScaledProblem(scaled, h(dr), h(dc), time.perf_counter() - t0, device_csr=(ptr, col, val),
+                         row_scale_device=dr, col_scale_device=dc)

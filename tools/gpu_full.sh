@@ -5,5 +5,5 @@ python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log | cut -c1-400
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/bench_ref.log | cut -c1-300
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-spmv > gpurun_out/ncu_launch.log 2>&1; echo "ncu1 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:sell32_kernel<.*Op(Dual|Primal)' -s 40 -c 2 -o gpurun_out/prof_sell32 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-spmv > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-spmv --no-extra > gpurun_out/ncu_launch.log 2>&1; echo "ncu1 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:sell32(_pipe)?_kernel<.*Op(Dual|Primal)' -s 40 -c 2 -o gpurun_out/prof_sell32 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-spmv --no-extra > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"

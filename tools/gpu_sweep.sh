@@ -4,7 +4,7 @@ CFG=${CFG:-cfg3}
 IFS=';' read -ra ARR <<< "$SETS"
 for item in "${ARR[@]}"; do
   tag=${item%%:*}; flags=${item#*:}
-  timeout 900 python bench.py --config $CFG --steps ${STEPS:-10} --warmup 3 --no-e2e --no-cpu-baseline --no-spmv $flags \
+  timeout 900 python bench.py --config $CFG --steps ${STEPS:-10} --warmup 3 --no-e2e --no-cpu-baseline --no-spmv --no-extra $flags \
     > gpurun_out/sw_${CFG}_$tag.log 2>&1
   python - "gpurun_out/sw_${CFG}_$tag.log" "$CFG $tag" <<'PY'
 import json, sys

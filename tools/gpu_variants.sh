@@ -10,7 +10,7 @@ for cfg in ${CFGS:-cfg2 cfg3}; do
   for v in ${VARIANTS:-0 1 2 3 4}; do
     for ch in ${CHAINS:-1}; do
       tag=${cfg}_v${v}_c${ch}
-      timeout 900 python bench.py --config $cfg --steps ${STEPS:-10} --warmup 3 --no-e2e --no-cpu-baseline --no-spmv \
+      timeout 900 python bench.py --config $cfg --steps ${STEPS:-10} --warmup 3 --no-e2e --no-cpu-baseline --no-spmv --no-extra \
         --tuning sell_variant=$v --tuning chain_products=$ch $EXTRA > gpurun_out/var_$tag.log 2>&1
       python - "$tag" <<'PY'
 import json, sys
