@@ -357,6 +357,7 @@ def spmv_compare(problem, device, reps=20) -> dict:
     lib = {}
     t_lib = timed(lambda: lib.__setitem__("y", torch.mm(T, xs)))
     same = bool(torch.equal(lib["y"].reshape(m), ours))
+    direct = cusparse_direct(T, x, m, n, h.nnz, reps, ours)
     bytes_ = 12 * h.nnz + 4 * (m + 1) + 8 * n + 8 * m
     out = {"rows": m, "cols": n, "nnz": h.nnz, "bytes_per_product": bytes_,
            "ours_us": t_ours * 1e6, "ours_GBs": bytes_ / t_ours / 1e9,
@@ -364,10 +365,48 @@ def spmv_compare(problem, device, reps=20) -> dict:
            "sorted_equals_natural_bitwise": same_sorted, "speedup_sorted_vs_cusparse": t_lib / t_sorted,
            "cusparse_us": t_lib * 1e6, "cusparse_GBs": bytes_ / t_lib / 1e9,
            "speedup_vs_cusparse": t_lib / t_ours, "cusparse_bitwise_equal_ours": same,
-           "median_of": reps, "light_row_max": light, "ours_us_by_light_row_max": per_light}
+           "median_of": reps, "light_row_max": light, "ours_us_by_light_row_max": per_light,
+           "cusparse_spmv_direct": direct}
+    if direct:
+        best = min(v["us"] for v in direct.values())
+        out["speedup_vs_cusparse_spmv_best_alg"] = best / (t_ours * 1e6)
+        out["speedup_sorted_vs_cusparse_spmv_best_alg"] = best / (t_sorted * 1e6)
     del A, As, ops, T
     torch.cuda.empty_cache()
     return out
+
+
+def cusparse_direct(T, x, m, n, nnz, reps, ours):
+    """cusparseSpMV called directly (tools/cusparse_ref.cu) with
+    CUSPARSE_SPMV_CSR_ALG1 and ALG2 on the same CSR and vector: median µs of
+    `reps`, and whether its y equals ours bit for bit."""
+    import ctypes
+
+    import torch
+
+    so = ROOT / "tools" / "_lib" / "libcusparse_ref.so"
+    if not so.exists():
+        return None
+    lib = ctypes.CDLL(str(so))
+    f = lib.cusparse_ref_spmv
+    f.argtypes = [ctypes.c_int64] * 3 + [ctypes.c_void_p] * 5 + [ctypes.c_int, ctypes.c_int,
+                                                                ctypes.POINTER(ctypes.c_float), ctypes.c_void_p]
+    f.restype = ctypes.c_int
+    ptr, col, val = T.crow_indices(), T.col_indices(), T.values()
+    res = {}
+    for alg in (1, 2):
+        y = torch.empty(m, dtype=torch.float64, device=x.device)
+        ms = ctypes.c_float(0.0)
+        rc = f(m, n, nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), x.data_ptr(), y.data_ptr(), alg, reps,
+               ctypes.byref(ms), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        if rc == 0:
+            bytes_ = 12 * nnz + 4 * (m + 1) + 8 * n + 8 * m
+            res[f"CSR_ALG{alg}"] = {"us": ms.value * 1e3, "GBs": bytes_ / (ms.value * 1e-3) / 1e9,
+                                    "bitwise_equal_ours": bool(torch.equal(y, ours))}
+        else:
+            res[f"CSR_ALG{alg}"] = {"error": rc}
+    return res
 
 
 def kernel_times(engine, reps=20):

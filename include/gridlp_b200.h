@@ -44,7 +44,8 @@ enum gridlp_status {
   GRIDLP_OK = 0,
   GRIDLP_ERR_ARG = 1,      /* invalid argument (ValueError in the reference) */
   GRIDLP_ERR_CUDA = 2,     /* CUDA launch / runtime failure                   */
-  GRIDLP_ERR_WORKSPACE = 3 /* reduction workspace too small                   */
+  GRIDLP_ERR_WORKSPACE = 3, /* reduction workspace too small                  */
+  GRIDLP_ERR_UNSUPPORTED = 4 /* valid input this entry point does not handle (caller falls back) */
 };
 
 /* Max number of reduction slots an op can produce (see gridlp_red_t). */
@@ -363,6 +364,20 @@ int gridlp_op_init_primal(const gridlp_primal_t* pv, void* stream);
 /* d_step->inner_k += delta on the device (a captured chunk of `delta`
  * iterations advances the Halpern counter itself, pdhg_engine.py:400). */
 int gridlp_op_step_advance(gridlp_step_t* d_step, int64_t delta, void* stream);
+
+/* n_iters fused iterations of a single-block grid in ONE cooperative launch
+ * (launch-bound LPs, e.g. BASELINE configs[0]): grid-wide barriers between
+ * the primal and dual products instead of kernel boundaries; iterates are
+ * gridlp_pdhg_iterate's bit for bit. `scratch`: caller-owned device memory of
+ * gridlp_persistent_scratch_bytes(), zeroed once before first use (a grid
+ * barrier's counter; it resets itself). GRIDLP_ERR_UNSUPPORTED when a matrix
+ * has heavy (chunked) rows — use gridlp_pdhg_iterate. Same call site as
+ * gridlp_pdhg_iterate (pdhg_engine.py:394-400). */
+size_t gridlp_persistent_scratch_bytes(void);
+int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
+                                   const gridlp_src_t* dual_src, const gridlp_dual_t* dv,
+                                   gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,
+                                   void* scratch, void* stream);
 
 /* --- one-off device preprocessing (csrc/gridlp_setup.cu) -----------------
  * Replaces permute_problem / distribute / slice_block / transpose

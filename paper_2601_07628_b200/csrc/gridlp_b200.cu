@@ -27,6 +27,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -872,6 +873,136 @@ __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_
   pdl_wait();
 }
 
+// ----------------------------------------- persistent kernel (launch-bound LPs)
+// A whole chunk of iterations in ONE cooperative launch: every warp of a
+// co-resident grid walks the SELL slices (lane = row, sequential sum) and the
+// exact long rows (warp per row, entry-order add chain by lane 0) of the
+// primal product, grid barrier, then the dual product, grid barrier, for
+// n_iters iterations. Per-row arithmetic is that of sell32 / long_row, so
+// the iterates are the graph path's bit for bit; what goes is the per-kernel
+// launch and drain (two products of ~20k nonzeros per iteration at
+// BASELINE configs[0] are a few µs of launch each). Vectors rewritten inside
+// the launch are read through L2 (ld.global.cg), never the incoherent L1 /
+// read-only paths. Heavy (chunked) rows are not supported: the caller falls
+// back to gridlp_pdhg_iterate.
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsigned int* gen, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1u) {
+      *count = 0u;
+      __threadfence();
+      *gen = g + 1u;
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <class Op>
+__device__ __forceinline__ void persistent_product(const gridlp_csr_t& A, const double* __restrict__ g, const Op& op,
+                                                   int64_t gw, int64_t W, double* prod) {
+  const int lane = threadIdx.x & 31;
+  double acc[1] = {0.0};
+  for (int64_t slice = gw; slice < A.num_slices; slice += W) {
+    const int64_t r = slice * 32 + lane;
+    const int info = A.lane_info[r];
+    if (info < 0) continue;
+    const int len = info >> 8;
+    const int64_t base = A.slice_off[slice] + lane;
+    double s = A.carry ? ld_cg(A.carry + r) : 0.0;
+    for (int j = 0; j < len; j += SELL_U) {
+      int c[SELL_U];
+      double v[SELL_U], x[SELL_U];
+#pragma unroll
+      for (int u = 0; u < SELL_U; ++u) {
+        const bool ok = j + u < len;
+        c[u] = ok ? A.sell_cols[base + 32 * (j + u)] : 0;
+        v[u] = ok ? A.sell_vals[base + 32 * (j + u)] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < SELL_U; ++u) x[u] = (j + u < len) ? ld_cg(g + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < SELL_U; ++u)
+        if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
+    }
+    const typename Op::Data d = op.load(r);
+    op.row(r, s, d, acc);
+  }
+  // exact long rows: warp per row, products parked in shared memory, lane 0
+  // adds them in entry order (long_row_kernel's chain)
+  for (int64_t q = gw; q < A.num_exact_long; q += W) {
+    const int h = A.exact_long[q];
+    const int64_t p0 = A.long_ptr[h];
+    const int len = A.long_ptr[h + 1] - A.long_ptr[h];
+    double s = A.carry ? ld_cg(A.carry + A.long_rows[h]) : 0.0;
+    for (int j0 = 0; j0 < len; j0 += 32) {
+      const int k = j0 + lane;
+      const double pv = k < len ? dmul(A.long_vals[p0 + k], ld_cg(g + A.long_cols[p0 + k])) : 0.0;
+      __syncwarp();
+      prod[lane] = pv;
+      __syncwarp();
+      if (lane == 0) {
+        const int cnt = len - j0 < 32 ? len - j0 : 32;
+        for (int t = 0; t < cnt; ++t) s = dadd(s, prod[t]);
+      }
+    }
+    if (lane == 0) {
+      const int row = A.long_rows[h];
+      const typename Op::Data d = op.load(row);
+      op.row(row, s, d, acc);
+    }
+    __syncwarp();
+  }
+}
+
+// coherent epilogue loads for the persistent kernel (x, y, x_bar rewritten in-launch)
+struct OpPrimalCg : OpPrimal {
+  __device__ Data load(int64_t r) const {
+    Data d;
+    d.x = ld_cg(x + r); d.c = c[r]; d.lo = lo[r]; d.hi = hi[r];
+    d.x0 = halpern ? x0[r] : 0.0;
+    return d;
+  }
+};
+struct OpDualCg : OpDual {
+  __device__ Data load(int64_t r) const {
+    Data d;
+    d.y = ld_cg(y + r); d.lo = lo[r]; d.hi = hi[r];
+    d.y0 = halpern ? y0[r] : 0.0;
+    return d;
+  }
+};
+
+constexpr int PERSIST_TPB = 256;
+__global__ void __launch_bounds__(PERSIST_TPB) persistent_iterate_kernel(gridlp_csr_t AT, gridlp_csr_t A,
+                                                                        OpPrimalCg pop, OpDualCg dop, int32_t n_iters,
+                                                                        unsigned int* bar, gridlp_step_t* step) {
+  __shared__ double prod[PERSIST_TPB / 32][32];
+  const int warp = threadIdx.x >> 5;
+  const int64_t W = (int64_t)gridDim.x * (PERSIST_TPB / 32);
+  const int64_t gw = (int64_t)blockIdx.x * (PERSIST_TPB / 32) + warp;
+  volatile unsigned int* gen = bar + 1;
+  for (int32_t t = 0; t < n_iters; ++t) {
+    OpPrimalCg p = pop;
+    p.iter = t;
+    p.prepare();
+    persistent_product(AT, (const double*)dop.y, p, gw, W, prod[warp]);   // K1 gathers y
+    grid_barrier(bar, gen, gridDim.x);
+    OpDualCg d = dop;
+    d.iter = t;
+    d.prepare();
+    persistent_product(A, (const double*)pop.xbar, d, gw, W, prod[warp]);   // K2 gathers x_bar
+    grid_barrier(bar, gen, gridDim.x);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) step->inner_k += n_iters;
+}
+
 // Row-wise epilogue over ascending-order sums of partial vectors.
 template <class Op>
 __global__ void __launch_bounds__(TPB) rows_kernel(gridlp_src_t src, int64_t n, Op op,
@@ -1379,6 +1510,53 @@ int gridlp_pdhg_iterate(const gridlp_src_t* primal_src, const gridlp_primal_t* p
     if (rc) return rc;
   }
   return n_iters > 0 ? gridlp_op_step_advance(d_step, n_iters, stream) : GRIDLP_OK;
+}
+
+size_t gridlp_persistent_scratch_bytes(void) { return 64; }
+
+int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
+                                   const gridlp_src_t* dual_src, const gridlp_dual_t* dv, gridlp_step_t* d_step,
+                                   int32_t n_iters, uint32_t flags, void* scratch, void* stream) {
+  if (!primal_src || !dual_src || !pv || !dv || !d_step || n_iters < 0 || !scratch)
+    return fail(GRIDLP_ERR_ARG, "pdhg_iterate_persistent: bad argument");
+  const gridlp_csr_t* AT = primal_src->A;
+  const gridlp_csr_t* A = dual_src->A;
+  if (!AT || !A) return fail(GRIDLP_ERR_ARG, "pdhg_iterate_persistent: needs fused sources");
+  int rc = check_csr(AT);
+  if (!rc) rc = check_csr(A);
+  if (rc) return rc;
+  if (AT->num_chunks > 0 || A->num_chunks > 0)
+    return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_persistent: heavy (chunked) rows need the graph path");
+  if (AT->num_rows != pv->n || A->num_rows != dv->m)
+    return fail(GRIDLP_ERR_ARG, "pdhg_iterate_persistent: length mismatch");
+  if (n_iters == 0) return GRIDLP_OK;
+  static int blocks_per_sm = 0, sms = 0;
+  if (!blocks_per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, persistent_iterate_kernel, PERSIST_TPB, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  // enough warps for the larger product's slices, never more than co-resident
+  const int64_t work = std::max(std::max(AT->num_slices, A->num_slices), std::max(AT->num_exact_long,
+                                                                                  A->num_exact_long));
+  int64_t want = (work + PERSIST_TPB / 32 - 1) / (PERSIST_TPB / 32);
+  const int64_t cap = (int64_t)blocks_per_sm * sms;
+  const int nblocks = (int)std::max<int64_t>(1, std::min(want, cap));
+  OpPrimalCg pop{};
+  pop.x = pv->x; pop.xbar = pv->x_bar; pop.x0 = pv->x_anchor; pop.c = pv->c; pop.lo = pv->lo; pop.hi = pv->hi;
+  pop.step = d_step; pop.halpern = (flags & GRIDLP_F_HALPERN) != 0;
+  OpDualCg dop{};
+  dop.y = dv->y; dop.y0 = dv->y_anchor; dop.lo = dv->lo; dop.hi = dv->hi;
+  dop.step = d_step; dop.halpern = (flags & GRIDLP_F_HALPERN) != 0;
+  gridlp_csr_t at = *AT, a = *A;
+  unsigned int* bar = static_cast<unsigned int*>(scratch);
+  void* args[] = {&at, &a, &pop, &dop, &n_iters, &bar, &d_step};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)persistent_iterate_kernel, dim3(nblocks),
+                                              dim3(PERSIST_TPB), args, 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("pdhg_iterate_persistent: ") + cudaGetErrorString(e));
+  return GRIDLP_OK;
 }
 
 }  // extern "C"

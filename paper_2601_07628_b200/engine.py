@@ -104,6 +104,11 @@ class EngineOptions:
     # a CUDA graph too, as the single-GPU and peer executors do
     graph_nccl: bool = True
     graph_chunk: int = 128
+    # single-block LPs up to this many nonzeros run each chunk of iterations
+    # as ONE cooperative launch with grid barriers between the products
+    # (gridlp_pdhg_iterate_persistent; launch-bound sizes, bit-identical
+    # iterates); 0 = never
+    persistent_max_nnz: int = 1 << 21
     # NCCL executor, main loop: each axis sum is an ordered reduce-scatter
     # (all-to-all of the partial shards, then the epilogue adds the G member
     # slices in ascending order — the reference's order, comm.py:75-84) and
@@ -626,7 +631,9 @@ class PdhgEngine:
             so a band is one contiguous run of the gathered vector in HBM
             (L2-resident while its band is multiplied) as well as a
             contiguous piece of every row's add chain."""
-            cuts = self._band_cuts(length)
+            # only with forced bands: timed (auto) bands keep the plain class
+            # order, band-major measured slower on cfg3 (profiles/r2/README.md)
+            cuts = self._band_cuts(length) if self.opts.column_bands is not None else [0, length]
             if len(cuts) == 2:
                 return piece(0, length)
             parts = [a + piece(a, b) for a, b in zip(cuts[:-1], cuts[1:])]
@@ -975,12 +982,24 @@ class PdhgEngine:
         return est
 
     # -------------------------------------------------------- main loop
+    def _persistent(self) -> bool:
+        """Single block, no column bands, small enough to be launch bound."""
+        if getattr(self, "_persist_ok", None) is None:
+            nnz = sum(b.A.nnz for b in self.blocks.values())
+            self._persist_ok = (self.R == 1 and self.C == 1 and hasattr(self.ops, "iterate_persistent")
+                                and not self._banded and 0 < nnz <= self.opts.persistent_max_nnz)
+        return self._persist_ok
+
     def _launch_iterations(self, count: int):
         ops, h = self.ops, self.opts.halpern
         if self.R == 1 and self.C == 1 and hasattr(ops, "iterate") and count > 0 and not self._banded:
             # one block, fused sources: the whole chunk in one C-ABI call
             (j, col), = self.cols.items()
             (i, row), = self.rows.items()
+            if self._persistent():
+                if ops.iterate_persistent(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h):
+                    return
+                self._persist_ok = False          # heavy rows: the graph path
             ops.iterate(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h)
             return
         comm = self.comm
@@ -1040,7 +1059,7 @@ class PdhgEngine:
 
     def _run_iterations_inner(self, count: int):
         g = max(1, min(self.opts.graph_chunk, self.opts.kkt_interval))
-        if not self._graphable() or count < g:
+        if not self._graphable() or count < g or self._persistent():
             self._launch_iterations(count)
             return
         if self._graph is None:

@@ -108,6 +108,9 @@ SIGNATURES = {
     "gridlp_op_step_advance": ([_P, c_int64, _P], c_int),
     "gridlp_pdhg_iterate": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32, c_uint32, _P],
                             c_int),
+    "gridlp_persistent_scratch_bytes": ([], ctypes.c_size_t),
+    "gridlp_pdhg_iterate_persistent": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,
+                                        c_uint32, _P, _P], c_int),
     "gridlp_setup_workspace_bytes": ([c_int64, c_int64], ctypes.c_size_t),
     "gridlp_block_count": ([_P, _P, _P, c_int64, _P, c_int32, c_int32, _P, _P, ctypes.c_size_t, _P], c_int),
     "gridlp_block_fill": ([_P, _P, _P, _P, c_int64, _P, c_int32, c_int32, _P, c_int64, _P, _P, _P,

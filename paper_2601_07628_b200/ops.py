@@ -230,6 +230,25 @@ class CudaOps:
                       self.dual_struct(row), self.step.data_ptr(), int(count), native.F_HALPERN if halpern else 0,
                       self.stream())
 
+    def iterate_persistent(self, psrc, col, dsrc, row, count: int, halpern: bool) -> bool:
+        """count fused iterations of a single-block grid in one cooperative
+        launch (gridlp_pdhg_iterate_persistent). False (nothing launched)
+        when the blocks have heavy rows: the caller uses iterate()."""
+        scratch = getattr(self, "_persist_scratch", None)
+        if scratch is None:
+            nbytes = int(self.lib._lib.gridlp_persistent_scratch_bytes())
+            scratch = self._persist_scratch = torch.zeros(max(nbytes // 8, 1), dtype=torch.float64,
+                                                          device=self.device)
+        rc = self.lib._lib.gridlp_pdhg_iterate_persistent(
+            self.src(psrc), self.primal_struct(col), self.src(dsrc), self.dual_struct(row), self.step.data_ptr(),
+            int(count), native.F_HALPERN if halpern else 0, scratch.data_ptr(), self.stream())
+        if rc == 4:              # GRIDLP_ERR_UNSUPPORTED
+            return False
+        if rc != 0:
+            raise native.GridlpError(f"gridlp_pdhg_iterate_persistent failed ({rc}): {self.lib.last_error()}")
+        self.launches += 1 if count else 0
+        return True
+
     def step_advance(self, delta: int):
         self.launches += 1
         self.lib.call("gridlp_op_step_advance", self.step.data_ptr(), int(delta), self.stream())

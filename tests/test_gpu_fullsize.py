@@ -10,7 +10,8 @@ reference's own solves) on the SAME instance:
   default engine path on a 1x1 grid, then the final KKT re-evaluation;
 * y after iteration 1 bit-identical on every row of <= 4096 entries (the
   products are sequential sums there, reference sparse_kernels.py:18-24);
-* x, y after 8 iterations within 1e-12 relative max-norm (rows > 4096 are
+* x, y after 8 iterations bit-identical when every row has <= 4096 entries
+  (cfg4), else within 1e-8 relative max-norm (cfg3: rows > 4096 are
   deterministic tree sums, and their rounding propagates);
 * KKT residuals and objectives within 1e-9 relative.
 
@@ -79,8 +80,14 @@ def test_fixed_step_full_size(name):
     else:
         assert _relmax(y1, want.trace[1][1]) <= 1e-12
     x8, y8 = snaps[8]
-    assert _relmax(x8, want.trace[8][0]) <= 1e-12
-    assert _relmax(y8, want.trace[8][1]) <= 1e-12
+    # without heavy rows every product is the reference's sequential sum:
+    # the trajectory is bit-identical. Rows > 4096 entries are tree-summed
+    # (deterministic; ~1e-13 relative per sum, tests/test_gpu_parity.py) and
+    # the dual step's sigma amplifies that through 8 iterations: measured
+    # 3.7e-10 relative max-norm on cfg3 (its heavy rows hold up to ~1e5 entries)
+    tol = 0.0 if exact.all() else 1e-8
+    assert _relmax(x8, want.trace[8][0]) <= tol
+    assert _relmax(y8, want.trace[8][1]) <= tol
     for key in ("r_primal", "r_dual", "r_gap", "obj_primal", "obj_dual"):
         a, b = getattr(got.report, key), getattr(want, key)
         assert abs(a - b) <= 1e-9 * max(abs(b), 1e-300), (key, a, b)

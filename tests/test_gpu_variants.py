@@ -101,3 +101,33 @@ def test_fixed_step_trajectory_every_variant(tuning, variant, chain):
     r = reference_solve(p, SolverConfig(**cfg))
     np.testing.assert_array_equal(r.x, want.x)
     assert got.iterations == r.iterations == 200
+
+
+@pytest.mark.parametrize("heavy", [False, True])
+def test_persistent_launch_equals_graph_path(heavy):
+    """gridlp_pdhg_iterate_persistent (one cooperative launch per chunk, grid
+    barriers between the products) reproduces the kernel-per-product path bit
+    for bit, with long exact rows (warp per row); heavy rows fall back."""
+    from paper_2601_07628_b200.api import _solve
+    from paper_2601_07628_b200.problem import LpProblem, SparseMatrix
+
+    rng = np.random.default_rng(5)
+    m, n = 900, 7000
+    lens = rng.integers(1, 40, m)
+    lens[[2, 50, 400]] = [300, 1500, 4000]
+    if heavy:
+        lens[7] = 6000
+    ptr = np.concatenate([[0], np.cumsum(lens)])
+    col = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int64)
+    val = rng.standard_normal(len(col))
+    xh = rng.uniform(1, 3, n)
+    ax = np.array([val[ptr[i]:ptr[i + 1]] @ xh[col[ptr[i]:ptr[i + 1]]] for i in range(m)])
+    p = LpProblem(SparseMatrix(m, n, ptr, col, val), rng.standard_normal(n), np.zeros(n), np.full(n, 4.0),
+                  ax - 0.3, ax + 0.3)
+    cfg = SolverConfig(tolerance=1e-7, seed=3, max_iterations=3000)
+    a = _solve(p, cfg)
+    b = _solve(p, cfg, engine_overrides={"persistent_max_nnz": 0})
+    assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
+    assert a.report == b.report
