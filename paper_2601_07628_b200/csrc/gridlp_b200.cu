@@ -904,12 +904,15 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsig
   __syncthreads();
 }
 
+// light slices [lbeg, lend) with stride lstep (this CTA's range, warp-strided),
+// then (longs) the exact long rows strided over every warp of the grid
 template <class Op>
 __device__ __forceinline__ void persistent_product(const gridlp_csr_t& A, const double* __restrict__ g, const Op& op,
-                                                   int64_t gw, int64_t W, double* prod) {
+                                                   int64_t gw, int64_t W, double* prod, int64_t lbeg, int64_t lend,
+                                                   int64_t lstep, bool longs) {
   const int lane = threadIdx.x & 31;
   double acc[1] = {0.0};
-  for (int64_t slice = gw; slice < A.num_slices; slice += W) {
+  for (int64_t slice = lbeg; slice < lend; slice += lstep) {
     const int64_t r = slice * 32 + lane;
     const int info = A.lane_info[r];
     if (info < 0) continue;
@@ -936,7 +939,7 @@ __device__ __forceinline__ void persistent_product(const gridlp_csr_t& A, const 
   }
   // exact long rows: warp per row, products parked in shared memory, lane 0
   // adds them in entry order (long_row_kernel's chain)
-  for (int64_t q = gw; q < A.num_exact_long; q += W) {
+  for (int64_t q = gw; longs && q < A.num_exact_long; q += W) {
     const int h = A.exact_long[q];
     const int64_t p0 = A.long_ptr[h];
     const int len = A.long_ptr[h + 1] - A.long_ptr[h];
@@ -980,25 +983,161 @@ struct OpDualCg : OpDual {
 };
 
 constexpr int PERSIST_TPB = 256;
+constexpr int PERSIST_WARPS = PERSIST_TPB / 32;
+constexpr int PERSIST_U = 8;          // gathers in flight per lane (indices come from shared memory)
+
+// One CTA's contiguous range of light slices of one product, resident in
+// shared memory for the whole launch when it fits: SELL indices and values,
+// lane_info, the slice offsets, and the epilogue operands of its rows (the
+// iterate itself, x or y, lives there too and is written back at the end).
+struct SmemSlices {
+  int64_t s0, s1;                     // slice range
+  int64_t e0;                         // slice_off[s0]
+  const int* cols;
+  const double* vals;
+  const int* info;                    // lane_info[32 (s - s0) + lane]
+  const int64_t* off;                 // slice_off[s] - e0, s in [s0, s1]
+  double* v[5];                       // per-row operands (op specific), row = 32 (s - s0) + lane
+};
+
+__device__ __forceinline__ void persist_range(int64_t nslices, int64_t& s0, int64_t& s1) {
+  s0 = nslices * blockIdx.x / gridDim.x;
+  s1 = nslices * (blockIdx.x + 1) / gridDim.x;
+}
+
+// bytes of shared memory a CTA's range needs (nv per-row operands)
+__device__ __forceinline__ int64_t smem_need(const gridlp_csr_t& A, int64_t s0, int64_t s1, int nv) {
+  const int64_t ent = A.slice_off[s1] - A.slice_off[s0];
+  const int64_t rows = 32 * (s1 - s0);
+  return 12 * ent + 4 * rows + 8 * (s1 - s0 + 1) + 8 * nv * rows + 64;
+}
+
+// carve + fill (all threads); returns the bytes used
+__device__ int64_t smem_stage(const gridlp_csr_t& A, int64_t s0, int64_t s1, unsigned char* base, int nv,
+                              const double* const* src, SmemSlices& S) {
+  const int64_t e0 = A.slice_off[s0];
+  const int64_t ent = A.slice_off[s1] - e0;
+  const int64_t rows = 32 * (s1 - s0);
+  unsigned char* p = base;
+  double* vals = reinterpret_cast<double*>(p);
+  p += 8 * ent;
+  for (int q = 0; q < nv; ++q) {
+    S.v[q] = reinterpret_cast<double*>(p);
+    p += 8 * rows;
+  }
+  int64_t* off = reinterpret_cast<int64_t*>(p);
+  p += 8 * (s1 - s0 + 1);
+  int* cols = reinterpret_cast<int*>(p);
+  p += 4 * ent;
+  int* info = reinterpret_cast<int*>(p);
+  p += 4 * rows;
+  for (int64_t k = threadIdx.x; k < ent; k += blockDim.x) {
+    vals[k] = A.sell_vals[e0 + k];
+    cols[k] = A.sell_cols[e0 + k];
+  }
+  for (int64_t k = threadIdx.x; k <= s1 - s0; k += blockDim.x) off[k] = A.slice_off[s0 + k] - e0;
+  for (int64_t k = threadIdx.x; k < rows; k += blockDim.x) {
+    const int64_t r = 32 * s0 + k;
+    info[k] = A.lane_info[r];
+    for (int q = 0; q < nv; ++q) S.v[q][k] = (src[q] && r < A.num_rows) ? src[q][r] : 0.0;
+  }
+  S.s0 = s0; S.s1 = s1; S.e0 = e0; S.cols = cols; S.vals = vals; S.info = info; S.off = off;
+  return (int64_t)(p - base);
+}
+
+// sequential sum of one lane's row from the staged slice (sell32's order)
+__device__ __forceinline__ double smem_row_sum(const SmemSlices& S, int64_t ls, int lane, int len,
+                                               const double* __restrict__ g, double s) {
+  const int64_t base = S.off[ls] + lane;
+  for (int j = 0; j < len; j += PERSIST_U) {
+    double x[PERSIST_U];
+#pragma unroll
+    for (int u = 0; u < PERSIST_U; ++u) x[u] = (j + u < len) ? ld_cg(g + S.cols[base + 32 * (j + u)]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < PERSIST_U; ++u)
+      if (j + u < len) s = dadd(s, dmul(S.vals[base + 32 * (j + u)], x[u]));
+  }
+  return s;
+}
+
 __global__ void __launch_bounds__(PERSIST_TPB) persistent_iterate_kernel(gridlp_csr_t AT, gridlp_csr_t A,
                                                                         OpPrimalCg pop, OpDualCg dop, int32_t n_iters,
-                                                                        unsigned int* bar, gridlp_step_t* step) {
-  __shared__ double prod[PERSIST_TPB / 32][32];
-  const int warp = threadIdx.x >> 5;
-  const int64_t W = (int64_t)gridDim.x * (PERSIST_TPB / 32);
-  const int64_t gw = (int64_t)blockIdx.x * (PERSIST_TPB / 32) + warp;
+                                                                        unsigned int* bar, gridlp_step_t* step,
+                                                                        int64_t smem_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double prod[PERSIST_WARPS][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * PERSIST_WARPS;
+  const int64_t gw = (int64_t)blockIdx.x * PERSIST_WARPS + warp;
   volatile unsigned int* gen = bar + 1;
+  // this CTA's light slices of both products, staged in shared memory when
+  // they fit (uniform per CTA); rows of long / heavy-free exact long rows stay
+  // in global memory (warp per row, strided over the grid)
+  int64_t ps0, ps1, ds0, ds1;
+  persist_range(AT.num_slices, ps0, ps1);
+  persist_range(A.num_slices, ds0, ds1);
+  // primal operands: x, c, lo, hi, x0; dual: y, lo, hi, y0
+  const bool staged = smem_need(AT, ps0, ps1, 5) + smem_need(A, ds0, ds1, 4) <= smem_bytes;
+  SmemSlices P{}, D{};
+  if (staged) {
+    const double* psrc[5] = {pop.x, pop.c, pop.lo, pop.hi, pop.halpern ? pop.x0 : nullptr};
+    const double* dsrc[4] = {dop.y, dop.lo, dop.hi, dop.halpern ? dop.y0 : nullptr};
+    const int64_t used = smem_stage(AT, ps0, ps1, smem, 5, psrc, P);
+    smem_stage(A, ds0, ds1, smem + ((used + 15) & ~int64_t(15)), 4, dsrc, D);
+    __syncthreads();
+  }
   for (int32_t t = 0; t < n_iters; ++t) {
     OpPrimalCg p = pop;
     p.iter = t;
     p.prepare();
-    persistent_product(AT, (const double*)dop.y, p, gw, W, prod[warp]);   // K1 gathers y
+    if (staged) {
+      for (int64_t ls = warp; ls < ps1 - ps0; ls += PERSIST_WARPS) {
+        const int64_t k = 32 * ls + lane;
+        const int info = P.info[k];
+        if (info < 0) continue;
+        const int64_t r = 32 * (ps0 + ls) + lane;
+        const double aty = smem_row_sum(P, ls, lane, info >> 8, dop.y, AT.carry ? ld_cg(AT.carry + r) : 0.0);
+        // OpPrimal::row on the staged operands (x kept in shared memory)
+        const double xv = P.v[0][k];
+        const double xh = np_clip(dsub(xv, dmul(p.tau, dsub(P.v[1][k], aty))), P.v[2][k], P.v[3][k]);
+        p.xbar[r] = dsub(dmul(2.0, xh), xv);
+        P.v[0][k] = p.halpern ? halpern_mix(xh, xv, P.v[4][k], p.wm, p.gamma, p.wa) : xh;
+      }
+    } else {
+      persistent_product(AT, (const double*)dop.y, p, gw, W, prod[warp], ps0 + warp, ps1, PERSIST_WARPS,
+                         false);                                              // K1 gathers y
+    }
+    persistent_product(AT, (const double*)dop.y, p, gw, W, prod[warp], 0, 0, 1, true);    // exact long rows
     grid_barrier(bar, gen, gridDim.x);
     OpDualCg d = dop;
     d.iter = t;
     d.prepare();
-    persistent_product(A, (const double*)pop.xbar, d, gw, W, prod[warp]);   // K2 gathers x_bar
+    if (staged) {
+      for (int64_t ls = warp; ls < ds1 - ds0; ls += PERSIST_WARPS) {
+        const int64_t k = 32 * ls + lane;
+        const int info = D.info[k];
+        if (info < 0) continue;
+        const int64_t r = 32 * (ds0 + ls) + lane;
+        const double z = smem_row_sum(D, ls, lane, info >> 8, pop.xbar, A.carry ? ld_cg(A.carry + r) : 0.0);
+        const double yv = D.v[0][k];
+        const double yh = dual_map(yv, z, d.sigma, D.v[1][k], D.v[2][k]);
+        const double yn = d.halpern ? halpern_mix(yh, yv, D.v[3][k], d.wm, d.gamma, d.wa) : yh;
+        D.v[0][k] = yn;
+        d.y[r] = yn;                    // the next primal product gathers y
+      }
+    } else {
+      persistent_product(A, (const double*)pop.xbar, d, gw, W, prod[warp], ds0 + warp, ds1, PERSIST_WARPS,
+                         false);                                              // K2 gathers x_bar
+    }
+    persistent_product(A, (const double*)pop.xbar, d, gw, W, prod[warp], 0, 0, 1, true);
     grid_barrier(bar, gen, gridDim.x);
+  }
+  if (staged) {
+    // the primal iterate lived in shared memory: write it back
+    for (int64_t k = threadIdx.x; k < 32 * (ps1 - ps0); k += blockDim.x) {
+      const int64_t r = 32 * ps0 + k;
+      if (r < AT.num_rows && P.info[k] >= 0) pop.x[r] = P.v[0][k];
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) step->inner_k += n_iters;
 }
@@ -1530,20 +1669,27 @@ int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_
   if (AT->num_rows != pv->n || A->num_rows != dv->m)
     return fail(GRIDLP_ERR_ARG, "pdhg_iterate_persistent: length mismatch");
   if (n_iters == 0) return GRIDLP_OK;
+  // one CTA per SM with up to PERSIST_SMEM of shared memory: each CTA stages
+  // its slice range of both matrices there when it fits
+  constexpr int PERSIST_SMEM = 200 * 1024;
   static int blocks_per_sm = 0, sms = 0;
   if (!blocks_per_sm) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, persistent_iterate_kernel, PERSIST_TPB, 0);
+    cudaFuncSetAttribute(persistent_iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PERSIST_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, persistent_iterate_kernel, PERSIST_TPB,
+                                                  PERSIST_SMEM);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  // enough warps for the larger product's slices, never more than co-resident
+  // enough warps for the larger product's slices (one slice per warp), never
+  // more than co-resident
   const int64_t work = std::max(std::max(AT->num_slices, A->num_slices), std::max(AT->num_exact_long,
                                                                                   A->num_exact_long));
-  int64_t want = (work + PERSIST_TPB / 32 - 1) / (PERSIST_TPB / 32);
+  int64_t want = (work + PERSIST_WARPS - 1) / PERSIST_WARPS;
   const int64_t cap = (int64_t)blocks_per_sm * sms;
   const int nblocks = (int)std::max<int64_t>(1, std::min(want, cap));
+  int64_t smem_bytes = PERSIST_SMEM;
   OpPrimalCg pop{};
   pop.x = pv->x; pop.xbar = pv->x_bar; pop.x0 = pv->x_anchor; pop.c = pv->c; pop.lo = pv->lo; pop.hi = pv->hi;
   pop.step = d_step; pop.halpern = (flags & GRIDLP_F_HALPERN) != 0;
@@ -1552,9 +1698,10 @@ int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_
   dop.step = d_step; dop.halpern = (flags & GRIDLP_F_HALPERN) != 0;
   gridlp_csr_t at = *AT, a = *A;
   unsigned int* bar = static_cast<unsigned int*>(scratch);
-  void* args[] = {&at, &a, &pop, &dop, &n_iters, &bar, &d_step};
+  void* args[] = {&at, &a, &pop, &dop, &n_iters, &bar, &d_step, &smem_bytes};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)persistent_iterate_kernel, dim3(nblocks),
-                                              dim3(PERSIST_TPB), args, 0, static_cast<cudaStream_t>(stream));
+                                              dim3(PERSIST_TPB), args, PERSIST_SMEM,
+                                              static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("pdhg_iterate_persistent: ") + cudaGetErrorString(e));
   return GRIDLP_OK;
 }

@@ -108,7 +108,7 @@ class EngineOptions:
     # as ONE cooperative launch with grid barriers between the products
     # (gridlp_pdhg_iterate_persistent; launch-bound sizes, bit-identical
     # iterates); 0 = never
-    persistent_max_nnz: int = 1 << 21
+    persistent_max_nnz: int = 1 << 17
     # NCCL executor, main loop: each axis sum is an ordered reduce-scatter
     # (all-to-all of the partial shards, then the epilogue adds the G member
     # slices in ascending order — the reference's order, comm.py:75-84) and
@@ -624,47 +624,27 @@ class PdhgEngine:
             row_len = np.diff(np.asarray(A.row_offsets, np.int64))[lay.perm.row_perm]
             col_len = np.bincount(A.col_indices, minlength=int(A.num_cols))[lay.perm.col_perm]
             order, inverse = length_order, inverse_order
-        def banded(length, piece):
-            """Band-major order: the ranges a gather vector of `length`
-            entries would be cut into as column bands (_band_cuts) keep their
-            layout positions, and `piece(a, b)` orders each range inside —
-            so a band is one contiguous run of the gathered vector in HBM
-            (L2-resident while its band is multiplied) as well as a
-            contiguous piece of every row's add chain."""
-            # only with forced bands: timed (auto) bands keep the plain class
-            # order, band-major measured slower on cfg3 (profiles/r2/README.md)
-            cuts = self._band_cuts(length) if self.opts.column_bands is not None else [0, length]
-            if len(cuts) == 2:
-                return piece(0, length)
-            parts = [a + piece(a, b) for a, b in zip(cuts[:-1], cuts[1:])]
-            return torch.cat(parts) if isinstance(parts[0], torch.Tensor) else np.concatenate(parts)
-
         for i in range(self.R):
             r0, r1 = lay.row_range(i)
-            rl = row_len[r0:r1]
-            self.row_order[i] = banded(r1 - r0, lambda a, b: order(rl[a:b]))
+            self.row_order[i] = order(row_len[r0:r1])
             self.row_inv[i] = inverse(self.row_order[i])
         touch = self._first_touch(setup) if setup is not None and self.opts.first_touch_cols else None
         for j in range(self.C):
             c0, c1 = lay.col_range(j)
-            cl = col_len[c0:c1]
             if touch is None:
-                self.col_order[j] = banded(c1 - c0, lambda a, b: order(cl[a:b]))
+                self.col_order[j] = order(col_len[c0:c1])
             else:
                 # first-touch order inside each length class (stable sorts:
                 # by first touch, then by class)
-                tj = touch[c0:c1]
-
-                def piece(a, b):
-                    base = torch.sort(tj[a:b], stable=True).indices
-                    return base[length_order_device(cl[a:b][base])]
-                self.col_order[j] = banded(c1 - c0, piece)
+                base = torch.sort(touch[c0:c1], stable=True).indices
+                self.col_order[j] = base[length_order_device(col_len[c0:c1][base])]
             self.col_inv[j] = inverse(self.col_order[j])
 
     def _band_cuts(self, length: int) -> list:
         """Column-band cuts of a gather vector of `length` doubles: one band
-        unless it exceeds band_bytes (or column_bands forces a count); the
-        same cuts in the internal order (band-major) and in _block_auto."""
+        unless it exceeds band_bytes (or column_bands forces a count). (A
+        band-major internal order — bands contiguous in HBM — was measured on
+        cfg3 and did not pay: profiles/r2/README.md.)"""
         o = self.opts
         if o.column_bands is not None:
             K = int(o.column_bands)

@@ -34,7 +34,7 @@ def main():
     for variant in (0, 1):
         lib.set_tuning("sell_variant", variant)
         for grid in ((1, 1), (2, 2)):
-            r = solve(p, SolverConfig(tolerance=1e-6, max_iterations=640, seed=1, n_procs=grid[0] * grid[1],
+            r = solve(p, SolverConfig(tolerance=1e-6, max_iterations=192, seed=1, n_procs=grid[0] * grid[1],
                                       grid=grid))
             print(f"variant {variant} grid {grid}: {r.status} it={r.iterations} obj={r.objective:.10g}")
     print("SANITIZER_CASE_DONE")
