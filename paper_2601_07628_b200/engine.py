@@ -106,9 +106,12 @@ class EngineOptions:
     graph_chunk: int = 128
     # single-block LPs up to this many nonzeros run each chunk of iterations
     # as ONE cooperative launch with grid barriers between the products
-    # (gridlp_pdhg_iterate_persistent; launch-bound sizes, bit-identical
-    # iterates); 0 = never
-    persistent_max_nnz: int = 1 << 17
+    # (gridlp_pdhg_iterate_persistent, bit-identical iterates); 0 = never.
+    # Off by default: measured slower than the chained CUDA-graph path at
+    # every size (cfg1 8.96 vs 7.25 µs/iteration, profiles/r2/README.md) —
+    # two global-memory grid barriers per iteration cost more than the
+    # kernel boundaries PDL already hides
+    persistent_max_nnz: int = 0
     # NCCL executor, main loop: each axis sum is an ordered reduce-scatter
     # (all-to-all of the partial shards, then the epilogue adds the G member
     # slices in ascending order — the reference's order, comm.py:75-84) and

@@ -125,7 +125,7 @@ def test_persistent_launch_equals_graph_path(heavy):
     p = LpProblem(SparseMatrix(m, n, ptr, col, val), rng.standard_normal(n), np.zeros(n), np.full(n, 4.0),
                   ax - 0.3, ax + 0.3)
     cfg = SolverConfig(tolerance=1e-7, seed=3, max_iterations=3000)
-    a = _solve(p, cfg)
+    a = _solve(p, cfg, engine_overrides={"persistent_max_nnz": 1 << 30})
     b = _solve(p, cfg, engine_overrides={"persistent_max_nnz": 0})
     assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
     np.testing.assert_array_equal(a.x, b.x)

@@ -37,6 +37,11 @@ def main():
             r = solve(p, SolverConfig(tolerance=1e-6, max_iterations=192, seed=1, n_procs=grid[0] * grid[1],
                                       grid=grid))
             print(f"variant {variant} grid {grid}: {r.status} it={r.iterations} obj={r.objective:.10g}")
+    from paper_2601_07628_b200.api import _solve
+
+    r = _solve(p, SolverConfig(tolerance=1e-6, max_iterations=192, seed=1),
+               engine_overrides={"persistent_max_nnz": 1 << 30})      # the persistent cooperative launch
+    print(f"persistent: {r.status} it={r.iterations} obj={r.objective:.10g}")
     print("SANITIZER_CASE_DONE")
 
 
