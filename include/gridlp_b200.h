@@ -374,6 +374,18 @@ int gridlp_op_step_advance(gridlp_step_t* d_step, int64_t delta, void* stream);
  * has heavy (chunked) rows — use gridlp_pdhg_iterate. Same call site as
  * gridlp_pdhg_iterate (pdhg_engine.py:394-400). */
 size_t gridlp_persistent_scratch_bytes(void);
+/* n_iters fused iterations of a TINY single-block LP in ONE thread-block
+ * cluster launch (16 CTAs): x_bar / y replicated in every CTA's shared
+ * memory, each CTA's slices of A and A^T with their row operands resident
+ * there, owners broadcast their new entries through distributed shared
+ * memory, hardware cluster barriers between the products. Bit-identical to
+ * gridlp_pdhg_iterate. GRIDLP_ERR_UNSUPPORTED (nothing launched) when the LP
+ * does not fit one cluster's shared memory or has long rows / column bands.
+ * The first call per matrix pair reads the slice offsets (synchronous D2H):
+ * not capturable in a CUDA graph. */
+int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
+                                const gridlp_src_t* dual_src, const gridlp_dual_t* dv,
+                                gridlp_step_t* d_step, int32_t n_iters, uint32_t flags, void* stream);
 int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
                                    const gridlp_src_t* dual_src, const gridlp_dual_t* dv,
                                    gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,

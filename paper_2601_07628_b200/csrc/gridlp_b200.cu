@@ -25,6 +25,7 @@
 //    slot per CTA, then one fixed-order final pass.
 #include "../../include/gridlp_b200.h"
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,6 +35,7 @@
 #include <string>
 #include <type_traits>
 #include <utility>
+#include <vector>
 
 namespace {
 
@@ -1142,6 +1144,113 @@ __global__ void __launch_bounds__(PERSIST_TPB) persistent_iterate_kernel(gridlp_
   if (blockIdx.x == 0 && threadIdx.x == 0) step->inner_k += n_iters;
 }
 
+// ------------------------------------------------ cluster kernel (tiny LPs)
+// For LPs whose vectors and matrix fit in one thread-block cluster's shared
+// memory (BASELINE configs[0]: 2k x 4k, 20k nonzeros), a chunk of iterations
+// runs in ONE cluster launch with no global-memory round trip per product:
+// every CTA holds a replica of x_bar and y, and its contiguous range of both
+// matrices' SELL slices with the row operands; a product's gathers read the
+// local replica, the owner lane of a row broadcasts its new x_bar / y entry
+// into every CTA's replica through distributed shared memory, and a hardware
+// cluster barrier (release / acquire) separates the products. Per-row
+// arithmetic is sell32's (sequential sums, the same epilogue functions), so
+// iterates are the graph path's bit for bit.
+namespace cg = cooperative_groups;
+constexpr int CLUSTER_CTAS = 16;     // non-portable cluster size (B200: 16)
+constexpr int CLUSTER_TPB = 256;
+constexpr int CLUSTER_WARPS = CLUSTER_TPB / 32;
+
+// slice ranges of the CTAs, balanced by SELL entries (host: cluster_plan)
+struct ClusterPlan {
+  int64_t pb[CLUSTER_CTAS + 1];       // primal product (A^T) slice boundaries
+  int64_t db[CLUSTER_CTAS + 1];       // dual product (A) slice boundaries
+};
+
+__global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(CLUSTER_TPB)
+    cluster_iterate_kernel(gridlp_csr_t AT, gridlp_csr_t A, OpPrimal pop, OpDual dop, int32_t n_iters,
+                           gridlp_step_t* step, ClusterPlan plan) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned rank = cluster.block_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n = AT.num_rows, m = A.num_rows;
+  double* xbar_r = reinterpret_cast<double*>(smem);             // replica [n]
+  double* y_r = xbar_r + n;                                      // replica [m]
+  unsigned char* rest = reinterpret_cast<unsigned char*>(y_r + m);
+  const int64_t ps0 = plan.pb[rank], ps1 = plan.pb[rank + 1], ds0 = plan.db[rank], ds1 = plan.db[rank + 1];
+  SmemSlices P{}, D{};
+  const double* psrc[5] = {pop.x, pop.c, pop.lo, pop.hi, pop.halpern ? pop.x0 : nullptr};
+  const double* dsrc[4] = {dop.y, dop.lo, dop.hi, dop.halpern ? dop.y0 : nullptr};
+  const int64_t used = smem_stage(AT, ps0, ps1, rest, 5, psrc, P);
+  smem_stage(A, ds0, ds1, rest + ((used + 15) & ~int64_t(15)), 4, dsrc, D);
+  for (int64_t k = threadIdx.x; k < m; k += CLUSTER_TPB) y_r[k] = dop.y[k];
+  // remote replicas of every CTA in the cluster
+  double* xbar_at[CLUSTER_CTAS];
+  double* y_at[CLUSTER_CTAS];
+#pragma unroll
+  for (int q = 0; q < CLUSTER_CTAS; ++q) {
+    xbar_at[q] = cluster.map_shared_rank(xbar_r, q);
+    y_at[q] = cluster.map_shared_rank(y_r, q);
+  }
+  cluster.sync();
+  for (int32_t t = 0; t < n_iters; ++t) {
+    OpPrimal p = pop;
+    p.iter = t;
+    p.prepare();
+    for (int64_t ls = warp; ls < ps1 - ps0; ls += CLUSTER_WARPS) {
+      const int64_t k = 32 * ls + lane;
+      const int info = P.info[k];
+      if (info < 0) continue;
+      const int len = info >> 8;
+      const int64_t base = P.off[ls] + lane;
+      double aty = 0.0;
+      for (int j = 0; j < len; ++j) aty = dadd(aty, dmul(P.vals[base + 32 * j], y_r[P.cols[base + 32 * j]]));
+      const int64_t r = 32 * (ps0 + ls) + lane;
+      const double xv = P.v[0][k];
+      const double xh = np_clip(dsub(xv, dmul(p.tau, dsub(P.v[1][k], aty))), P.v[2][k], P.v[3][k]);
+      const double xb = dsub(dmul(2.0, xh), xv);
+      P.v[0][k] = p.halpern ? halpern_mix(xh, xv, P.v[4][k], p.wm, p.gamma, p.wa) : xh;
+#pragma unroll
+      for (int q = 0; q < CLUSTER_CTAS; ++q) xbar_at[q][r] = xb;
+    }
+    cluster.sync();
+    OpDual d = dop;
+    d.iter = t;
+    d.prepare();
+    for (int64_t ls = warp; ls < ds1 - ds0; ls += CLUSTER_WARPS) {
+      const int64_t k = 32 * ls + lane;
+      const int info = D.info[k];
+      if (info < 0) continue;
+      const int len = info >> 8;
+      const int64_t base = D.off[ls] + lane;
+      double z = 0.0;
+      for (int j = 0; j < len; ++j) z = dadd(z, dmul(D.vals[base + 32 * j], xbar_r[D.cols[base + 32 * j]]));
+      const int64_t r = 32 * (ds0 + ls) + lane;
+      const double yv = D.v[0][k];
+      const double yh = dual_map(yv, z, d.sigma, D.v[1][k], D.v[2][k]);
+      const double yn = d.halpern ? halpern_mix(yh, yv, D.v[3][k], d.wm, d.gamma, d.wa) : yh;
+      D.v[0][k] = yn;
+#pragma unroll
+      for (int q = 0; q < CLUSTER_CTAS; ++q) y_at[q][r] = yn;
+    }
+    cluster.sync();
+  }
+  // owners write the iterates back (x_bar for completeness: the next chunk
+  // recomputes it before use)
+  for (int64_t k = threadIdx.x; k < 32 * (ps1 - ps0); k += CLUSTER_TPB) {
+    const int64_t r = 32 * ps0 + k;
+    if (r < n && P.info[k] >= 0) {
+      pop.x[r] = P.v[0][k];
+      pop.xbar[r] = xbar_r[r];
+    }
+  }
+  for (int64_t k = threadIdx.x; k < 32 * (ds1 - ds0); k += CLUSTER_TPB) {
+    const int64_t r = 32 * ds0 + k;
+    if (r < m && D.info[k] >= 0) dop.y[r] = D.v[0][k];
+  }
+  if (rank == 0 && threadIdx.x == 0) step->inner_k += n_iters;
+}
+
 // Row-wise epilogue over ascending-order sums of partial vectors.
 template <class Op>
 __global__ void __launch_bounds__(TPB) rows_kernel(gridlp_src_t src, int64_t n, Op op,
@@ -1649,6 +1758,104 @@ int gridlp_pdhg_iterate(const gridlp_src_t* primal_src, const gridlp_primal_t* p
     if (rc) return rc;
   }
   return n_iters > 0 ? gridlp_op_step_advance(d_step, n_iters, stream) : GRIDLP_OK;
+}
+
+int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_primal_t* pv, const gridlp_src_t* dual_src,
+                                const gridlp_dual_t* dv, gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,
+                                void* stream) {
+  if (!primal_src || !dual_src || !pv || !dv || !d_step || n_iters < 0)
+    return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: bad argument");
+  const gridlp_csr_t* AT = primal_src->A;
+  const gridlp_csr_t* A = dual_src->A;
+  if (!AT || !A) return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: needs fused sources");
+  int rc = check_csr(AT);
+  if (!rc) rc = check_csr(A);
+  if (rc) return rc;
+  if (AT->num_rows != pv->n || A->num_rows != dv->m || AT->num_cols != A->num_rows || A->num_cols != AT->num_rows)
+    return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: length mismatch");
+  if (AT->num_long_rows > 0 || A->num_long_rows > 0 || AT->carry || A->carry)
+    return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_cluster: long rows / column bands need the graph path");
+  const int64_t n = AT->num_rows, m = A->num_rows;
+  constexpr int64_t SMEM_MAX = 227 * 1024;
+  // quick reject before reading any offsets: the replicas alone
+  if (8 * (n + m) + 12 * (AT->nnz + A->nnz) / CLUSTER_CTAS > SMEM_MAX || AT->num_slices > (1 << 16) ||
+      A->num_slices > (1 << 16))
+    return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_cluster: LP does not fit one cluster's shared memory");
+  // the plan (entry-balanced slice ranges and the exact shared memory of the
+  // largest CTA) is computed once per matrix pair from its slice offsets
+  struct Cached {
+    const void* at;
+    const void* a;
+    ClusterPlan plan;
+    int64_t smem;
+  };
+  static Cached cache[8];
+  static int ncache = 0, next_slot = 0;
+  const Cached* hit = nullptr;
+  for (int q = 0; q < ncache; ++q)
+    if (cache[q].at == AT->slice_off && cache[q].a == A->slice_off) hit = &cache[q];
+  if (!hit) {
+    Cached c{AT->slice_off, A->slice_off, {}, 0};
+    auto balance = [](const std::vector<int64_t>& off, int64_t* b) {
+      const int64_t ns = (int64_t)off.size() - 1;
+      const int64_t total = off[ns] + 64 * ns;
+      int64_t s = 0;
+      b[0] = 0;
+      for (int q = 1; q < CLUSTER_CTAS; ++q) {
+        const int64_t target = total * q / CLUSTER_CTAS;
+        while (s < ns && off[s] + 64 * s < target) ++s;
+        b[q] = s;
+      }
+      b[CLUSTER_CTAS] = ns;
+    };
+    std::vector<int64_t> po(AT->num_slices + 1), dofs(A->num_slices + 1);
+    if (cudaMemcpy(po.data(), AT->slice_off, 8 * po.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(dofs.data(), A->slice_off, 8 * dofs.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(GRIDLP_ERR_CUDA, "pdhg_iterate_cluster: slice offsets");
+    balance(po, c.plan.pb);
+    balance(dofs, c.plan.db);
+    auto need = [](const std::vector<int64_t>& off, int64_t s0, int64_t s1, int nv) {
+      const int64_t rows = 32 * (s1 - s0);
+      return 12 * (off[s1] - off[s0]) + 4 * rows + 8 * (s1 - s0 + 1) + 8 * nv * rows + 64;
+    };
+    int64_t mx = 0;
+    for (int q = 0; q < CLUSTER_CTAS; ++q) {
+      const int64_t a = need(po, c.plan.pb[q], c.plan.pb[q + 1], 5);
+      const int64_t b = need(dofs, c.plan.db[q], c.plan.db[q + 1], 4);
+      mx = std::max(mx, ((a + 15) & ~int64_t(15)) + b);
+    }
+    c.smem = 8 * (n + m) + mx + 64;
+    const int slot = ncache < 8 ? ncache++ : (next_slot++ & 7);
+    cache[slot] = c;
+    hit = &cache[slot];
+  }
+  const int64_t per_cta = hit->smem;
+  if (per_cta > SMEM_MAX)
+    return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_cluster: LP does not fit one cluster's shared memory");
+  if (n_iters == 0) return GRIDLP_OK;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(cluster_iterate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(cluster_iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX);
+    attr = true;
+  }
+  OpPrimal pop{};
+  pop.x = pv->x; pop.xbar = pv->x_bar; pop.x0 = pv->x_anchor; pop.c = pv->c; pop.lo = pv->lo; pop.hi = pv->hi;
+  pop.step = d_step; pop.halpern = (flags & GRIDLP_F_HALPERN) != 0;
+  OpDual dop{};
+  dop.y = dv->y; dop.y0 = dv->y_anchor; dop.lo = dv->lo; dop.hi = dv->hi;
+  dop.step = d_step; dop.halpern = (flags & GRIDLP_F_HALPERN) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CLUSTER_CTAS);
+  cfg.blockDim = dim3(CLUSTER_TPB);
+  cfg.dynamicSmemBytes = (size_t)per_cta;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, cluster_iterate_kernel, *AT, *A, pop, dop, n_iters, d_step, hit->plan);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GRIDLP_ERR_UNSUPPORTED, std::string("pdhg_iterate_cluster: ") + cudaGetErrorString(e));
+  }
+  return GRIDLP_OK;
 }
 
 size_t gridlp_persistent_scratch_bytes(void) { return 64; }

@@ -92,6 +92,10 @@ class EngineOptions:
     # product says so; an int forces that many (1 = never). Bit-identical.
     column_bands: int | None = None
     band_bytes: int = 48 << 20
+    # blocks above this many nonzeros skip the timed column-band choice (the
+    # torch-level band split needs ~40 B/nnz of temporaries: a 2B-nnz block
+    # of cfg5 on a 2x2 grid would not fit next to its own SELL copy)
+    band_max_nnz: int = 1 << 28
     device_setup: bool = True
     # gathered vectors larger than this many bytes keep only their first
     # hot_gather_bytes (the highest-degree columns / longest rows in the
@@ -112,6 +116,11 @@ class EngineOptions:
     # two global-memory grid barriers per iteration cost more than the
     # kernel boundaries PDL already hides
     persistent_max_nnz: int = 0
+    # tiny single-block LPs (vectors + matrix within one 16-CTA cluster's
+    # shared memory, e.g. BASELINE configs[0]) run each chunk of iterations
+    # in one thread-block-cluster launch (gridlp_pdhg_iterate_cluster,
+    # bit-identical iterates); falls back by itself when the LP is too big
+    cluster_small: bool = True
     # NCCL executor, main loop: each axis sum is an ordered reduce-scatter
     # (all-to-all of the partial shards, then the epilogue adds the G member
     # slices in ascending order — the reference's order, comm.py:75-84) and
@@ -539,6 +548,8 @@ class PdhgEngine:
         each row's add chain."""
         best = self._sell_auto(setup, arr)
         o = self.opts
+        if o.column_bands is None and arr.nnz > o.band_max_nnz:
+            return best
         cuts = self._band_cuts(arr.num_cols) if arr.nnz or o.column_bands is not None else [0, arr.num_cols]
         K = len(cuts) - 1
         if K <= 1:
@@ -973,12 +984,38 @@ class PdhgEngine:
                                 and not self._banded and 0 < nnz <= self.opts.persistent_max_nnz)
         return self._persist_ok
 
+    def _cluster_first(self, count: int) -> bool:
+        """True when the cluster launch takes this chunk (it is one launch
+        already, and its first call per matrix reads offsets synchronously,
+        so it is not graph-captured); decided by trying it once."""
+        if not self._cluster():
+            return False
+        if getattr(self, "_cluster_tried", False):
+            return self._cluster_ok
+        self._cluster_tried = True
+        (j, col), = self.cols.items()
+        (i, row), = self.rows.items()
+        # probe with zero iterations: validates the fit without touching state
+        self._cluster_ok = self.ops.iterate_cluster(self.plan_primal[j][2], col, self.plan_dual[i][2], row, 0,
+                                                    self.opts.halpern)
+        return self._cluster_ok
+
+    def _cluster(self) -> bool:
+        if getattr(self, "_cluster_ok", None) is None:
+            self._cluster_ok = (self.opts.cluster_small and self.R == 1 and self.C == 1
+                                and hasattr(self.ops, "iterate_cluster") and not self._banded)
+        return self._cluster_ok
+
     def _launch_iterations(self, count: int):
         ops, h = self.ops, self.opts.halpern
         if self.R == 1 and self.C == 1 and hasattr(ops, "iterate") and count > 0 and not self._banded:
             # one block, fused sources: the whole chunk in one C-ABI call
             (j, col), = self.cols.items()
             (i, row), = self.rows.items()
+            if self._cluster():
+                if ops.iterate_cluster(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h):
+                    return
+                self._cluster_ok = False          # does not fit: the other paths
             if self._persistent():
                 if ops.iterate_persistent(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h):
                     return
@@ -1042,7 +1079,7 @@ class PdhgEngine:
 
     def _run_iterations_inner(self, count: int):
         g = max(1, min(self.opts.graph_chunk, self.opts.kkt_interval))
-        if not self._graphable() or count < g or self._persistent():
+        if not self._graphable() or count < g or self._persistent() or self._cluster_first(count):
             self._launch_iterations(count)
             return
         if self._graph is None:

@@ -109,6 +109,8 @@ SIGNATURES = {
     "gridlp_pdhg_iterate": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32, c_uint32, _P],
                             c_int),
     "gridlp_persistent_scratch_bytes": ([], ctypes.c_size_t),
+    "gridlp_pdhg_iterate_cluster": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,
+                                     c_uint32, _P], c_int),
     "gridlp_pdhg_iterate_persistent": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,
                                         c_uint32, _P, _P], c_int),
     "gridlp_setup_workspace_bytes": ([c_int64, c_int64], ctypes.c_size_t),

@@ -249,6 +249,20 @@ class CudaOps:
         self.launches += 1 if count else 0
         return True
 
+    def iterate_cluster(self, psrc, col, dsrc, row, count: int, halpern: bool) -> bool:
+        """count fused iterations of a tiny single-block LP in one cluster
+        launch (gridlp_pdhg_iterate_cluster). False (nothing launched) when
+        the LP does not fit one cluster's shared memory."""
+        rc = self.lib._lib.gridlp_pdhg_iterate_cluster(
+            self.src(psrc), self.primal_struct(col), self.src(dsrc), self.dual_struct(row), self.step.data_ptr(),
+            int(count), native.F_HALPERN if halpern else 0, self.stream())
+        if rc == 4:              # GRIDLP_ERR_UNSUPPORTED
+            return False
+        if rc != 0:
+            raise native.GridlpError(f"gridlp_pdhg_iterate_cluster failed ({rc}): {self.lib.last_error()}")
+        self.launches += 1 if count else 0
+        return True
+
     def step_advance(self, delta: int):
         self.launches += 1
         self.lib.call("gridlp_op_step_advance", self.step.data_ptr(), int(delta), self.stream())

@@ -131,3 +131,22 @@ def test_persistent_launch_equals_graph_path(heavy):
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
     assert a.report == b.report
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_cluster_launch_equals_graph_path(seed):
+    """gridlp_pdhg_iterate_cluster (one 16-CTA cluster launch per chunk:
+    replicated vectors and the matrix in shared memory, DSMEM broadcasts,
+    cluster barriers) reproduces the kernel-per-product path bit for bit on
+    BASELINE cfg1-shaped LPs; an LP with long rows falls back by itself."""
+    from paper_2601_07628_b200.api import _solve
+
+    p = generate(GeneratorSpec(kind="uniform_random", num_rows=2000, num_cols=4000, nnz_target=20000,
+                               inequality_fraction=0.3, seed=seed))
+    cfg = SolverConfig(tolerance=1e-6, seed=seed, max_iterations=4000)
+    a = _solve(p, cfg, engine_overrides={"cluster_small": True})
+    b = _solve(p, cfg, engine_overrides={"cluster_small": False})
+    assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
+    assert a.report == b.report
