@@ -231,6 +231,8 @@ typedef struct gridlp_red {
 #define GRIDLP_F_HALPERN 1u   /* EngineConfig.halpern (pdhg_engine.py:396-399) */
 #define GRIDLP_F_SUMSQ 2u     /* op_store: also reduce sum of squares */
 #define GRIDLP_F_STREAM 4u    /* op_store: streaming (evict-first) output, e.g. column-band carries */
+#define GRIDLP_F_UNIFORM_BOUNDS 8u /* op_primal / pdhg_iterate: every variable's bounds equal lo[0], hi[0]
+                                    * (the arrays stay full length; the op reads two scalars instead) */
 
 /* --- library / device ---------------------------------------------------- */
 int gridlp_abi_version(void);
@@ -379,13 +381,19 @@ size_t gridlp_persistent_scratch_bytes(void);
  * memory, each CTA's slices of A and A^T with their row operands resident
  * there, owners broadcast their new entries through distributed shared
  * memory, hardware cluster barriers between the products. Bit-identical to
- * gridlp_pdhg_iterate. GRIDLP_ERR_UNSUPPORTED (nothing launched) when the LP
- * does not fit one cluster's shared memory or has long rows / column bands.
- * The first call per matrix pair reads the slice offsets (synchronous D2H):
- * not capturable in a CUDA graph. */
+ * gridlp_pdhg_iterate. `plan` (host memory, GRIDLP_CLUSTER_PLAN_LEN int64)
+ * comes from gridlp_cluster_plan for the same matrices: entry-balanced slice
+ * ranges per CTA and the shared memory per CTA; it reads the slice offsets
+ * (synchronous D2H, once per matrix pair — outside any graph capture) and
+ * returns GRIDLP_ERR_UNSUPPORTED when the LP does not fit one cluster's
+ * shared memory or has long rows / column bands (use gridlp_pdhg_iterate). */
+#define GRIDLP_CLUSTER_PLAN_LEN 35
+int gridlp_cluster_plan(const gridlp_src_t* primal_src, const gridlp_src_t* dual_src, int64_t* plan,
+                        int64_t plan_len);
 int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
                                 const gridlp_src_t* dual_src, const gridlp_dual_t* dv,
-                                gridlp_step_t* d_step, int32_t n_iters, uint32_t flags, void* stream);
+                                gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,
+                                const int64_t* plan, void* stream);
 int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
                                    const gridlp_src_t* dual_src, const gridlp_dual_t* dv,
                                    gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,

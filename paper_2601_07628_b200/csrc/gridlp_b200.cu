@@ -239,7 +239,8 @@ struct OpPrimal {
   const gridlp_step_t* step;
   int32_t iter;
   bool halpern;
-  double tau, gamma, wm, wa;
+  bool uniform_bounds;     // every variable has the bounds lo[0], hi[0] (GRIDLP_F_UNIFORM_BOUNDS)
+  double tau, gamma, wm, wa, lo0, hi0;
   uint64_t pf;
   struct Data { double x, c, lo, hi, x0; };
   __device__ void prepare() {
@@ -247,14 +248,23 @@ struct OpPrimal {
     gamma = step->gamma;
     halpern_weights(gamma, step->inner_k + iter, wm, wa);
     pf = policy_evict_first();
+    if (uniform_bounds) {
+      lo0 = lo[0];
+      hi0 = hi[0];
+    }
   }
-  // read-once operands and the x rewrite leave L2 first (the gathered
-  // vectors' hot prefix stays); x_bar keeps the normal policy: it is the
-  // next product's gather vector
+  // read-once operands and the x rewrite leave L2 first; x_bar keeps the
+  // normal policy: it is the next product's gather vector
   __device__ Data load(int64_t r) const {
     Data d;
-    d.x = ld_once(x + r, pf); d.c = ld_stream(c + r, pf); d.lo = ld_stream(lo + r, pf);
-    d.hi = ld_stream(hi + r, pf);
+    d.x = ld_once(x + r, pf); d.c = ld_stream(c + r, pf);
+    if (uniform_bounds) {
+      d.lo = lo0;
+      d.hi = hi0;
+    } else {
+      d.lo = ld_stream(lo + r, pf);
+      d.hi = ld_stream(hi + r, pf);
+    }
     d.x0 = halpern ? ld_stream(x0 + r, pf) : 0.0;
     return d;
   }
@@ -1641,6 +1651,7 @@ int op_primal(const gridlp_src_t* src, const gridlp_primal_t* pv, const gridlp_s
   OpPrimal op{};
   op.x = pv->x; op.xbar = pv->x_bar; op.x0 = pv->x_anchor; op.c = pv->c; op.lo = pv->lo; op.hi = pv->hi;
   op.step = d_step; op.iter = iter; op.halpern = (flags & GRIDLP_F_HALPERN) != 0;
+  op.uniform_bounds = (flags & GRIDLP_F_UNIFORM_BOUNDS) != 0 && pv->n > 0;
   return launch_op(src, op, nullptr, stream, "op_primal", cross);
 }
 
@@ -1760,84 +1771,85 @@ int gridlp_pdhg_iterate(const gridlp_src_t* primal_src, const gridlp_primal_t* p
   return n_iters > 0 ? gridlp_op_step_advance(d_step, n_iters, stream) : GRIDLP_OK;
 }
 
-int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_primal_t* pv, const gridlp_src_t* dual_src,
-                                const gridlp_dual_t* dv, gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,
-                                void* stream) {
-  if (!primal_src || !dual_src || !pv || !dv || !d_step || n_iters < 0)
-    return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: bad argument");
+int gridlp_cluster_plan(const gridlp_src_t* primal_src, const gridlp_src_t* dual_src, int64_t* plan,
+                        int64_t plan_len) {
+  if (!primal_src || !dual_src || !plan || plan_len < GRIDLP_CLUSTER_PLAN_LEN)
+    return fail(GRIDLP_ERR_ARG, "cluster_plan: bad argument");
   const gridlp_csr_t* AT = primal_src->A;
   const gridlp_csr_t* A = dual_src->A;
-  if (!AT || !A) return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: needs fused sources");
+  if (!AT || !A) return fail(GRIDLP_ERR_ARG, "cluster_plan: needs fused sources");
   int rc = check_csr(AT);
   if (!rc) rc = check_csr(A);
   if (rc) return rc;
-  if (AT->num_rows != pv->n || A->num_rows != dv->m || AT->num_cols != A->num_rows || A->num_cols != AT->num_rows)
-    return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: length mismatch");
+  if (AT->num_cols != A->num_rows || A->num_cols != AT->num_rows)
+    return fail(GRIDLP_ERR_ARG, "cluster_plan: A and A^T shapes disagree");
   if (AT->num_long_rows > 0 || A->num_long_rows > 0 || AT->carry || A->carry)
-    return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_cluster: long rows / column bands need the graph path");
+    return fail(GRIDLP_ERR_UNSUPPORTED, "cluster_plan: long rows / column bands need the graph path");
   const int64_t n = AT->num_rows, m = A->num_rows;
   constexpr int64_t SMEM_MAX = 227 * 1024;
-  // quick reject before reading any offsets: the replicas alone
   if (8 * (n + m) + 12 * (AT->nnz + A->nnz) / CLUSTER_CTAS > SMEM_MAX || AT->num_slices > (1 << 16) ||
       A->num_slices > (1 << 16))
-    return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_cluster: LP does not fit one cluster's shared memory");
-  // the plan (entry-balanced slice ranges and the exact shared memory of the
-  // largest CTA) is computed once per matrix pair from its slice offsets
-  struct Cached {
-    const void* at;
-    const void* a;
-    ClusterPlan plan;
-    int64_t smem;
-  };
-  static Cached cache[8];
-  static int ncache = 0, next_slot = 0;
-  const Cached* hit = nullptr;
-  for (int q = 0; q < ncache; ++q)
-    if (cache[q].at == AT->slice_off && cache[q].a == A->slice_off) hit = &cache[q];
-  if (!hit) {
-    Cached c{AT->slice_off, A->slice_off, {}, 0};
-    auto balance = [](const std::vector<int64_t>& off, int64_t* b) {
-      const int64_t ns = (int64_t)off.size() - 1;
-      const int64_t total = off[ns] + 64 * ns;
-      int64_t s = 0;
-      b[0] = 0;
-      for (int q = 1; q < CLUSTER_CTAS; ++q) {
-        const int64_t target = total * q / CLUSTER_CTAS;
-        while (s < ns && off[s] + 64 * s < target) ++s;
-        b[q] = s;
-      }
-      b[CLUSTER_CTAS] = ns;
-    };
-    std::vector<int64_t> po(AT->num_slices + 1), dofs(A->num_slices + 1);
-    if (cudaMemcpy(po.data(), AT->slice_off, 8 * po.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(dofs.data(), A->slice_off, 8 * dofs.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
-      return fail(GRIDLP_ERR_CUDA, "pdhg_iterate_cluster: slice offsets");
-    balance(po, c.plan.pb);
-    balance(dofs, c.plan.db);
-    auto need = [](const std::vector<int64_t>& off, int64_t s0, int64_t s1, int nv) {
-      const int64_t rows = 32 * (s1 - s0);
-      return 12 * (off[s1] - off[s0]) + 4 * rows + 8 * (s1 - s0 + 1) + 8 * nv * rows + 64;
-    };
-    int64_t mx = 0;
-    for (int q = 0; q < CLUSTER_CTAS; ++q) {
-      const int64_t a = need(po, c.plan.pb[q], c.plan.pb[q + 1], 5);
-      const int64_t b = need(dofs, c.plan.db[q], c.plan.db[q + 1], 4);
-      mx = std::max(mx, ((a + 15) & ~int64_t(15)) + b);
+    return fail(GRIDLP_ERR_UNSUPPORTED, "cluster_plan: LP does not fit one cluster's shared memory");
+  // entry-balanced slice ranges per CTA and the exact shared memory of the
+  // largest CTA, from the slice offsets (synchronous D2H, a few KB)
+  std::vector<int64_t> po(AT->num_slices + 1), dofs(A->num_slices + 1);
+  if (cudaMemcpy(po.data(), AT->slice_off, 8 * po.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(dofs.data(), A->slice_off, 8 * dofs.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(GRIDLP_ERR_CUDA, "cluster_plan: slice offsets");
+  auto balance = [](const std::vector<int64_t>& off, int64_t* b) {
+    const int64_t ns = (int64_t)off.size() - 1;
+    const int64_t total = off[ns] + 64 * ns;
+    int64_t s = 0;
+    b[0] = 0;
+    for (int q = 1; q < CLUSTER_CTAS; ++q) {
+      const int64_t target = total * q / CLUSTER_CTAS;
+      while (s < ns && off[s] + 64 * s < target) ++s;
+      b[q] = s;
     }
-    c.smem = 8 * (n + m) + mx + 64;
-    const int slot = ncache < 8 ? ncache++ : (next_slot++ & 7);
-    cache[slot] = c;
-    hit = &cache[slot];
+    b[CLUSTER_CTAS] = ns;
+  };
+  int64_t* pb = plan;
+  int64_t* db = plan + CLUSTER_CTAS + 1;
+  balance(po, pb);
+  balance(dofs, db);
+  auto need = [](const std::vector<int64_t>& off, int64_t s0, int64_t s1, int nv) {
+    const int64_t rows = 32 * (s1 - s0);
+    return 12 * (off[s1] - off[s0]) + 4 * rows + 8 * (s1 - s0 + 1) + 8 * nv * rows + 64;
+  };
+  int64_t mx = 0;
+  for (int q = 0; q < CLUSTER_CTAS; ++q) {
+    const int64_t x = need(po, pb[q], pb[q + 1], 5);
+    const int64_t y = need(dofs, db[q], db[q + 1], 4);
+    mx = std::max(mx, ((x + 15) & ~int64_t(15)) + y);
   }
-  const int64_t per_cta = hit->smem;
-  if (per_cta > SMEM_MAX)
-    return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_cluster: LP does not fit one cluster's shared memory");
+  const int64_t smem = 8 * (n + m) + mx + 64;
+  plan[2 * (CLUSTER_CTAS + 1)] = smem;
+  if (smem > SMEM_MAX) return fail(GRIDLP_ERR_UNSUPPORTED, "cluster_plan: LP does not fit one cluster's shared memory");
+  return GRIDLP_OK;
+}
+
+int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_primal_t* pv, const gridlp_src_t* dual_src,
+                                const gridlp_dual_t* dv, gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,
+                                const int64_t* plan, void* stream) {
+  if (!primal_src || !dual_src || !pv || !dv || !d_step || n_iters < 0 || !plan)
+    return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: bad argument");
+  const gridlp_csr_t* AT = primal_src->A;
+  const gridlp_csr_t* A = dual_src->A;
+  if (!AT || !A || AT->num_rows != pv->n || A->num_rows != dv->m)
+    return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: needs fused sources of matching lengths");
+  const int64_t smem = plan[2 * (CLUSTER_CTAS + 1)];
+  if (smem <= 0 || smem > 227 * 1024) return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: plan from gridlp_cluster_plan");
   if (n_iters == 0) return GRIDLP_OK;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(cluster_iterate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(cluster_iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX);
+    cudaFuncSetAttribute(cluster_iterate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
+  }
+  ClusterPlan cp;
+  for (int q = 0; q <= CLUSTER_CTAS; ++q) {
+    cp.pb[q] = plan[q];
+    cp.db[q] = plan[CLUSTER_CTAS + 1 + q];
   }
   OpPrimal pop{};
   pop.x = pv->x; pop.xbar = pv->x_bar; pop.x0 = pv->x_anchor; pop.c = pv->c; pop.lo = pv->lo; pop.hi = pv->hi;
@@ -1848,13 +1860,10 @@ int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_pri
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CLUSTER_CTAS);
   cfg.blockDim = dim3(CLUSTER_TPB);
-  cfg.dynamicSmemBytes = (size_t)per_cta;
+  cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, cluster_iterate_kernel, *AT, *A, pop, dop, n_iters, d_step, hit->plan);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(GRIDLP_ERR_UNSUPPORTED, std::string("pdhg_iterate_cluster: ") + cudaGetErrorString(e));
-  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, cluster_iterate_kernel, *AT, *A, pop, dop, n_iters, d_step, cp);
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("pdhg_iterate_cluster: ") + cudaGetErrorString(e));
   return GRIDLP_OK;
 }
 

@@ -186,7 +186,7 @@ __global__ void permute_fill_kernel(const int32_t* __restrict__ ptr, const int32
 // SELL-32 plan: one warp per 32-row window, lane = row & 31; long rows (length >
 // light_row_max) and rows past the end take the last lanes as empty (-1).
 __global__ void sell_plan_kernel(const int32_t* __restrict__ ptr, int64_t nrows, int32_t light_row_max,
-                                 int32_t* __restrict__ lane_info, int32_t* __restrict__ slice_elems,
+                                 int32_t* __restrict__ lane_info, int64_t* __restrict__ slice_elems,
                                  int32_t* __restrict__ rank_of, char* __restrict__ long_flag,
                                  int32_t* __restrict__ long_len, int64_t nslices) {
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -210,7 +210,7 @@ __global__ void sell_plan_kernel(const int32_t* __restrict__ ptr, int64_t nrows,
   }
   lane_info[s * 32 + lane] = eff >= 0 ? ((eff << 8) | lane) : -1;
   if (row < nrows) rank_of[row] = lane;
-  if (lane == 0) slice_elems[s] = 32 * mx;
+  if (lane == 0) slice_elems[s] = 32 * (int64_t)mx;   // int64: padded entries may pass 2^31
 }
 
 __global__ void iota_kernel(int32_t* __restrict__ out, int64_t n) {
@@ -374,17 +374,20 @@ int gridlp_sell_plan(const int32_t* ptr, int64_t nrows, int32_t light_row_max, i
   Ws w = carve(ws, nrows + 8, nrows + nslices + 2);
   char* flags = reinterpret_cast<char*>(w.vals);
   int64_t* nsel = reinterpret_cast<int64_t*>(w.vals + (nrows + 7) / 8 + 1);
+  // per-slice padded entry counts, scanned in int64 (a block's padded SELL
+  // entries may pass 2^31 even when its nonzeros do not)
+  int64_t* elems = reinterpret_cast<int64_t*>(w.vals + (nrows + 7) / 8 + 2);
   int32_t* hlen = w.keys;
   int32_t* ids = w.aux2;
   int rc;
-  if ((rc = cuda_ok(cudaMemsetAsync(w.aux, 0, 4 * (size_t)(nslices + 1), s), "sell_plan memset"))) return rc;
+  if ((rc = cuda_ok(cudaMemsetAsync(elems, 0, 8 * (size_t)(nslices + 1), s), "sell_plan memset"))) return rc;
   if (nslices > 0) {
-    sell_plan_kernel<<<warps_grid(nslices), 256, 0, s>>>(ptr, nrows, light_row_max, lane_info, w.aux, rank_of, flags,
+    sell_plan_kernel<<<warps_grid(nslices), 256, 0, s>>>(ptr, nrows, light_row_max, lane_info, elems, rank_of, flags,
                                                          hlen, nslices);
     if ((rc = cuda_ok(cudaGetLastError(), "sell_plan"))) return rc;
   }
   size_t tb = w.cub_bytes;
-  if ((rc = cuda_ok(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.aux, slice_off, (int)(nslices + 1), s), "plan scan")))
+  if ((rc = cuda_ok(cub::DeviceScan::ExclusiveSum(w.cub, tb, elems, slice_off, (int)(nslices + 1), s), "plan scan")))
     return rc;
   if ((rc = cuda_ok(cudaMemsetAsync(nsel, 0, 8, s), "sell_plan memset2"))) return rc;
   if (nrows > 0) {

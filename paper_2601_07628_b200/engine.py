@@ -145,6 +145,7 @@ class ColState:
     v: torch.Tensor
     s: torch.Tensor
     scale: torch.Tensor | None = None     # Dc of a scaled LP (KKT on the original LP)
+    uniform_bounds: bool = False          # every variable bounded by lo[0], hi[0] (GRIDLP_F_UNIFORM_BOUNDS)
 
 
 @dataclass
@@ -395,6 +396,10 @@ class PdhgEngine:
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64),
                                     t(self._kkt_scale[0] if dev_vec else self._kkt_scale[0].cpu().numpy())
                                     if self._kkt_scale is not None else None)
+        for col in self.cols.values():
+            if col.n and col.lo.is_cuda:
+                col.uniform_bounds = bool(torch.equal(col.lo, col.lo[:1].expand(col.n))
+                                          and torch.equal(col.hi, col.hi[:1].expand(col.n)))
         kw = dict(exact_row_max=self.opts.exact_row_max,
                   light_row_max=self.opts.light_row_max if self.opts.light_row_max is not None
                   else DEFAULT_LIGHT_ROW_MAX)
@@ -984,26 +989,19 @@ class PdhgEngine:
                                 and not self._banded and 0 < nnz <= self.opts.persistent_max_nnz)
         return self._persist_ok
 
-    def _cluster_first(self, count: int) -> bool:
-        """True when the cluster launch takes this chunk (it is one launch
-        already, and its first call per matrix reads offsets synchronously,
-        so it is not graph-captured); decided by trying it once."""
-        if not self._cluster():
-            return False
-        if getattr(self, "_cluster_tried", False):
-            return self._cluster_ok
-        self._cluster_tried = True
-        (j, col), = self.cols.items()
-        (i, row), = self.rows.items()
-        # probe with zero iterations: validates the fit without touching state
-        self._cluster_ok = self.ops.iterate_cluster(self.plan_primal[j][2], col, self.plan_dual[i][2], row, 0,
-                                                    self.opts.halpern)
-        return self._cluster_ok
-
     def _cluster(self) -> bool:
+        """Tiny single-block LP that fits one thread-block cluster: each
+        chunk is one cluster launch (no graph; the plan is computed once,
+        outside any capture)."""
         if getattr(self, "_cluster_ok", None) is None:
-            self._cluster_ok = (self.opts.cluster_small and self.R == 1 and self.C == 1
-                                and hasattr(self.ops, "iterate_cluster") and not self._banded)
+            ok = (self.opts.cluster_small and self.R == 1 and self.C == 1
+                  and hasattr(self.ops, "cluster_plan") and not self._banded)
+            self._cluster_plan = None
+            if ok:
+                (j, _), = self.cols.items()
+                (i, _), = self.rows.items()
+                self._cluster_plan = self.ops.cluster_plan(self.plan_primal[j][2], self.plan_dual[i][2])
+            self._cluster_ok = self._cluster_plan is not None
         return self._cluster_ok
 
     def _launch_iterations(self, count: int):
@@ -1013,9 +1011,9 @@ class PdhgEngine:
             (j, col), = self.cols.items()
             (i, row), = self.rows.items()
             if self._cluster():
-                if ops.iterate_cluster(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h):
-                    return
-                self._cluster_ok = False          # does not fit: the other paths
+                ops.iterate_cluster(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h,
+                                    self._cluster_plan)
+                return
             if self._persistent():
                 if ops.iterate_persistent(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h):
                     return
@@ -1079,7 +1077,7 @@ class PdhgEngine:
 
     def _run_iterations_inner(self, count: int):
         g = max(1, min(self.opts.graph_chunk, self.opts.kkt_interval))
-        if not self._graphable() or count < g or self._persistent() or self._cluster_first(count):
+        if not self._graphable() or count < g or self._persistent() or self._cluster():
             self._launch_iterations(count)
             return
         if self._graph is None:

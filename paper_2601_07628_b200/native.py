@@ -27,6 +27,8 @@ ROW_MAX_LIMIT = 65536
 F_HALPERN = 1
 F_SUMSQ = 2
 F_STREAM = 4
+F_UNIFORM_BOUNDS = 8
+CLUSTER_PLAN_LEN = 35
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -109,8 +111,9 @@ SIGNATURES = {
     "gridlp_pdhg_iterate": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32, c_uint32, _P],
                             c_int),
     "gridlp_persistent_scratch_bytes": ([], ctypes.c_size_t),
+    "gridlp_cluster_plan": ([POINTER(Src), POINTER(Src), POINTER(c_int64), c_int64], c_int),
     "gridlp_pdhg_iterate_cluster": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,
-                                     c_uint32, _P], c_int),
+                                     c_uint32, POINTER(c_int64), _P], c_int),
     "gridlp_pdhg_iterate_persistent": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,
                                         c_uint32, _P, _P], c_int),
     "gridlp_setup_workspace_bytes": ([c_int64, c_int64], ctypes.c_size_t),

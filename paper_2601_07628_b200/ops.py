@@ -57,6 +57,13 @@ def _heavy(src) -> int:
     return src.mat.launches() - 1 if isinstance(src, Fused) else 0
 
 
+def _pflags(col, halpern: bool) -> int:
+    """Flags of a primal op: Halpern, and uniform variable bounds (the op
+    then reads lo[0], hi[0] instead of two n-vectors)."""
+    return (native.F_HALPERN if halpern else 0) | (native.F_UNIFORM_BOUNDS if getattr(col, "uniform_bounds", False)
+                                                   else 0)
+
+
 def _ptr(t):
     return t.data_ptr() if t is not None and t.numel() else None
 
@@ -174,7 +181,7 @@ class CudaOps:
     def primal(self, src, col, it: int, halpern: bool):
         self.launches += 1 + _heavy(src)
         self.lib.call("gridlp_op_primal", self.src(src), self.primal_struct(col),
-                      self.step.data_ptr(), it, native.F_HALPERN if halpern else 0, self.stream())
+                      self.step.data_ptr(), it, _pflags(col, halpern), self.stream())
 
     def dual(self, src, row, it: int, halpern: bool):
         self.launches += 1 + _heavy(src)
@@ -227,7 +234,7 @@ class CudaOps:
         (gridlp_pdhg_iterate), step counter advanced on the device."""
         self.launches += count * (2 + _heavy(psrc) + _heavy(dsrc)) + (1 if count else 0)
         self.lib.call("gridlp_pdhg_iterate", self.src(psrc), self.primal_struct(col), self.src(dsrc),
-                      self.dual_struct(row), self.step.data_ptr(), int(count), native.F_HALPERN if halpern else 0,
+                      self.dual_struct(row), self.step.data_ptr(), int(count), _pflags(col, halpern),
                       self.stream())
 
     def iterate_persistent(self, psrc, col, dsrc, row, count: int, halpern: bool) -> bool:
@@ -249,19 +256,24 @@ class CudaOps:
         self.launches += 1 if count else 0
         return True
 
-    def iterate_cluster(self, psrc, col, dsrc, row, count: int, halpern: bool) -> bool:
-        """count fused iterations of a tiny single-block LP in one cluster
-        launch (gridlp_pdhg_iterate_cluster). False (nothing launched) when
-        the LP does not fit one cluster's shared memory."""
-        rc = self.lib._lib.gridlp_pdhg_iterate_cluster(
-            self.src(psrc), self.primal_struct(col), self.src(dsrc), self.dual_struct(row), self.step.data_ptr(),
-            int(count), native.F_HALPERN if halpern else 0, self.stream())
-        if rc == 4:              # GRIDLP_ERR_UNSUPPORTED
-            return False
+    def cluster_plan(self, psrc, dsrc):
+        """gridlp_cluster_plan for a matrix pair: the host plan array, or None
+        when the LP does not fit one cluster (GRIDLP_ERR_UNSUPPORTED)."""
+        plan = (ctypes.c_int64 * native.CLUSTER_PLAN_LEN)()
+        rc = self.lib._lib.gridlp_cluster_plan(self.src(psrc), self.src(dsrc), plan, native.CLUSTER_PLAN_LEN)
+        if rc == 4:
+            return None
         if rc != 0:
-            raise native.GridlpError(f"gridlp_pdhg_iterate_cluster failed ({rc}): {self.lib.last_error()}")
+            raise native.GridlpError(f"gridlp_cluster_plan failed ({rc}): {self.lib.last_error()}")
+        return plan
+
+    def iterate_cluster(self, psrc, col, dsrc, row, count: int, halpern: bool, plan):
+        """count fused iterations of a tiny single-block LP in one cluster
+        launch (gridlp_pdhg_iterate_cluster) with a plan of cluster_plan()."""
+        self.lib.call("gridlp_pdhg_iterate_cluster", self.src(psrc), self.primal_struct(col), self.src(dsrc),
+                      self.dual_struct(row), self.step.data_ptr(), int(count), _pflags(col, halpern), plan,
+                      self.stream())
         self.launches += 1 if count else 0
-        return True
 
     def step_advance(self, delta: int):
         self.launches += 1

@@ -1,6 +1,7 @@
 """µs per PDHG iteration of small LPs (the launch-bound regime of BASELINE
-configs[0]) with the persistent cooperative launch vs the CUDA-graph path
-(kernel per product, chained), and time to 1e-4 for cfg1 both ways.
+configs[0]): the persistent cooperative launch, the CUDA-graph path (kernel
+per product, chained) and the cluster launch (falls back to the graph path
+when the LP does not fit), and time to 1e-4 for cfg1 each way.
 
     python tools/persistent_sweep.py
 """
@@ -40,13 +41,16 @@ def main():
     for m, n, nnz in ((2000, 4000, 20000), (6000, 12000, 60000), (20000, 40000, 200000), (60000, 120000, 600000)):
         p = generate(GeneratorSpec(kind="uniform_random", num_rows=m, num_cols=n, nnz_target=nnz,
                                    inequality_fraction=0.3, seed=0))
-        on = per_iter(p, {"persistent_max_nnz": 1 << 30})
-        off = per_iter(p, {"persistent_max_nnz": 0})
-        print(json.dumps({"m": m, "n": n, "nnz": nnz, "persistent_us_per_iter": on, "graph_us_per_iter": off}),
-              flush=True)
+        on = per_iter(p, {"persistent_max_nnz": 1 << 30, "cluster_small": False})
+        off = per_iter(p, {"persistent_max_nnz": 0, "cluster_small": False})
+        cl = per_iter(p, {"persistent_max_nnz": 0, "cluster_small": True})
+        print(json.dumps({"m": m, "n": n, "nnz": nnz, "persistent_us_per_iter": on, "graph_us_per_iter": off,
+                          "cluster_or_fallback_us_per_iter": cl}), flush=True)
     p = generate(GeneratorSpec(kind="uniform_random", num_rows=2000, num_cols=4000, nnz_target=20000,
                                inequality_fraction=0.3, seed=0))
-    for name, over in (("persistent", {"persistent_max_nnz": 1 << 30}), ("graph", {"persistent_max_nnz": 0})):
+    for name, over in (("persistent", {"persistent_max_nnz": 1 << 30, "cluster_small": False}),
+                       ("graph", {"persistent_max_nnz": 0, "cluster_small": False}),
+                       ("cluster", {"persistent_max_nnz": 0, "cluster_small": True})):
         _solve(p, SolverConfig(tolerance=1e-4, seed=0), engine_overrides=over)
         walls = []
         for _ in range(3):
