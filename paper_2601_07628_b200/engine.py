@@ -425,7 +425,10 @@ class PdhgEngine:
                 torch.cuda.synchronize(dev)
                 t2 = time.perf_counter()
                 da = self._block_auto(setup, a, self.col_order[j] if self.sorted else None)
+                del a                   # each CSR input goes as soon as its SELL copy exists (peak HBM)
+                a = None
                 dt = self._block_auto(setup, at, self.row_order[i] if self.sorted else None)
+                at = None
                 torch.cuda.synchronize(dev)
                 t3 = time.perf_counter()
                 tm["setup_extract_s"] = tm.get("setup_extract_s", 0.0) + t1 - t0
