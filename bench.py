@@ -275,6 +275,11 @@ def iteration_bytes(engine) -> dict:
         out["K1"] += 12 * nnz + 4 * (n + 1) + 8 * m + 56 * n
         out["K2"] += 12 * nnz + 4 * (m + 1) + 8 * n + 40 * m
     out["iteration"] = out["K1"] + out["K2"]
+    # bytes the kernels actually have to move on this instance: with uniform
+    # variable bounds (GRIDLP_F_UNIFORM_BOUNDS) K1 reads two scalars instead
+    # of the two n-vectors lo, hi
+    out["iteration_moved"] = out["iteration"] - sum(
+        16 * c.n for c in engine.cols.values() if getattr(c, "uniform_bounds", False))
     # L1->L2 requests: one 32-byte sector request per gathered element (random
     # columns: no two lanes of a warp share a 128-byte line) plus one request
     # per 128-byte line of every streamed array
@@ -651,6 +656,11 @@ def run_ours(args, rank, world, local_rank):
                      "bytes_per_launch": bytes_["iteration"], "seconds_per_launch": t_iter,
                      "peak_source": peak_src,
                      "frac_of_8TBs": achieved / 8000.0,
+                     "bytes_per_launch_moved": bytes_["iteration_moved"],
+                     "frac_moved": bytes_["iteration_moved"] / t_iter / 1e9 / peak,
+                     "moved_note": "frac uses SURVEY 8d's byte model (24 nnz + 68 n + 52 m); frac_moved drops the "
+                                   "16 B/column of lo/hi the primal kernel skips when every variable has the same "
+                                   "bounds (GRIDLP_F_UNIFORM_BOUNDS, true for the reference generator's box)",
                      "request_bound": {
                          "requests_per_iteration": bytes_["requests"],
                          "ceiling_requests_per_s": GATHER_CEILING_PER_S,
