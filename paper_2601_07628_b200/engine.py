@@ -1093,12 +1093,32 @@ class PdhgEngine:
             stream = torch.cuda.Stream(self.device)
             graph = torch.cuda.CUDAGraph()
             before = getattr(self.ops, "launches", 0)
-            with torch.cuda.stream(stream):
-                graph.capture_begin()
+            if self.comm.kind == "nccl":
+                # collectives inside a capture: fall back to eager launches if
+                # this NCCL / driver combination refuses (never observed on one
+                # rank; a multi-GPU first)
+                torch.cuda.synchronize(self.device)
                 try:
-                    self._launch_iterations(g)
-                finally:
-                    graph.capture_end()
+                    with torch.cuda.stream(stream):
+                        graph.capture_begin()
+                        try:
+                            self._launch_iterations(g)
+                        finally:
+                            graph.capture_end()
+                except RuntimeError as exc:
+                    log.warning("CUDA-graph capture of the NCCL iterations failed (%s); running eager", exc)
+                    self.opts.graph_nccl = False
+                    torch.cuda.synchronize(self.device)
+                    if count:
+                        self._launch_iterations(count)   # captures do not execute: all remaining eagerly
+                    return
+            else:
+                with torch.cuda.stream(stream):
+                    graph.capture_begin()
+                    try:
+                        self._launch_iterations(g)
+                    finally:
+                        graph.capture_end()
             self._graph_launches = getattr(self.ops, "launches", 0) - before
             if hasattr(self.ops, "launches"):
                 self.ops.launches = before     # capture records, it does not launch
