@@ -255,7 +255,7 @@ def kernel_tuning() -> dict:
     from paper_2601_07628_b200 import native
 
     lib = native.load()
-    return {k: lib.get_tuning(k) for k in ("sell_variant", "tma_ctas_per_sm", "chain_products")}
+    return {k: lib.get_tuning(k) for k in ("sell_variant", "chain_products")}
 
 
 def workload_name(cfg: str) -> str:
@@ -739,7 +739,7 @@ def main():
     ap.add_argument("--force-nccl", action="store_true",
                     help="run the NCCL executor even at world size 1 (exercises the multi-GPU path on one GPU)")
     ap.add_argument("--tuning", action="append", default=[],
-                    help="KEY=VALUE kernel knob (gridlp_set_tuning: sell_variant, tma_ctas_per_sm, chain_products)")
+                    help="KEY=VALUE kernel knob (gridlp_set_tuning: sell_variant, chain_products)")
     ap.add_argument("--cpu-sample-iters", type=int, default=24)
     ap.add_argument("--ref-sample-iters", type=int, default=4)
     args = ap.parse_args()

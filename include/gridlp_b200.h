@@ -246,11 +246,9 @@ int gridlp_enable_peer_access(int peer_device);
 int64_t gridlp_op_slots(const gridlp_src_t* src);
 /* Process-wide kernel knobs (no reference counterpart; results are
  * bit-identical for every value — they pick kernels, not arithmetic):
- *   "sell_variant"    0 = SELL lanes with LSU streams (one slice per warp,
- *                     default), 1..4 = TMA-staged streams, persistent warps
- *                     (stages x depth 8x2, 8x3, 16x2, 4x4), 5 = LSU streams
- *                     issued one step block ahead of the gathers
- *   "tma_ctas_per_sm" cap on resident CTAs of the TMA kernel (0 = occupancy)
+ *   "sell_variant"    1 = SELL lanes with the column/value streams issued
+ *                     one step block ahead of the gathers (default),
+ *                     0 = the round-1 kernel (streams, then gathers)
  *   "chain_products"  gridlp_pdhg_iterate chains its products by
  *                     programmatic dependent launch (default 1)
  * Unknown key or out-of-range value: GRIDLP_ERR_ARG. get returns -1 for an

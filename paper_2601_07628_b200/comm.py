@@ -216,6 +216,8 @@ class NcclGrid:
         storage padded to G*S) into every member's copy, in place."""
         group = self._axis_group(axis, index)
         G = self.rows if axis == "R" else self.cols
+        if vec.storage_offset() != 0 or vec.untyped_storage().nbytes() < G * S * vec.element_size():
+            raise ValueError("gather_shard needs a view at the start of storage padded to G*S elements")
         full = torch.as_strided(vec, (G * S,), (1,))      # the padded storage behind the view
         mine = full[me * S:(me + 1) * S]
         if self._gloo_cuda(group, full):

@@ -1170,6 +1170,27 @@ constexpr int CLUSTER_CTAS = 16;     // non-portable cluster size (B200: 16)
 constexpr int CLUSTER_TPB = 256;
 constexpr int CLUSTER_WARPS = CLUSTER_TPB / 32;
 
+// a lane's sequential row sum from shared memory: indices, then the replica
+// values, PERSIST_U entries at a time in flight, then the in-order add chain
+__device__ __forceinline__ double cluster_row_sum(const SmemSlices& S, int64_t base, int len, const double* rep) {
+  double s = 0.0;
+  for (int j = 0; j < len; j += PERSIST_U) {
+    int c[PERSIST_U];
+    double x[PERSIST_U], v[PERSIST_U];
+#pragma unroll
+    for (int u = 0; u < PERSIST_U; ++u) c[u] = (j + u < len) ? S.cols[base + 32 * (j + u)] : 0;
+#pragma unroll
+    for (int u = 0; u < PERSIST_U; ++u) {
+      x[u] = rep[c[u]];
+      v[u] = (j + u < len) ? S.vals[base + 32 * (j + u)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PERSIST_U; ++u)
+      if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
+  }
+  return s;
+}
+
 // slice ranges of the CTAs, balanced by SELL entries (host: cluster_plan)
 struct ClusterPlan {
   int64_t pb[CLUSTER_CTAS + 1];       // primal product (A^T) slice boundaries
@@ -1213,8 +1234,7 @@ __global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(CLUSTER_T
       if (info < 0) continue;
       const int len = info >> 8;
       const int64_t base = P.off[ls] + lane;
-      double aty = 0.0;
-      for (int j = 0; j < len; ++j) aty = dadd(aty, dmul(P.vals[base + 32 * j], y_r[P.cols[base + 32 * j]]));
+      const double aty = cluster_row_sum(P, base, len, y_r);
       const int64_t r = 32 * (ps0 + ls) + lane;
       const double xv = P.v[0][k];
       const double xh = np_clip(dsub(xv, dmul(p.tau, dsub(P.v[1][k], aty))), P.v[2][k], P.v[3][k]);
@@ -1233,8 +1253,7 @@ __global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(CLUSTER_T
       if (info < 0) continue;
       const int len = info >> 8;
       const int64_t base = D.off[ls] + lane;
-      double z = 0.0;
-      for (int j = 0; j < len; ++j) z = dadd(z, dmul(D.vals[base + 32 * j], xbar_r[D.cols[base + 32 * j]]));
+      const double z = cluster_row_sum(D, base, len, xbar_r);
       const int64_t r = 32 * (ds0 + ls) + lane;
       const double yv = D.v[0][k];
       const double yh = dual_map(yv, z, d.sigma, D.v[1][k], D.v[2][k]);

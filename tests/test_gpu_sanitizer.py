@@ -26,7 +26,7 @@ def test_sanitizer_clean(tool):
     if not Path(SAN).exists():  # pragma: no cover
         pytest.skip("compute-sanitizer not installed")
     cmd = [SAN, "--tool", tool, "--error-exitcode", "99", "--print-limit", "20",
-           "--kernel-name", "regex=sell32|heavy_chunk|long_row|rows_kernel|reduce_kernel|terms_reduce|step_advance|epoch_advance",
+           "--kernel-name", "regex=sell32|heavy_chunk|long_row|rows_kernel|reduce_kernel|terms_reduce|step_advance|epoch_advance|persistent|cluster",
            sys.executable, str(ROOT / "tools" / "sanitizer_case.py")]
     env = dict(os.environ, PYTHONPATH=str(ROOT))
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env)

@@ -1,8 +1,10 @@
 """Small workload for compute-sanitizer (tests/test_gpu_sanitizer.py): every
-kernel family of the hot path on one LP — SELL lanes (both variants),
-warp-per-row long rows (shared-memory add chain), chunked heavy rows (the
-cross-CTA arrival counter), fused KKT / probe reductions, chained products
-in a captured graph, the 2x2 virtual grid's partial sums, power iteration."""
+kernel family of the hot path — SELL lanes (both variants), warp-per-row
+long rows (shared-memory add chain), chunked heavy rows (the cross-CTA
+arrival counter), fused KKT / probe reductions, chained products in a
+captured graph, the 2x2 virtual grid's partial sums, power iteration, the
+persistent cooperative launch and the thread-block-cluster launch (DSMEM
+broadcasts, cluster barriers)."""
 
 import sys
 from pathlib import Path
@@ -42,6 +44,12 @@ def main():
     r = _solve(p, SolverConfig(tolerance=1e-6, max_iterations=192, seed=1),
                engine_overrides={"persistent_max_nnz": 1 << 30})      # the persistent cooperative launch
     print(f"persistent: {r.status} it={r.iterations} obj={r.objective:.10g}")
+    from paper_2601_07628_b200 import GeneratorSpec, generate
+
+    q = generate(GeneratorSpec(kind="uniform_random", num_rows=600, num_cols=1000, nnz_target=6000,
+                               inequality_fraction=0.3, seed=2))
+    r = solve(q, SolverConfig(tolerance=1e-6, max_iterations=192, seed=2))   # all rows light: cluster launch
+    print(f"cluster: {r.status} it={r.iterations} obj={r.objective:.10g}")
     print("SANITIZER_CASE_DONE")
 
 
