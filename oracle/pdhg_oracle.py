@@ -632,15 +632,25 @@ def iteration_rate(problem, iters: int, grid=(1, 1), threads: int = 1, eta: floa
     x0 = [v.copy() for v in xs]
     y0 = [v.copy() for v in ys]
     tau, sigma = eta / omega, eta * omega
+    # with a pool the per-block epilogues run on it too (numpy releases the
+    # GIL), as each device's whole iteration does in the reference's threads
+    # executor (comm.py:185-221)
+    pmap = (lambda f, n: list(g.pool.map(f, range(n)))) if g.pool is not None else (
+        lambda f, n: [f(q) for q in range(n)])
     t0 = time.perf_counter()
     for k in range(iters):
         aty = g.row_products(ys)
-        xh = [primal_map(xs[j], g.c[j], aty[j], tau, g.lv[j], g.uv[j]) for j in range(C)]
-        xb = [2.0 * xh[j] - xs[j] for j in range(C)]
+
+        def primal(j):
+            xh = primal_map(xs[j], g.c[j], aty[j], tau, g.lv[j], g.uv[j])
+            return xh, 2.0 * xh - xs[j]
+        pj = pmap(primal, C)
+        xh = [h for h, _ in pj]
+        xb = [b for _, b in pj]
         z, _ = g.col_products(xb)
-        yh = [dual_map(ys[i], z[i], sigma, g.lc[i], g.uc[i]) for i in range(R)]
-        xs = [anchor_mix(xh[j], xs[j], x0[j], k, 0.0) for j in range(C)]
-        ys = [anchor_mix(yh[i], ys[i], y0[i], k, 0.0) for i in range(R)]
+        yh = pmap(lambda i: dual_map(ys[i], z[i], sigma, g.lc[i], g.uc[i]), R)
+        xs = pmap(lambda j: anchor_mix(xh[j], xs[j], x0[j], k, 0.0), C)
+        ys = pmap(lambda i: anchor_mix(yh[i], ys[i], y0[i], k, 0.0), R)
     dt = time.perf_counter() - t0
     if g.pool is not None:
         g.pool.shutdown()
