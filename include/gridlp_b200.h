@@ -375,7 +375,7 @@ int gridlp_op_step_advance(gridlp_step_t* d_step, int64_t delta, void* stream);
  * gridlp_pdhg_iterate (pdhg_engine.py:394-400). */
 size_t gridlp_persistent_scratch_bytes(void);
 /* n_iters fused iterations of a TINY single-block LP in ONE thread-block
- * cluster launch (16 CTAs): x_bar / y replicated in every CTA's shared
+ * cluster launch (8 CTAs x 512 threads): x_bar / y replicated in every CTA's shared
  * memory, each CTA's slices of A and A^T with their row operands resident
  * there, owners broadcast their new entries through distributed shared
  * memory, hardware cluster barriers between the products. Bit-identical to

@@ -1166,8 +1166,8 @@ __global__ void __launch_bounds__(PERSIST_TPB) persistent_iterate_kernel(gridlp_
 // arithmetic is sell32's (sequential sums, the same epilogue functions), so
 // iterates are the graph path's bit for bit.
 namespace cg = cooperative_groups;
-constexpr int CLUSTER_CTAS = 16;     // non-portable cluster size (B200: 16)
-constexpr int CLUSTER_TPB = 256;
+constexpr int CLUSTER_CTAS = 8;      // portable cluster size (16 measured: 4.68 µs/iteration on cfg1)
+constexpr int CLUSTER_TPB = 512;
 constexpr int CLUSTER_WARPS = CLUSTER_TPB / 32;
 
 // a lane's sequential row sum from shared memory: indices, then the replica

@@ -116,7 +116,7 @@ class EngineOptions:
     # two global-memory grid barriers per iteration cost more than the
     # kernel boundaries PDL already hides
     persistent_max_nnz: int = 0
-    # tiny single-block LPs (vectors + matrix within one 16-CTA cluster's
+    # tiny single-block LPs (vectors + matrix within one 8-CTA cluster's
     # shared memory, e.g. BASELINE configs[0]) run each chunk of iterations
     # in one thread-block-cluster launch (gridlp_pdhg_iterate_cluster,
     # bit-identical iterates); falls back by itself when the LP is too big

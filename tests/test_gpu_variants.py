@@ -135,7 +135,7 @@ def test_persistent_launch_equals_graph_path(heavy):
 
 @pytest.mark.parametrize("seed", [0, 1])
 def test_cluster_launch_equals_graph_path(seed):
-    """gridlp_pdhg_iterate_cluster (one 16-CTA cluster launch per chunk:
+    """gridlp_pdhg_iterate_cluster (one 8-CTA cluster launch per chunk:
     replicated vectors and the matrix in shared memory, DSMEM broadcasts,
     cluster barriers) reproduces the kernel-per-product path bit for bit on
     BASELINE cfg1-shaped LPs; an LP with long rows falls back by itself."""
