@@ -13,7 +13,9 @@ reference's own solves) on the SAME instance:
 * x, y after 8 iterations bit-identical when every row has <= 4096 entries
   (cfg4), else within 1e-8 relative max-norm (cfg3: rows > 4096 are
   deterministic tree sums, and their rounding propagates);
-* KKT residuals and objectives within 1e-9 relative.
+* KKT residuals and objectives within 1e-9 relative;
+* cfg4 again with 4 forced column bands per orientation (carry chains):
+  bit-identical iterates to the unbanded run.
 
 Each case holds the instance on the host for the oracle (~10 / ~25 GB) and
 takes one to a few minutes of CPU time on the GPU box."""
@@ -91,5 +93,20 @@ def test_fixed_step_full_size(name):
     for key in ("r_primal", "r_dual", "r_gap", "obj_primal", "obj_dual"):
         a, b = getattr(got.report, key), getattr(want, key)
         assert abs(a - b) <= 1e-9 * max(abs(b), 1e-300), (key, a, b)
+    if name == "cfg4":
+        # column bands with carry chains at full size: forced 4 bands on both
+        # orientations must reproduce the unbanded run bit for bit
+        from paper_2601_07628_b200.api import _solve
+
+        tb = Keep()
+        banded = _solve(p, SolverConfig(**cfg), trace=tb, force_1x1=True, engine_overrides={"column_bands": 4})
+        assert banded.timings is not None
+        for (it_a, xa, ya), (it_b, xb, yb) in zip(tr, tb):
+            assert it_a == it_b
+            np.testing.assert_array_equal(xa, xb)
+            np.testing.assert_array_equal(ya, yb)
+        assert banded.report == got.report or all(
+            abs(getattr(banded.report, k) - getattr(got.report, k)) <= 1e-12 * max(abs(getattr(got.report, k)), 1e-300)
+            for k in ("r_primal", "r_dual", "r_gap", "obj_primal", "obj_dual"))
     print(f"{name}: nnz={p.matrix.nnz} heavy rows={int((~exact).sum())} "
           f"x8 rel={_relmax(x8, want.trace[8][0]):.2e} y8 rel={_relmax(y8, want.trace[8][1]):.2e}")
