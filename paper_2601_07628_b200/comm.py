@@ -180,11 +180,30 @@ class NcclGrid:
             raise CollectiveTimeout(f"collective {what} timed out after {self.timeout}s")
 
     def reduce(self, axis, index, partials, scratch=None):
+        """Axis sum of the members' partial vectors in ASCENDING member order
+        (the reference's order, comm.py:75-84): all-gather the partials, then
+        add them in order on every member — so every rank holds the same bits
+        as the virtual grid, whatever algorithm / protocol NCCL would pick
+        for an allreduce (NCCL_ALGO / NCCL_PROTO do not matter). Used by the
+        KKT pass and the power iteration; the main loop uses the sharded
+        exchange (exchange / gather_shard), which has the same property."""
         (p,) = partials
-        buf = p if scratch is None else scratch.copy_(p)
-        group = self.col_groups[index] if axis == "R" else self.row_groups[index]
-        if (axis == "R" and self.rows > 1) or (axis == "C" and self.cols > 1):
-            self.dist.all_reduce(buf, group=group)
+        buf = p if scratch is None else scratch
+        group = self._axis_group(axis, index)
+        G = self.rows if axis == "R" else self.cols
+        if G > 1:
+            n = p.numel()
+            stack = torch.empty((G, n), dtype=p.dtype, device=p.device)
+            if self._gloo_cuda(group, p) or self.dist.get_backend(group) != "nccl":
+                outs = list(stack.unbind(0))
+                self.dist.all_gather(outs, p.contiguous(), group=group)
+            else:
+                self.dist.all_gather_into_tensor(stack.view(-1), p.contiguous(), group=group)
+            buf.copy_(stack[0])
+            for q in range(1, G):
+                buf.add_(stack[q])
+        elif scratch is not None:
+            buf.copy_(p)
         return [buf]
 
     def _axis_group(self, axis, index):
