@@ -1014,9 +1014,13 @@ class PdhgEngine:
             (j, col), = self.cols.items()
             (i, row), = self.rows.items()
             if self._cluster():
-                ops.iterate_cluster(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h,
-                                    self._cluster_plan)
-                return
+                try:
+                    ops.iterate_cluster(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h,
+                                        self._cluster_plan)
+                    return
+                except native.GridlpError as exc:        # launch refused (e.g. no cluster scheduling)
+                    log.warning("cluster launch refused (%s); using the kernel-per-product path", exc)
+                    self._cluster_ok = False
             if self._persistent():
                 if ops.iterate_persistent(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h):
                     return
