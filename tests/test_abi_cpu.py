@@ -207,3 +207,37 @@ def test_column_band_split(K, exact, relabel):
             pieces_v.append(b.val[p0:p1].numpy())
         np.testing.assert_array_equal(np.concatenate(pieces_c), col[ptr[r]:ptr[r + 1]])
         np.testing.assert_array_equal(np.concatenate(pieces_v), val[ptr[r]:ptr[r + 1]])
+
+
+def test_tuning_knobs_are_host_only_and_validated(lib):
+    """gridlp_set_tuning / gridlp_get_tuning: kernel-choice knobs (no device
+    work, so checkable here); unknown keys and out-of-range values are
+    GRIDLP_ERR_ARG, get returns -1 for an unknown key."""
+    saved = {k: lib.get_tuning(k) for k in ("sell_variant", "chain_products")}
+    try:
+        lib.set_tuning("sell_variant", 0)
+        assert lib.get_tuning("sell_variant") == 0
+        lib.set_tuning("chain_products", 0)
+        assert lib.get_tuning("chain_products") == 0
+        with pytest.raises(native.GridlpError, match="sell_variant"):
+            lib.set_tuning("sell_variant", 7)
+        with pytest.raises(native.GridlpError, match="unknown key"):
+            lib.set_tuning("no_such_knob", 1)
+        assert lib.get_tuning("no_such_knob") == -1
+    finally:
+        for k, v in saved.items():
+            lib.set_tuning(k, v)
+    assert saved == {"sell_variant": 1, "chain_products": 1}
+
+
+def test_cluster_and_persistent_entry_points_validate_arguments(lib):
+    import ctypes
+
+    with pytest.raises(native.GridlpError, match="bad argument"):
+        lib.call("gridlp_pdhg_iterate_persistent", None, None, None, None, None, 1, 0, None, None)
+    with pytest.raises(native.GridlpError, match="bad argument"):
+        lib.call("gridlp_cluster_plan", None, None, None, 0)
+    plan = (ctypes.c_int64 * native.CLUSTER_PLAN_LEN)()
+    with pytest.raises(native.GridlpError, match="bad argument"):
+        lib.call("gridlp_pdhg_iterate_cluster", None, None, None, None, None, 1, 0, plan, None)
+    assert int(lib._lib.gridlp_persistent_scratch_bytes()) >= 8
