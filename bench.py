@@ -88,22 +88,62 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled DURING the timed region: NVML
+    (pynvml) polled every 5 ms on a helper thread, plus one sample at entry
+    and one at exit, so even a sub-second timed region has samples;
+    `nvidia-smi -lms` as the fallback when pynvml is missing."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index: int):
         self.index = index
+        self.samples = []          # (sm_mhz, max_mhz, reasons bitmask)
+        self._stop = threading.Event()
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nvml = None
         self.proc = None
         self.lines = []
 
+    def _sample(self):
+        p = self._nvml
+        try:
+            sm = float(p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM))
+            try:
+                rs = int(p.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            except AttributeError:
+                rs = int(p.nvmlDeviceGetCurrentClocksThrottleReasons(self._h))
+            self.samples.append((sm, self._max, rs))
+        except Exception:
+            pass
+
+    def _poll(self):
+        while not self._stop.wait(0.005):
+            self._sample()
+
     def __enter__(self):
+        if self._nvml is not None:
+            self._sample()
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
+            return self
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -116,6 +156,11 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self._nvml is not None:
+            self._stop.set()
+            self._t.join(timeout=1)
+            self._sample()
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -125,23 +170,32 @@ class ClockSampler:
 
     def summary(self):
         sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[4:8]):
-                if val.lower() == "active":
-                    reasons.add(name)
+        if self._nvml is not None:
+            for c, mx, rs in self.samples:
+                sm.append(c)
+                smax.append(mx)
+                for name, attr in self.REASONS:
+                    bit = getattr(self._nvml, attr, 0)
+                    if bit and rs & bit:
+                        reasons.add(name)
+        else:
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for line in self.lines:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    smax.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for name, val in zip(names, parts[2:6]):
+                    if val.lower() == "active":
+                        reasons.add(name)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def make_problem(name):

@@ -6,10 +6,10 @@ all_reduce / all_gather on CUDA tensors, so four processes sharing cuda:0
 exercise everything the 8-GPU run does except NCCL itself: per-rank blocks
 built on the device, partial products and the fused epilogues from the
 sm_100a library, axis collectives on device vectors, the once-per-pass
-scalar table and the final x / y gather. With two ranks per reduction group
-an allreduce is one IEEE addition, so a 2x2 grid must reproduce the
-single-process virtual grid bit for bit; wider groups match to FP64
-rounding."""
+scalar table and the final x / y gather. Every axis sum runs in ascending
+member order (the sharded exchange in the main loop, ordered all-gather sums
+elsewhere), so every grid shape reproduces the single-process virtual grid
+bit for bit."""
 
 import os
 import socket
@@ -45,7 +45,7 @@ def _worker(rank, world, port, grid, backend, q):
         if backend == "peer":
             p, cfg = generate(GeneratorSpec(**PEER_CASE)), dict(PEER_CFG)
         else:
-            p, cfg = generate(GeneratorSpec(**CASE)), dict(tolerance=1e-6, seed=6)
+            p, cfg = generate(GeneratorSpec(**CASE)), dict(tolerance=1e-5, seed=6)
         r = solve(p, SolverConfig(**cfg, n_procs=world, grid=grid, comm_backend=backend))
         q.put((rank, r.status, r.iterations, r.restarts, r.x, r.y, r.report.as_dict(), r.counters, r.layout))
         dist.barrier()          # members keep their IPC-shared buffers alive until everyone is done
@@ -78,7 +78,7 @@ def test_multirank_device_path_matches_virtual_grid(grid, bitwise):
 
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     p = generate(GeneratorSpec(**CASE))
-    want = solve(p, SolverConfig(tolerance=1e-6, seed=6, n_procs=grid[0] * grid[1], grid=grid))
+    want = solve(p, SolverConfig(tolerance=1e-5, seed=6, n_procs=grid[0] * grid[1], grid=grid))
     res = _run(grid)
     for rank, status, iters, restarts, x, y, kkt, counters, layout in res:
         assert (status, iters, restarts) == (want.status, want.iterations, want.restarts), rank
@@ -127,7 +127,7 @@ def _band_worker(rank, world, port, grid, q):
 
         spec = PlantedSpec(1500, 2000, 6, seed=13)
         prob = BandProblem(PlantedBands(spec, torch.device("cuda", 0), chunk_draws=6 * 400))
-        r = solve(prob, SolverConfig(tolerance=1e-7, seed=13, n_procs=world, grid=grid, permutation="none",
+        r = solve(prob, SolverConfig(tolerance=1e-6, seed=13, n_procs=world, grid=grid, permutation="none",
                                      partitioning="uniform", comm_backend="nccl", max_iterations=200_000))
         q.put((rank, r.status, r.iterations, r.objective, r.layout["total_nnz"]))
         dist.barrier()
@@ -159,4 +159,4 @@ def test_band_problem_sharded_over_processes_reaches_planted_optimum():
     assert len({(s, it, obj) for _, s, it, obj, _ in out}) == 1      # replicated decisions
     _, status, _, obj, nnz = out[0]
     assert status == "optimal" and nnz > 0
-    assert abs(obj - star) <= 1e-5 * (1.0 + abs(star))
+    assert abs(obj - star) <= 1e-4 * (1.0 + abs(star))
