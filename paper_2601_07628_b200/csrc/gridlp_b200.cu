@@ -812,12 +812,18 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
 // round trip (the gathers) instead of two (streams, then the gathers that
 // depend on them). More registers (fewer warps per SM): it pays on long
 // lanes whose streams miss L2 (power-law rows), not on short ones.
-constexpr int PIPE_MINB = 20;        // 40 warps per SM at <= 51 registers
+#ifndef GRIDLP_PIPE_MINB
+#define GRIDLP_PIPE_MINB 20          // 40 warps per SM at <= 51 registers
+#endif
+#ifndef GRIDLP_PIPE_U
+#define GRIDLP_PIPE_U SELL_U
+#endif
+constexpr int PIPE_MINB = GRIDLP_PIPE_MINB;
 template <class Op>
 __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
                                                                         Op op, double* __restrict__ partials,
                                                                         double* __restrict__ terms, int cross_wait) {
-  constexpr int U = SELL_U;
+  constexpr int U = GRIDLP_PIPE_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
