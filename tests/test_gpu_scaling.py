@@ -122,3 +122,18 @@ def test_scaled_solve_reports_original_kkt_and_matches_unscaled_oracle(seed):
     cx = float(np.dot(q.objective, got.x))
     assert abs(got.report.obj_primal - cx) <= 1e-9 * max(1.0, abs(cx))
     assert got.timings["scaling_s"] > 0
+
+
+def test_scaled_solve_on_a_grid_matches_unscaled_oracle():
+    """Scaling on a 2x2 virtual grid: the KKT scale vectors follow each grid
+    band's internal order (engine ColState / RowState.scale), so the report
+    is still the original LP's and the optimum the unscaled oracle's."""
+    q = generate(GeneratorSpec(kind="uniform_random", num_rows=500, num_cols=800, nnz_target=6000,
+                               inequality_fraction=0.3, seed=9))
+    base = dict(tolerance=1e-9, seed=9, max_iterations=400_000)
+    want = pdhg_oracle.oracle_solve(q, **base)
+    got = solve(q, SolverConfig(**base, n_procs=4, grid=(2, 2), scaling="ruiz+pock_chambolle"))
+    assert got.status == want.status == "optimal"
+    assert abs(got.objective - want.objective) <= 1e-6 * max(1.0, abs(want.objective))
+    rp = _host_rp(q, got.x)
+    assert abs(got.report.r_primal - rp) <= 1e-6 * max(rp, 1e-300) + 1e-15
