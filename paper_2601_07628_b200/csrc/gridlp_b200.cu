@@ -529,6 +529,9 @@ constexpr int SELL_WPB = 2;          // warps (slices) per CTA
 constexpr int SELL_NT = SELL_WPB * 32;
 constexpr int SELL_U = 4;            // steps in flight per lane
 constexpr int SELL_MINB = 32;        // 64 warps per SM at <= 32 registers
+#ifndef GRIDLP_HEAVY_U
+#define GRIDLP_HEAVY_U SELL_U        // heavy-chunk kernel: loads in flight per thread
+#endif
 #ifndef LONG_U
 #define LONG_U 2                     // long-row kernel: 64-entry blocks (registers -> occupancy)
 #endif
@@ -592,7 +595,7 @@ template <class Op>
 __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
                                                               double* __restrict__ partials, double* __restrict__ terms,
                                                               int cross_wait) {
-  constexpr int U = SELL_U;
+  constexpr int U = GRIDLP_HEAVY_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   if (cross_wait) pdl_wait();     // chained to the previous product (see launch_op)
   pdl_launch_dependents();
