@@ -108,8 +108,6 @@ class EngineOptions:
     # a CUDA graph too, as the single-GPU and peer executors do
     graph_nccl: bool = True
     graph_chunk: int = 128
-    # capture the KKT / restart-probe pass in a CUDA graph too (virtual grid)
-    pass_graphs: bool = True
     # single-block LPs up to this many nonzeros run each chunk of iterations
     # as ONE cooperative launch with grid barriers between the products
     # (gridlp_pdhg_iterate_persistent, bit-identical iterates); 0 = never.
@@ -1142,49 +1140,6 @@ class PdhgEngine:
         (report, pieces) with host scalars reduced in the reference order."""
         ops = self.ops
         self._sync_shards()
-        if self._pass_graphable():
-            # the pass's kernels (products, fused KKT / probe epilogues,
-            # reductions) as one CUDA graph per `restarts` flag: eager the
-            # first time, captured the second, replayed after — launch-bound
-            # LPs pay one launch per pass instead of ~10
-            graphs = self.__dict__.setdefault("_pass_graphs", {})
-            seen = self.__dict__.setdefault("_pass_seen", set())
-            g = graphs.get(restarts)
-            if g is not None:
-                g.replay()
-                if hasattr(ops, "launches"):
-                    ops.launches += self._pass_launches[restarts]
-            elif restarts in seen:
-                g = torch.cuda.CUDAGraph()
-                before = getattr(ops, "launches", 0)
-                stream = torch.cuda.Stream(self.device)
-                stream.wait_stream(torch.cuda.current_stream(self.device))
-                with torch.cuda.stream(stream):
-                    g.capture_begin()
-                    try:
-                        self._kkt_launch(restarts)
-                    finally:
-                        g.capture_end()
-                self.__dict__.setdefault("_pass_launches", {})[restarts] = getattr(ops, "launches", 0) - before
-                if hasattr(ops, "launches"):
-                    ops.launches = before
-                graphs[restarts] = g
-                g.replay()
-                if hasattr(ops, "launches"):
-                    ops.launches += self._pass_launches[restarts]
-            else:
-                seen.add(restarts)
-                self._kkt_launch(restarts)
-        else:
-            self._kkt_launch(restarts)
-        return self._kkt_finish(restarts)
-
-    def _pass_graphable(self) -> bool:
-        return (self.opts.use_graphs and self.opts.pass_graphs and self.device.type == "cuda"
-                and self.comm.kind == "virtual" and hasattr(self.ops, "read_slots"))
-
-    def _kkt_launch(self, restarts: bool):
-        ops = self.ops
         for i, row in self.rows.items():
             src = self._run_plan(self.plan_kkt_ax[i])
             fused = isinstance(src, Fused)
@@ -1204,9 +1159,6 @@ class PdhgEngine:
                         if blk is not None:
                             ops.halfdiff_dot(blk.bufs["pAx_A"], blk.bufs["pPr_A"], row.dy,
                                              self.slot[("cross", (i, j))])
-
-    def _kkt_finish(self, restarts: bool):
-        ops = self.ops
         vals = ops.read_slots(self.nslots)
         local = {}
         for (i, j) in self.comm.local:
