@@ -373,6 +373,18 @@ int gridlp_op_step_advance(gridlp_step_t* d_step, int64_t delta, void* stream);
  * barrier's counter; it resets itself). GRIDLP_ERR_UNSUPPORTED when a matrix
  * has heavy (chunked) rows — use gridlp_pdhg_iterate. Same call site as
  * gridlp_pdhg_iterate (pdhg_engine.py:394-400). */
+/* gridlp_pdhg_iterate of n_iters iterations recorded ONCE as a CUDA graph
+ * (stream capture on a private stream, no synchronisation, so the device
+ * keeps running earlier work while the host captures and instantiates);
+ * replay with gridlp_graph_launch on any stream, free with
+ * gridlp_graph_destroy. Kernel arguments are captured by value; the step
+ * parameters are read from d_step at replay, so one graph serves every
+ * chunk of a solve (pdhg_engine.py:394-400). */
+int gridlp_iterate_graph_create(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
+                                const gridlp_src_t* dual_src, const gridlp_dual_t* dv,
+                                gridlp_step_t* d_step, int32_t n_iters, uint32_t flags, void** graph_exec);
+int gridlp_graph_launch(void* graph_exec, void* stream);
+int gridlp_graph_destroy(void* graph_exec);
 size_t gridlp_persistent_scratch_bytes(void);
 /* n_iters fused iterations of a TINY single-block LP in ONE thread-block
  * cluster launch (8 CTAs x 512 threads): x_bar / y replicated in every CTA's shared

@@ -1895,6 +1895,49 @@ int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_pri
   return GRIDLP_OK;
 }
 
+int gridlp_iterate_graph_create(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
+                                const gridlp_src_t* dual_src, const gridlp_dual_t* dv, gridlp_step_t* d_step,
+                                int32_t n_iters, uint32_t flags, void** graph_exec) {
+  if (!graph_exec || n_iters < 1) return fail(GRIDLP_ERR_ARG, "iterate_graph_create: bad argument");
+  *graph_exec = nullptr;
+  cudaStream_t cs = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("iterate_graph_create: ") + cudaGetErrorString(e));
+  e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return fail(GRIDLP_ERR_CUDA, std::string("iterate_graph_create: ") + cudaGetErrorString(e));
+  }
+  const int rc = gridlp_pdhg_iterate(primal_src, pv, dual_src, dv, d_step, n_iters, flags, cs);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(cs, &g);
+  cudaStreamDestroy(cs);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess || !g)
+    return fail(GRIDLP_ERR_CUDA, std::string("iterate_graph_create: ") + cudaGetErrorString(e));
+  cudaGraphExec_t ge = nullptr;
+  e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("iterate_graph_create: ") + cudaGetErrorString(e));
+  *graph_exec = ge;
+  return GRIDLP_OK;
+}
+
+int gridlp_graph_launch(void* graph_exec, void* stream) {
+  if (!graph_exec) return fail(GRIDLP_ERR_ARG, "graph_launch: null graph");
+  cudaError_t e = cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("graph_launch: ") + cudaGetErrorString(e));
+  return GRIDLP_OK;
+}
+
+int gridlp_graph_destroy(void* graph_exec) {
+  if (graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec));
+  return GRIDLP_OK;
+}
+
 size_t gridlp_persistent_scratch_bytes(void) { return 64; }
 
 int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,

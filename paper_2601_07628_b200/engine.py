@@ -1094,6 +1094,21 @@ class PdhgEngine:
             # would add one), so instantiation overlaps device work
             self._launch_iterations(g)
             count -= g
+            if (self.R == 1 and self.C == 1 and not self._banded and hasattr(self.ops, "iterate_graph")):
+                # one block: the whole chunk is one C-ABI call, captured in C
+                # (no torch capture machinery, no synchronise, ~ms cheaper
+                # per solve); the device keeps running the warm chunk meanwhile
+                (j, col), = self.cols.items()
+                (i, row), = self.rows.items()
+                self._graph = self.ops.iterate_graph(self.plan_primal[j][2], col, self.plan_dual[i][2], row, g,
+                                                     self.opts.halpern)
+                self._graph_launches = 0            # the C graph counts its own launches
+                while count >= g:
+                    self._graph.replay()
+                    count -= g
+                if count:
+                    self._launch_iterations(count)
+                return
             stream = torch.cuda.Stream(self.device)
             graph = torch.cuda.CUDAGraph()
             before = getattr(self.ops, "launches", 0)
@@ -1129,7 +1144,7 @@ class PdhgEngine:
             self._graph = graph
         while count >= g:
             self._graph.replay()
-            if hasattr(self.ops, "launches"):
+            if hasattr(self.ops, "launches") and self._graph_launches:
                 self.ops.launches += self._graph_launches
             count -= g
         if count:

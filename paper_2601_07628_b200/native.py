@@ -110,6 +110,10 @@ SIGNATURES = {
     "gridlp_op_step_advance": ([_P, c_int64, _P], c_int),
     "gridlp_pdhg_iterate": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32, c_uint32, _P],
                             c_int),
+    "gridlp_iterate_graph_create": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,
+                                     c_uint32, POINTER(c_void_p)], c_int),
+    "gridlp_graph_launch": ([_P, _P], c_int),
+    "gridlp_graph_destroy": ([_P], c_int),
     "gridlp_persistent_scratch_bytes": ([], ctypes.c_size_t),
     "gridlp_cluster_plan": ([POINTER(Src), POINTER(Src), POINTER(c_int64), c_int64], c_int),
     "gridlp_pdhg_iterate_cluster": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,

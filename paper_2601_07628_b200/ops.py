@@ -68,6 +68,25 @@ def _ptr(t):
     return t.data_ptr() if t is not None and t.numel() else None
 
 
+class _IterateGraph:
+    """A captured chunk of iterations (gridlp_iterate_graph_create)."""
+
+    def __init__(self, ops, handle, launches: int):
+        self.ops, self.handle, self.launches = ops, handle, launches
+
+    def replay(self):
+        self.ops.lib.call("gridlp_graph_launch", self.handle, self.ops.stream())
+        self.ops.launches += self.launches
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.ops.lib._lib.gridlp_graph_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 class CudaOps:
     kind = "cuda"
 
@@ -255,6 +274,16 @@ class CudaOps:
             raise native.GridlpError(f"gridlp_pdhg_iterate_persistent failed ({rc}): {self.lib.last_error()}")
         self.launches += 1 if count else 0
         return True
+
+    def iterate_graph(self, psrc, col, dsrc, row, count: int, halpern: bool):
+        """A chunk of `count` fused iterations of a single-block grid
+        captured once in C (gridlp_iterate_graph_create) — no torch capture
+        machinery, no synchronisation; replay with graph_launch()."""
+        h = ctypes.c_void_p()
+        self.lib.call("gridlp_iterate_graph_create", self.src(psrc), self.primal_struct(col), self.src(dsrc),
+                      self.dual_struct(row), self.step.data_ptr(), int(count), _pflags(col, halpern), ctypes.byref(h))
+        launches = count * (2 + _heavy(psrc) + _heavy(dsrc)) + 1
+        return _IterateGraph(self, h, launches)
 
     def cluster_plan(self, psrc, dsrc):
         """gridlp_cluster_plan for a matrix pair: the host plan array, or None
