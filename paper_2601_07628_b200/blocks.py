@@ -385,29 +385,6 @@ _STAGING = {}
 STAGING_BYTES = 32 << 20
 
 
-_COPY_POOL = []
-COPY_THREADS = 4
-
-
-def _parallel_copyto(dst: np.ndarray, src: np.ndarray):
-    """np.copyto (with dtype conversion) split over a few threads: numpy
-    drops the GIL for large copies, and one thread's pageable -> pinned
-    memcpy runs at a fraction of the host memory bandwidth."""
-    n = len(dst)
-    if n < (1 << 20) or COPY_THREADS <= 1:
-        np.copyto(dst, src, casting="unsafe")
-        return
-    if not _COPY_POOL:
-        from concurrent.futures import ThreadPoolExecutor
-
-        _COPY_POOL.append(ThreadPoolExecutor(COPY_THREADS, thread_name_prefix="gridlp-copy"))
-    cuts = [(k * n) // COPY_THREADS for k in range(COPY_THREADS + 1)]
-    futs = [_COPY_POOL[0].submit(np.copyto, dst[a:b], src[a:b], casting="unsafe")
-            for a, b in zip(cuts[:-1], cuts[1:])]
-    for f in futs:
-        f.result()
-
-
 def upload(a, dtype, device) -> torch.Tensor:
     """Host array -> new device tensor of `dtype` through two reused pinned
     staging buffers: the dtype conversion happens in the copy into pinned
@@ -433,7 +410,7 @@ def upload(a, dtype, device) -> torch.Tensor:
         buf, ev = bufs[k & 1]
         ev.synchronize()                         # the DMA that last read this buffer is done
         view = buf[: (hi - lo) * dt.itemsize].numpy().view(dt)
-        _parallel_copyto(view, src[lo:hi])
+        np.copyto(view, src[lo:hi], casting="unsafe")
         out[lo:hi].copy_(torch.from_numpy(view), non_blocking=True)
         ev.record(stream)
     return out
