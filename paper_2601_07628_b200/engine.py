@@ -96,6 +96,9 @@ class EngineOptions:
     # torch-level band split needs ~40 B/nnz of temporaries: a 2B-nnz block
     # of cfg5 on a 2x2 grid would not fit next to its own SELL copy)
     band_max_nnz: int = 1 << 28
+    # band problems on the single-process grid: length-class order from a
+    # counting pass over the generated blocks (False: layout order)
+    band_class_order: bool = True
     device_setup: bool = True
     # gathered vectors larger than this many bytes keep only their first
     # hot_gather_bytes (the highest-degree columns / longest rows in the
@@ -318,9 +321,15 @@ class PdhgEngine:
         cp, rp = lay.perm.col_perm, lay.perm.row_perm
         t0 = time.perf_counter()
         # a band problem's row lengths are only known per block, and ranks sharing
-        # a band must agree on its order, so it keeps the layout order
-        self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order is not False and not banded,
-                              setup if on_device else None)
+        # a band must agree on its order, so across processes it keeps the layout
+        # order; on the single-process grid every block is local: a counting pass
+        # over the generated blocks gives the class order (_band_orders)
+        if banded and on_device and self.comm.kind == "virtual" and self.opts.sorted_order is not False \
+                and self.opts.band_class_order:
+            self._band_orders(setup)
+        else:
+            self._internal_orders(problem, dev.type == "cuda" and self.opts.sorted_order is not False and not banded,
+                                  setup if on_device else None)
         tm["setup_orders_s"] = time.perf_counter() - t0
         if on_device and not banded and self.sorted and self.opts.sorted_order is None:
             t0 = time.perf_counter()
@@ -370,7 +379,7 @@ class PdhgEngine:
                 t = lambda a: a[idx]  # noqa: E731
             if banded:
                 cj, lj, hj, _ = problem.bands.col_data(c0, c1)
-                t = lambda a: a  # noqa: E731
+                t = (lambda a, o=self.col_order[j].long(): a[o]) if self.sorted else (lambda a: a)  # noqa: E731
                 obj, vlo, vhi = cj, lj, hj
             self.cols[j] = ColState(j, n, t(obj), t(vlo), t(vhi), padded(n, self.R),
                                     padded(n, self.R), torch.zeros(n, **f64),
@@ -390,7 +399,7 @@ class PdhgEngine:
                 t = lambda a: a[idx]  # noqa: E731
             if banded:
                 li, hi_, _ = problem.bands.row_data(r0, r1)
-                t = lambda a: a  # noqa: E731
+                t = (lambda a, o=self.row_order[i].long(): a[o]) if self.sorted else (lambda a: a)  # noqa: E731
                 clo, chi = li, hi_
             self.rows[i] = RowState(i, m, t(clo), t(chi), padded(m, self.C), torch.zeros(m, **f64),
                                     torch.zeros(m, **f64), torch.zeros(m, **f64), torch.zeros(m, **f64),
@@ -662,6 +671,34 @@ class PdhgEngine:
                 self.col_order[j] = base[length_order_device(col_len[c0:c1][base])]
             self.col_inv[j] = inverse(self.col_order[j])
 
+    def _band_orders(self, setup):
+        """Length-class order for a band problem on the single-process grid:
+        one counting pass generates every block (deterministic, hash-based)
+        for its row lengths and column counts, summed over the grid, then the
+        blocks are generated again for the build. Cuts the layout order's
+        SELL padding (planted rows: max of 32 near-binomial lengths)."""
+        lay, dev = self.layout, self.device
+        row_len = {i: torch.zeros(lay.row_range(i)[1] - lay.row_range(i)[0], dtype=torch.int64, device=dev)
+                   for i in range(self.R)}
+        col_len = {j: torch.zeros(lay.col_range(j)[1] - lay.col_range(j)[0], dtype=torch.int64, device=dev)
+                   for j in range(self.C)}
+        for i in range(self.R):
+            for j in range(self.C):
+                a = setup.block(i, j)
+                row_len[i] += (a.ptr[1:] - a.ptr[:-1]).to(torch.int64)
+                if a.nnz:
+                    col_len[j] += torch.bincount(a.col[:a.nnz].long(), minlength=col_len[j].numel())
+                del a
+        self.sorted = True
+        self.row_order, self.row_inv, self.col_order, self.col_inv = {}, {}, {}, {}
+        for i in range(self.R):
+            self.row_order[i] = length_order_device(row_len[i])
+            self.row_inv[i] = inverse_order_device(self.row_order[i])
+        for j in range(self.C):
+            self.col_order[j] = length_order_device(col_len[j])
+            self.col_inv[j] = inverse_order_device(self.col_order[j])
+        self.choices["order"] = "sorted (band counting pass)"
+
     def _band_cuts(self, length: int) -> list:
         """Column-band cuts of a gather vector of `length` doubles: one band
         unless it exceeds band_bytes (or column_bands forces a count). (A
@@ -907,6 +944,8 @@ class PdhgEngine:
             if probe is None:
                 native.load().call("gridlp_gen_uniform", probe_seed, 31, c0, c1 - c0, -1.0, 1.0, col.v.data_ptr(),
                                    torch.cuda.current_stream(self.device).cuda_stream)
+                if self.sorted:      # drawn in layout order: into the internal order
+                    col.v.copy_(col.v[self.col_order[j].long()])
                 continue
             col.v.copy_(self._to_internal_col(j, np.asarray(probe[c0:c1], dtype=np.float64)))
         if self.comm.kind == "virtual" and self.R == 1 and self.C == 1 and self.device.type == "cuda":
