@@ -95,7 +95,7 @@ class EngineOptions:
     # blocks above this many nonzeros skip the timed column-band choice (the
     # torch-level band split needs ~40 B/nnz of temporaries: a 2B-nnz block
     # of cfg5 on a 2x2 grid would not fit next to its own SELL copy)
-    band_max_nnz: int = 1 << 28
+    band_max_nnz: int = 1 << 30
     # band problems on the single-process grid: length-class order from a
     # counting pass over the generated blocks (False: layout order)
     band_class_order: bool = True
