@@ -1297,7 +1297,12 @@ class PdhgEngine:
         tau, sigma = eta / omega, eta * omega
         total = st["total"]
         target = min((total // K + 1) * K, o.max_iterations)
-        ops.set_step(tau, sigma, o.gamma, st["inner_k"])
+        # the device step struct already holds (tau, sigma, gamma) and the
+        # advanced Halpern counter unless a restart changed them: skip the
+        # H2D write then (launch-bound LPs pay it once per pass otherwise)
+        key = (tau, sigma, o.gamma, st["inner_k"])
+        if key != st.get("device_step"):
+            ops.set_step(tau, sigma, o.gamma, st["inner_k"])
         self.count_iterations(target - total)
         trace = st["trace"]
         if trace is None:
@@ -1305,6 +1310,7 @@ class PdhgEngine:
                 self._run_iterations(target - total)
             st["inner_k"] += target - total
             total = target
+            st["device_step"] = (tau, sigma, o.gamma, st["inner_k"])
         else:
             while total < target:
                 self._launch_iterations(1)
