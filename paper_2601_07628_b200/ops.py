@@ -68,6 +68,10 @@ def _ptr(t):
     return t.data_ptr() if t is not None and t.numel() else None
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None) or (
+    lambda idx: torch.cuda.current_stream(idx).cuda_stream)
+
+
 class _IterateGraph:
     """A captured chunk of iterations (gridlp_iterate_graph_create)."""
 
@@ -93,6 +97,8 @@ class CudaOps:
     def __init__(self, device: torch.device, capacity: int, num_slots: int):
         self.lib = native.load()
         self.device = device
+        self._dev_index = torch.device(device).index if torch.device(device).index is not None else (
+            torch.cuda.current_device() if torch.cuda.is_available() else 0)
         self.capacity = max(int(capacity), 1)
         self.partials = torch.zeros(self.capacity * native.MAX_RED, dtype=torch.float64, device=device)
         self.slots = torch.zeros((max(num_slots, 1), native.MAX_RED), dtype=torch.float64, device=device)
@@ -105,7 +111,11 @@ class CudaOps:
 
     # -- plumbing ------------------------------------------------------------
     def stream(self):
-        return torch.cuda.current_stream(self.device).cuda_stream
+        # the current stream's raw handle (inside a torch graph capture: the
+        # capture stream); the raw query costs well under a microsecond where
+        # torch.cuda.current_stream() builds a Stream object (~7 µs a call,
+        # ~10 calls per KKT pass)
+        return _raw_stream(self._dev_index)
 
     def enable_terms(self, rows: int):
         """Canonical (layout-independent) reductions for fused products of up
