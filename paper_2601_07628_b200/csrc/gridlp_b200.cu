@@ -525,10 +525,13 @@ __device__ __forceinline__ uint64_t global_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-constexpr int SELL_WPB = 2;          // warps (slices) per CTA
+#ifndef GRIDLP_SELL_WPB
+#define GRIDLP_SELL_WPB 2
+#endif
+constexpr int SELL_WPB = GRIDLP_SELL_WPB;   // warps (slices) per CTA
 constexpr int SELL_NT = SELL_WPB * 32;
 constexpr int SELL_U = 4;            // steps in flight per lane
-constexpr int SELL_MINB = 32;        // 64 warps per SM at <= 32 registers
+constexpr int SELL_MINB = 64 / SELL_WPB;   // 64 warps per SM at <= 32 registers
 #ifndef GRIDLP_HEAVY_U
 #define GRIDLP_HEAVY_U SELL_U        // heavy-chunk kernel: loads in flight per thread
 #endif
@@ -816,7 +819,7 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
 // depend on them). More registers (fewer warps per SM): it pays on long
 // lanes whose streams miss L2 (power-law rows), not on short ones.
 #ifndef GRIDLP_PIPE_MINB
-#define GRIDLP_PIPE_MINB 20          // 40 warps per SM at <= 51 registers
+#define GRIDLP_PIPE_MINB (40 / GRIDLP_SELL_WPB)   // 40 warps per SM at <= 51 registers
 #endif
 #ifndef GRIDLP_PIPE_U
 #define GRIDLP_PIPE_U SELL_U
