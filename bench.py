@@ -532,8 +532,9 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": g.rows * g.cols,
                          "kind": "port",
                          "sample": f"{sample} main-loop iterations per step on a {g.rows}x{g.cols} "
-                                   f"block grid, one host thread per block (scipy csr_matvec releases "
-                                   f"the GIL), block build {setup:.1f}s untimed"},
+                                   f"block grid, one host thread per block for the block products and "
+                                   f"the per-block epilogues (scipy csr_matvec and numpy release the "
+                                   f"GIL), block build {setup:.1f}s untimed"},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
