@@ -254,11 +254,20 @@ def measure_config(name: str, dev, steps: int = 3) -> dict:
     t_iter = sum(a.elapsed_time(b) for a, b, _ in ev) * 1e-3 / max(sum(n for _, _, n in ev), 1)
     b = iteration_bytes(engine)
     peak, _ = measured_peak()
+    nnz = sum(v for v in engine.per_device_nnz if v >= 0)
     out = {"workload": f"{name}: {workload_name(name)}, m={p.num_constraints} n={p.num_variables} "
-                       f"nnz={sum(v for v in engine.per_device_nnz if v >= 0)}",
+                       f"nnz={nnz}",
            "us_per_iteration": t_iter * 1e6, "iterations_per_s": 1.0 / t_iter,
            "bytes_per_iteration": b["iteration"], "achieved_GBs": b["iteration"] / t_iter / 1e9,
            "frac": b["iteration"] / t_iter / 1e9 / peak, "layout_choices": dict(engine.choices)}
+    if name == "cfg3":
+        # the pattern's own ceiling: Zipf(0.8) 8-byte gathers over the 160 MB x_bar
+        # and the 80 MB y at the rates tools/microbench_l2.cu measured on this
+        # B200 (profiles/r2/microbench_l2.jsonl), before any stream byte
+        rates = {"x_bar_160MB": 200.6e9, "y_80MB": 251.2e9}
+        floor = nnz / rates["x_bar_160MB"] + nnz / rates["y_80MB"]
+        out["gather_bound"] = {"gathers_per_s": rates, "seconds_at_ceiling": floor, "frac": floor / t_iter,
+                               "source": "profiles/r2/microbench_l2.jsonl"}
     del engine, p
     torch.cuda.empty_cache()
     return out
