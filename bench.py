@@ -264,7 +264,7 @@ def measure_config(name: str, dev, steps: int = 3) -> dict:
         # the pattern's own ceiling: Zipf(0.8) 8-byte gathers over the 160 MB x_bar
         # and the 80 MB y at the rates tools/microbench_l2.cu measured on this
         # B200 (profiles/r2/microbench_l2.jsonl), before any stream byte
-        rates = {"x_bar_160MB": 200.6e9, "y_80MB": 251.2e9}
+        rates = {"x_bar_160MB": 203.2e9, "y_80MB": 308.5e9}
         floor = nnz / rates["x_bar_160MB"] + nnz / rates["y_80MB"]
         out["gather_bound"] = {"gathers_per_s": rates, "seconds_at_ceiling": floor, "frac": floor / t_iter,
                                "source": "profiles/r2/microbench_l2.jsonl"}

@@ -68,7 +68,7 @@ int main() {
   CK(cudaMemset(d_x, 0, 512l << 20));
   std::vector<int> h(n);
   std::mt19937_64 rng(1);
-  const int mbs[] = {8, 16, 32, 48, 64, 96, 128, 160, 256};
+  const int mbs[] = {8, 16, 32, 40, 48, 64, 80, 96, 128, 160, 256};
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
