@@ -137,3 +137,13 @@ def test_scaled_solve_on_a_grid_matches_unscaled_oracle():
     assert abs(got.objective - want.objective) <= 1e-6 * max(1.0, abs(want.objective))
     rp = _host_rp(q, got.x)
     assert abs(got.report.r_primal - rp) <= 1e-6 * max(rp, 1e-300) + 1e-15
+
+
+def test_scaling_refuses_band_problems():
+    """A band problem has no global matrix to equilibrate (its blocks are
+    generated per device): SolverConfig.scaling is refused up front."""
+    from paper_2601_07628_b200 import synth
+
+    p = synth.BandProblem(synth.PlantedBands(synth.PlantedSpec(100, 200, 4)), "planted")
+    with pytest.raises(ValueError, match="band problems"):
+        solve(p, SolverConfig(scaling="ruiz", permutation="none", partitioning="uniform"))
