@@ -531,7 +531,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 constexpr int SELL_WPB = GRIDLP_SELL_WPB;   // warps (slices) per CTA
 constexpr int SELL_NT = SELL_WPB * 32;
 constexpr int SELL_U = 4;            // steps in flight per lane
-constexpr int SELL_MINB = 64 / SELL_WPB;   // 64 warps per SM at <= 32 registers
+constexpr int SELL_MINB = 48 / SELL_WPB;   // 48 warps per SM at <= 42 registers (no spills with the hinted epilogues)
 #ifndef GRIDLP_HEAVY_U
 #define GRIDLP_HEAVY_U SELL_U        // heavy-chunk kernel: loads in flight per thread
 #endif
