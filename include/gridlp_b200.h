@@ -398,12 +398,34 @@ size_t gridlp_persistent_scratch_bytes(void);
  * returns GRIDLP_ERR_UNSUPPORTED when the LP does not fit one cluster's
  * shared memory or has long rows / column bands (use gridlp_pdhg_iterate). */
 #define GRIDLP_CLUSTER_PLAN_LEN 35
+/* The KKT / restart-probe pass fused into a cluster launch (evaluate_kkt
+ * and the restart probe, pdhg_engine.py:310-346, :419-427): after the
+ * iterations the same shared-memory slices give A x (KKT rows), A^T y (KKT
+ * columns, x_probe_bar) and, with mode 2, A x_probe_bar (probe). Each row's
+ * reduction terms land in t_rows [4 m] / t_cols [4 n] / t_probe [2 m] in
+ * the gridlp_red_t.terms layout (term q of row r at q * rows + r); reduce
+ * each with gridlp_reduce_terms — the same sums as the unfused ops. ax [m]
+ * and xpb [n] receive A x and x_probe_bar as gridlp_op_kkt_rows /
+ * gridlp_op_kkt_cols would write them. */
+typedef struct gridlp_cluster_kkt {
+  int32_t mode;            /* 0: no pass, 1: KKT rows + cols, 2: + restart probe */
+  int32_t reserved;
+  double* t_rows;
+  double* t_cols;
+  double* t_probe;
+  double* ax;
+  double* xpb;
+} gridlp_cluster_kkt_t;
 int gridlp_cluster_plan(const gridlp_src_t* primal_src, const gridlp_src_t* dual_src, int64_t* plan,
                         int64_t plan_len);
 int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
                                 const gridlp_src_t* dual_src, const gridlp_dual_t* dv,
                                 gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,
-                                const int64_t* plan, void* stream);
+                                const int64_t* plan, const gridlp_cluster_kkt_t* kkt_pass, void* stream);
+/* Fixed-order reduction of per-row terms (nred = 1, 2 or 4 per row, term q
+ * of row r at terms[q * n + r]) into red->out[0..nred): the canonical
+ * reduction every fused op uses (terms_reduce + final reduce). */
+int gridlp_reduce_terms(const double* terms, int64_t n, int32_t nred, const gridlp_red_t* red, void* stream);
 int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,
                                    const gridlp_src_t* dual_src, const gridlp_dual_t* dv,
                                    gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,

@@ -1209,9 +1209,25 @@ struct ClusterPlan {
   int64_t db[CLUSTER_CTAS + 1];       // dual product (A) slice boundaries
 };
 
+// The KKT / restart-probe pass fused into the cluster launch (gridlp_pdhg_iterate_cluster
+// with a gridlp_cluster_kkt_t): the three products of the pass read the same
+// shared-memory slices; each row's reduction terms go to the caller's term
+// buffers in the layout of gridlp_red_t.terms, reduced afterwards by
+// gridlp_reduce_terms exactly as the unfused ops reduce them.
+struct ClusterKkt {
+  int32_t mode;            // 0 none, 1 KKT rows + cols, 2 + restart probe
+  double* t_rows;          // [4 m]
+  double* t_cols;          // [4 n]
+  double* t_probe;         // [2 m]
+  double* ax;              // [m]  A x (the probe's cross term)
+  double* xpb;             // [n]  x_probe_bar
+  const double* dr;        // scale vectors of a scaled LP (or NULL)
+  const double* dc;
+};
+
 __global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(CLUSTER_TPB)
     cluster_iterate_kernel(gridlp_csr_t AT, gridlp_csr_t A, OpPrimal pop, OpDual dop, int32_t n_iters,
-                           gridlp_step_t* step, ClusterPlan plan) {
+                           gridlp_step_t* step, ClusterPlan plan, ClusterKkt kkt) {
   extern __shared__ __align__(16) unsigned char smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank();
@@ -1288,6 +1304,75 @@ __global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(CLUSTER_T
   for (int64_t k = threadIdx.x; k < 32 * (ds1 - ds0); k += CLUSTER_TPB) {
     const int64_t r = 32 * ds0 + k;
     if (r < m && D.info[k] >= 0) dop.y[r] = D.v[0][k];
+  }
+  if (kkt.mode > 0) {
+    // x into the x_bar replicas (x_bar was written back above); the y
+    // replicas already hold the final y
+    cluster.sync();
+    for (int64_t ls = warp; ls < ps1 - ps0; ls += CLUSTER_WARPS) {
+      const int64_t k = 32 * ls + lane;
+      if (P.info[k] < 0) continue;
+      const int64_t r = 32 * (ps0 + ls) + lane;
+#pragma unroll
+      for (int q = 0; q < CLUSTER_CTAS; ++q) xbar_at[q][r] = P.v[0][k];
+    }
+    cluster.sync();
+    // KKT rows: A x, range violation and bound penalty per row (OpKktRows)
+    OpKktRows kr{dop.y, dop.lo, dop.hi, kkt.ax, kkt.dr};
+    for (int64_t ls = warp; ls < ds1 - ds0; ls += CLUSTER_WARPS) {
+      const int64_t k = 32 * ls + lane;
+      const int info = D.info[k];
+      if (info < 0) continue;
+      const int64_t r = 32 * (ds0 + ls) + lane;
+      const double sx = cluster_row_sum(D, D.off[ls] + lane, info >> 8, xbar_r);
+      double t[4] = {0.0, 0.0, 0.0, 0.0};
+      kr.row(r, sx, OpKktRows::Data{D.v[0][k], D.v[1][k], D.v[2][k]}, t);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) kkt.t_rows[(int64_t)q * m + r] = t[q];
+    }
+    // KKT cols: A^T y, the projected-gradient terms and x_probe_bar (OpKktCols)
+    OpKktCols kc{};
+    kc.x = pop.x; kc.c = pop.c; kc.lo = pop.lo; kc.hi = pop.hi; kc.xpb = kkt.xpb; kc.step = step; kc.dc = kkt.dc;
+    kc.prepare();
+    for (int64_t ls = warp; ls < ps1 - ps0; ls += CLUSTER_WARPS) {
+      const int64_t k = 32 * ls + lane;
+      const int info = P.info[k];
+      if (info < 0) continue;
+      const int64_t r = 32 * (ps0 + ls) + lane;
+      const double aty = cluster_row_sum(P, P.off[ls] + lane, info >> 8, y_r);
+      double t[4] = {0.0, 0.0, 0.0, 0.0};
+      kc.row(r, aty, OpKktCols::Data{P.v[0][k], P.v[1][k], P.v[2][k], P.v[3][k]}, t);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) kkt.t_cols[(int64_t)q * n + r] = t[q];
+    }
+    if (kkt.mode > 1) {
+      cluster.sync();                           // every CTA is done reading the x replica
+      for (int64_t ls = warp; ls < ps1 - ps0; ls += CLUSTER_WARPS) {
+        const int64_t k = 32 * ls + lane;
+        if (P.info[k] < 0) continue;
+        const int64_t r = 32 * (ps0 + ls) + lane;
+        const double v = kkt.xpb[r];            // this thread's own write above
+#pragma unroll
+        for (int q = 0; q < CLUSTER_CTAS; ++q) xbar_at[q][r] = v;
+      }
+      cluster.sync();
+      // restart probe: A x_probe_bar, the dual map and its norms (OpProbe)
+      OpProbe pr{};
+      pr.y = dop.y; pr.lo = dop.lo; pr.hi = dop.hi; pr.ax = kkt.ax; pr.dy_out = nullptr; pr.step = step;
+      pr.prepare();
+      for (int64_t ls = warp; ls < ds1 - ds0; ls += CLUSTER_WARPS) {
+        const int64_t k = 32 * ls + lane;
+        const int info = D.info[k];
+        if (info < 0) continue;
+        const int64_t r = 32 * (ds0 + ls) + lane;
+        const double z = cluster_row_sum(D, D.off[ls] + lane, info >> 8, xbar_r);
+        double t[2] = {0.0, 0.0};
+        pr.row(r, z, OpProbe::Data{D.v[0][k], D.v[1][k], D.v[2][k], kkt.ax[r]}, t);
+        kkt.t_probe[r] = t[0];
+        kkt.t_probe[m + r] = t[1];
+      }
+    }
+    cluster.sync();                             // no CTA leaves while others read its replicas
   }
   if (rank == 0 && threadIdx.x == 0) step->inner_k += n_iters;
 }
@@ -1861,7 +1946,7 @@ int gridlp_cluster_plan(const gridlp_src_t* primal_src, const gridlp_src_t* dual
 
 int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_primal_t* pv, const gridlp_src_t* dual_src,
                                 const gridlp_dual_t* dv, gridlp_step_t* d_step, int32_t n_iters, uint32_t flags,
-                                const int64_t* plan, void* stream) {
+                                const int64_t* plan, const gridlp_cluster_kkt_t* kkt_pass, void* stream) {
   if (!primal_src || !dual_src || !pv || !dv || !d_step || n_iters < 0 || !plan)
     return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: bad argument");
   const gridlp_csr_t* AT = primal_src->A;
@@ -1870,7 +1955,16 @@ int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_pri
     return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: needs fused sources of matching lengths");
   const int64_t smem = plan[2 * (CLUSTER_CTAS + 1)];
   if (smem <= 0 || smem > 227 * 1024) return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: plan from gridlp_cluster_plan");
-  if (n_iters == 0) return GRIDLP_OK;
+  ClusterKkt kk{};
+  if (kkt_pass && kkt_pass->mode > 0) {
+    if (kkt_pass->mode > 2 || !kkt_pass->t_rows || !kkt_pass->t_cols || !kkt_pass->ax || !kkt_pass->xpb ||
+        (kkt_pass->mode > 1 && !kkt_pass->t_probe))
+      return fail(GRIDLP_ERR_ARG, "pdhg_iterate_cluster: incomplete KKT pass buffers");
+    kk.mode = kkt_pass->mode;
+    kk.t_rows = kkt_pass->t_rows; kk.t_cols = kkt_pass->t_cols; kk.t_probe = kkt_pass->t_probe;
+    kk.ax = kkt_pass->ax; kk.xpb = kkt_pass->xpb; kk.dr = dv->scale; kk.dc = pv->scale;
+  }
+  if (n_iters == 0 && kk.mode == 0) return GRIDLP_OK;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(cluster_iterate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1893,9 +1987,28 @@ int gridlp_pdhg_iterate_cluster(const gridlp_src_t* primal_src, const gridlp_pri
   cfg.blockDim = dim3(CLUSTER_TPB);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, cluster_iterate_kernel, *AT, *A, pop, dop, n_iters, d_step, cp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, cluster_iterate_kernel, *AT, *A, pop, dop, n_iters, d_step, cp, kk);
   if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("pdhg_iterate_cluster: ") + cudaGetErrorString(e));
   return GRIDLP_OK;
+}
+
+int gridlp_reduce_terms(const double* terms, int64_t n, int32_t nred, const gridlp_red_t* red, void* stream) {
+  if (n < 0 || (nred != 1 && nred != 2 && nred != 4) || !red || !red->out || (n > 0 && !terms))
+    return fail(GRIDLP_ERR_ARG, "reduce_terms: bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t slots = rows_blocks(n);
+  if (n > 0) {
+    if (!red->partials || red->capacity < slots) return fail(GRIDLP_ERR_WORKSPACE, "reduce_terms: workspace too small");
+    switch (nred) {
+      case 1: terms_reduce_kernel<1><<<(unsigned)slots, TPB, 0, s>>>(terms, n, red->partials); break;
+      case 2: terms_reduce_kernel<2><<<(unsigned)slots, TPB, 0, s>>>(terms, n, red->partials); break;
+      default: terms_reduce_kernel<4><<<(unsigned)slots, TPB, 0, s>>>(terms, n, red->partials); break;
+    }
+    int rc = check_launch("reduce_terms");
+    if (rc) return rc;
+  }
+  reduce_kernel<<<1, TPB, 0, s>>>(red->partials, n > 0 ? slots : 0, nred, red->out);
+  return check_launch("reduce_terms");
 }
 
 int gridlp_iterate_graph_create(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,

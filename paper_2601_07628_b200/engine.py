@@ -124,6 +124,9 @@ class EngineOptions:
     # in one thread-block-cluster launch (gridlp_pdhg_iterate_cluster,
     # bit-identical iterates); falls back by itself when the LP is too big
     cluster_small: bool = True
+    # with the cluster launch, the chunk's closing KKT / probe pass runs in the
+    # same launch (only the canonical term reductions follow)
+    cluster_fused_pass: bool = True
     # NCCL executor, main loop: each axis sum is an ordered reduce-scatter
     # (all-to-all of the partial shards, then the epilogue adds the G member
     # slices in ascending order — the reference's order, comm.py:75-84) and
@@ -1031,6 +1034,18 @@ class PdhgEngine:
                                 and not self._banded and 0 < nnz <= self.opts.persistent_max_nnz)
         return self._persist_ok
 
+    def _cluster_pass(self, mode: int, row, col):
+        """gridlp_cluster_kkt_t for a chunk that ends at a KKT pass: the pass's
+        per-row term buffers (allocated once) and the ax / x_probe_bar outputs."""
+        t = getattr(self, "_pass_terms", None)
+        if t is None:
+            f64 = dict(dtype=torch.float64, device=self.device)
+            t = self._pass_terms = {"rows": torch.zeros(4 * max(row.m, 1), **f64),
+                                    "cols": torch.zeros(4 * max(col.n, 1), **f64),
+                                    "probe": torch.zeros(2 * max(row.m, 1), **f64)}
+        return native.ClusterKkt(mode, 0, t["rows"].data_ptr(), t["cols"].data_ptr(), t["probe"].data_ptr(),
+                                 row.ax.data_ptr() if row.m else None, col.xpb.data_ptr() if col.n else None)
+
     def _cluster(self) -> bool:
         """Tiny single-block LP that fits one thread-block cluster: each
         chunk is one cluster launch (no graph; the plan is computed once,
@@ -1053,9 +1068,13 @@ class PdhgEngine:
             (j, col), = self.cols.items()
             (i, row), = self.rows.items()
             if self._cluster():
+                mode = self.__dict__.pop("_fuse_pass_mode", 0)
+                kkt = self._cluster_pass(mode, row, col) if mode else None
                 try:
                     ops.iterate_cluster(self.plan_primal[j][2], col, self.plan_dual[i][2], row, count, h,
-                                        self._cluster_plan)
+                                        self._cluster_plan, kkt)
+                    if mode:
+                        self._pass_in_launch = mode
                     return
                 except native.GridlpError as exc:        # launch refused (e.g. no cluster scheduling)
                     log.warning("cluster launch refused (%s); using the kernel-per-product path", exc)
@@ -1194,14 +1213,27 @@ class PdhgEngine:
         (report, pieces) with host scalars reduced in the reference order."""
         ops = self.ops
         self._sync_shards()
-        for i, row in self.rows.items():
+        fused_pass = self.__dict__.pop("_pass_in_launch", 0)
+        if fused_pass and fused_pass == (2 if restarts else 1):
+            # the cluster launch already computed the pass's per-row terms
+            # (and ax, x_probe_bar): only the canonical reductions remain
+            (i, row), = self.rows.items()
+            (j, col), = self.cols.items()
+            ops.reduce_terms(self._pass_terms["rows"], row.m, 4, self.slot[("kkt_rows", i)])
+            ops.reduce_terms(self._pass_terms["cols"], col.n, 4, self.slot[("kkt_cols", j)])
+            if restarts:
+                ops.reduce_terms(self._pass_terms["probe"], row.m, 2, self.slot[("probe", i)])
+            restarts_done = True
+        else:
+            restarts_done = False
+        for i, row in ([] if restarts_done else self.rows.items()):
             src = self._run_plan(self.plan_kkt_ax[i])
             fused = isinstance(src, Fused)
             ops.kkt_rows(src, row, row.ax if fused else None, self.slot[("kkt_rows", i)])
-        for j, col in self.cols.items():
+        for j, col in ([] if restarts_done else self.cols.items()):
             src = self._run_plan(self.plan_kkt_aty[j])
             ops.kkt_cols(src, col, self.slot[("kkt_cols", j)])
-        if restarts:
+        if restarts and not restarts_done:
             for i, row in self.rows.items():
                 src = self._run_plan(self.plan_probe[i])
                 if isinstance(src, Fused):
@@ -1306,6 +1338,9 @@ class PdhgEngine:
         self.count_iterations(target - total)
         trace = st["trace"]
         if trace is None:
+            if target % K == 0 and self.opts.cluster_fused_pass and self._cluster():
+                # the KKT pass that follows is computed inside the same cluster launch
+                self._fuse_pass_mode = 2 if o.restarts else 1
             with nvtx_range("gridlp.iterations"):
                 self._run_iterations(target - total)
             st["inner_k"] += target - total

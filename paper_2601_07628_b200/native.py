@@ -80,6 +80,11 @@ class Dual(ctypes.Structure):
 TERMS_PER_ROW = 4      # the most reduction terms a fused product op emits per row (KKT columns)
 
 
+class ClusterKkt(ctypes.Structure):
+    _fields_ = [("mode", c_int32), ("reserved", c_int32), ("t_rows", c_void_p), ("t_cols", c_void_p),
+                ("t_probe", c_void_p), ("ax", c_void_p), ("xpb", c_void_p)]
+
+
 class Red(ctypes.Structure):
     _fields_ = [("partials", c_void_p), ("capacity", c_int64), ("out", c_void_p), ("terms", c_void_p),
                 ("terms_capacity", c_int64)]
@@ -117,7 +122,8 @@ SIGNATURES = {
     "gridlp_persistent_scratch_bytes": ([], ctypes.c_size_t),
     "gridlp_cluster_plan": ([POINTER(Src), POINTER(Src), POINTER(c_int64), c_int64], c_int),
     "gridlp_pdhg_iterate_cluster": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,
-                                     c_uint32, POINTER(c_int64), _P], c_int),
+                                     c_uint32, POINTER(c_int64), POINTER(ClusterKkt), _P], c_int),
+    "gridlp_reduce_terms": ([_P, c_int64, c_int32, POINTER(Red), _P], c_int),
     "gridlp_pdhg_iterate_persistent": ([POINTER(Src), POINTER(Primal), POINTER(Src), POINTER(Dual), _P, c_int32,
                                         c_uint32, _P, _P], c_int),
     "gridlp_setup_workspace_bytes": ([c_int64, c_int64], ctypes.c_size_t),

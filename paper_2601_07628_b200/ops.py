@@ -306,13 +306,20 @@ class CudaOps:
             raise native.GridlpError(f"gridlp_cluster_plan failed ({rc}): {self.lib.last_error()}")
         return plan
 
-    def iterate_cluster(self, psrc, col, dsrc, row, count: int, halpern: bool, plan):
+    def iterate_cluster(self, psrc, col, dsrc, row, count: int, halpern: bool, plan, kkt=None):
         """count fused iterations of a tiny single-block LP in one cluster
-        launch (gridlp_pdhg_iterate_cluster) with a plan of cluster_plan()."""
+        launch (gridlp_pdhg_iterate_cluster) with a plan of cluster_plan();
+        `kkt` (native.ClusterKkt) fuses the closing KKT / probe pass."""
         self.lib.call("gridlp_pdhg_iterate_cluster", self.src(psrc), self.primal_struct(col), self.src(dsrc),
                       self.dual_struct(row), self.step.data_ptr(), int(count), _pflags(col, halpern), plan,
-                      self.stream())
-        self.launches += 1 if count else 0
+                      ctypes.byref(kkt) if kkt is not None else None, self.stream())
+        self.launches += 1 if (count or kkt is not None) else 0
+
+    def reduce_terms(self, terms, n: int, nred: int, slot: int):
+        """gridlp_reduce_terms: the canonical reduction of per-row terms into
+        a reduction slot."""
+        self.launches += 2
+        self.lib.call("gridlp_reduce_terms", terms.data_ptr(), int(n), int(nred), self.red(slot), self.stream())
 
     def step_advance(self, delta: int):
         self.launches += 1
