@@ -239,5 +239,7 @@ def test_cluster_and_persistent_entry_points_validate_arguments(lib):
         lib.call("gridlp_cluster_plan", None, None, None, 0)
     plan = (ctypes.c_int64 * native.CLUSTER_PLAN_LEN)()
     with pytest.raises(native.GridlpError, match="bad argument"):
-        lib.call("gridlp_pdhg_iterate_cluster", None, None, None, None, None, 1, 0, plan, None)
+        lib.call("gridlp_pdhg_iterate_cluster", None, None, None, None, None, 1, 0, plan, None, None)
+    with pytest.raises(native.GridlpError, match="bad argument"):
+        lib.call("gridlp_reduce_terms", None, 10, 3, None, None)
     assert int(lib._lib.gridlp_persistent_scratch_bytes()) >= 8
