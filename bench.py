@@ -343,6 +343,15 @@ def iteration_bytes(engine) -> dict:
     # of the two n-vectors lo, hi
     out["iteration_moved"] = out["iteration"] - sum(
         16 * c.n for c in engine.cols.values() if getattr(c, "uniform_bounds", False))
+    # ... and with a compact value codec (DeviceCsr.val_codec: +-1 values in the
+    # column's sign bit, or exact floats) 8 resp. 4 fewer bytes per nonzero
+    saved = 0
+    for blk in engine.blocks.values():
+        for mat in (blk.A, blk.AT):
+            for d in getattr(mat, "bands", [mat]):
+                saved += (0, 4, 8)[getattr(d, "val_codec", 0)] * d.nnz
+    out["iteration_moved"] -= saved
+    out["value_bytes_saved"] = saved
     # L1->L2 requests: one 32-byte sector request per gathered element (random
     # columns: no two lanes of a warp share a 128-byte line) plus one request
     # per 128-byte line of every streamed array
@@ -608,6 +617,8 @@ def run_ours(args, rank, world, local_rank):
         over["graph_nccl"] = True
     if args.hot_mb is not None:
         over["hot_gather_bytes"] = int(args.hot_mb) << 20
+    if args.value_codec is not None:
+        over["value_codec"] = args.value_codec
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
     log(f"[bench] rank {rank}: setup {time.perf_counter() - t0:.1f}s {tim}")
     R, C = layout.topology.rows, layout.topology.cols
@@ -793,6 +804,8 @@ def main():
     ap.add_argument("--no-first-touch", action="store_true", help="EngineOptions.first_touch_cols=False")
     ap.add_argument("--graph-nccl", action="store_true", help="capture NCCL iterations in CUDA graphs (default now)")
     ap.add_argument("--hot-mb", type=int, default=None, help="EngineOptions.hot_gather_bytes in MiB (0 = off)")
+    ap.add_argument("--value-codec", choices=("auto", "f64"), default=None,
+                    help="EngineOptions.value_codec (lossless compact value storage; default auto)")
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")
     ap.add_argument("--permutation", default=None, help="SolverConfig.permutation override")
     ap.add_argument("--partitioning", default=None, help="SolverConfig.partitioning override")

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define GRIDLP_ABI_VERSION 1
+#define GRIDLP_ABI_VERSION 2
 
 enum gridlp_status {
   GRIDLP_OK = 0,
@@ -56,6 +56,14 @@ enum gridlp_status {
 #define GRIDLP_HEAVY_CHUNK 2048
 /* Largest light_row_max / exact_row_max accepted. */
 #define GRIDLP_ROW_MAX_LIMIT 65536
+
+/* Value storage of a block (gridlp_csr_t.val_codec). Every codec is
+ * LOSSLESS: the kernels rebuild the exact FP64 value and multiply it by the
+ * gathered entry as with FP64 storage, so products are bit-identical. */
+#define GRIDLP_VALS_F64 0   /* sell_vals / long_vals are double (12 B per nonzero)            */
+#define GRIDLP_VALS_F32 1   /* ... are float; every value is exactly a float (8 B per nonzero)  */
+#define GRIDLP_VALS_UNIT 2  /* every value is +1.0 or -1.0: no value arrays, bit 31 of the
+                               column index is the sign (4 B per nonzero; network / MCF rows)   */
 
 /*
  * One device-resident block A_ij (or its stored transpose) in SELL-32 plus
@@ -126,6 +134,13 @@ typedef struct gridlp_csr {
    * length-class order puts the highest-degree columns first). <= 0: every
    * gather evict_last. Picks a cache policy, never a value. */
   int64_t hot_cols;
+  /* GRIDLP_VALS_*: how sell_vals / long_vals store the values (F32: cast the
+   * pointers to const float*; UNIT: both NULL allowed, sell_cols / long_cols
+   * carry the sign in bit 31). The setup detects the codec per block from
+   * the values themselves (lp_model.py:53-55 stores FP64 values; integer
+   * and +-1 coefficients are exact in the narrower forms). */
+  int32_t val_codec;
+  int32_t reserved_codec;
 } gridlp_csr_t;
 
 /*

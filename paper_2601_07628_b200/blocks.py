@@ -5,7 +5,10 @@ Reference: permute_problem / distribute (partition.py:262-319), slice_block
 and transpose (sparse_kernels.py:27-58). The reference builds CSR with int64
 indices (16 B/nnz); a device block here is SELL-32 with int32 column indices
 and FP64 values (12 B/nnz per orientation) plus a compact CSR of its long
-rows (include/gridlp_b200.h, gridlp_csr_t).
+rows (include/gridlp_b200.h, gridlp_csr_t). Values that are all exactly
+floats, or all +-1, are stored in the narrower lossless codecs
+(GRIDLP_VALS_F32: 8 B/nnz, GRIDLP_VALS_UNIT: 4 B/nnz) — the kernels rebuild
+the exact FP64 value, so products are unchanged bit for bit.
 """
 
 from __future__ import annotations
@@ -208,6 +211,32 @@ def long_row_plan(long_ptr: torch.Tensor, exact_row_max: int):
     return exact.to(torch.int32), first.to(torch.int32), rows.to(torch.int32)
 
 
+CODEC_NAMES = {native.VALS_F64: "f64", native.VALS_F32: "f32", native.VALS_UNIT: "unit"}
+_CODEC_OF = {v: k for k, v in CODEC_NAMES.items()}
+_CODEC_CHUNK = 1 << 26          # values examined per pass (bounds the temporaries on 2B-nnz blocks)
+_SIGN32 = -(2 ** 31)
+
+
+def value_codec_of(vals) -> int:
+    """Narrowest lossless storage of a block's values (numpy or torch, the
+    real entries only): GRIDLP_VALS_UNIT when every value is +1.0 or -1.0,
+    GRIDLP_VALS_F32 when every value survives float32 exactly (NaN and
+    subnormals do not), else GRIDLP_VALS_F64."""
+    if isinstance(vals, np.ndarray):
+        vals = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64))
+    n = int(vals.numel())
+    unit = f32 = True
+    for a in range(0, n, _CODEC_CHUNK):
+        v = vals[a: a + _CODEC_CHUNK]
+        if unit:
+            unit = bool(((v == 1.0) | (v == -1.0)).all())
+        if not unit:
+            f32 = bool((v.float().double() == v).all())
+            if not f32:
+                break
+    return native.VALS_UNIT if unit else native.VALS_F32 if f32 else native.VALS_F64
+
+
 class DeviceCsr:
     """One block resident in HBM; `.struct` is its gridlp_csr_t.
 
@@ -216,7 +245,7 @@ class DeviceCsr:
     rows' chunked CSR and the chunk scratch live in HBM."""
 
     def __init__(self, host, device, exact_row_max: int = DEFAULT_EXACT_ROW_MAX,
-                 light_row_max: int = DEFAULT_LIGHT_ROW_MAX):
+                 light_row_max: int = DEFAULT_LIGHT_ROW_MAX, value_codec: str = "f64"):
         if not 0 <= light_row_max <= exact_row_max <= native.ROW_MAX_LIMIT:
             raise ValueError(f"need 0 <= light_row_max <= exact_row_max <= {native.ROW_MAX_LIMIT}")
         if isinstance(host, dict):      # SELL arrays already built on the device (DeviceSetup.sell)
@@ -245,6 +274,10 @@ class DeviceCsr:
         self.dev["chunk_sums"] = torch.zeros(max(self.num_chunks, 1), dtype=torch.float64, device=device)
         self.dev["chunk_done"] = torch.zeros(max(self.long_rows, 1), dtype=torch.int32, device=device)
         self.num_slices = int(sd["num_slices"])
+        self.val_codec = native.VALS_F64
+        if value_codec != "f64" and self.nnz and torch.device(device).type == "cuda":
+            real = sd["src_vals"] if isinstance(host, dict) else host.val
+            self._apply_codec(value_codec, real)
         ptr = lambda k: self.dev[k].data_ptr() if self.dev[k].numel() else None  # noqa: E731
         self.struct = native.Csr(self.num_rows, self.num_cols, self.nnz,
                                  ptr("vals"), ptr("cols"), ptr("slice_off"), ptr("lane_info"), self.num_slices,
@@ -252,6 +285,36 @@ class DeviceCsr:
                                  self.long_rows, ptr("exact_long"), self.num_exact_long,
                                  ptr("chunk_first"), ptr("chunk_row"), self.num_chunks, ptr("chunk_sums"),
                                  ptr("chunk_done"), light_row_max, exact_row_max)
+        self.struct.val_codec = self.val_codec
+
+    def _apply_codec(self, want: str, real):
+        """Re-store the values in codec `want` ("auto": the narrowest lossless
+        one; "f32" / "unit": forced, ValueError if not lossless). UNIT folds
+        the sign into bit 31 of the column indices (padding entries are never
+        read) and drops the value arrays; F32 narrows them."""
+        if want not in ("auto", "f32", "unit"):
+            raise ValueError(f"value_codec must be 'auto', 'f64', 'f32' or 'unit', not {want!r}")
+        best = value_codec_of(real)
+        if want != "auto":
+            need = _CODEC_OF[want]
+            if need > best:
+                raise ValueError(f"value_codec={want!r} is not lossless for this block's values")
+            best = need
+        if best == native.VALS_UNIT:
+            for vk, ck in (("vals", "cols"), ("long_vals", "long_cols")):
+                v, c = self.dev[vk], self.dev[ck]
+                for a in range(0, int(v.numel()), _CODEC_CHUNK):
+                    neg = (v[a: a + _CODEC_CHUNK] < 0).to(torch.int32).mul_(_SIGN32)
+                    c[a: a + _CODEC_CHUNK].bitwise_or_(neg)
+                self.dev[vk] = v[:0]
+        elif best == native.VALS_F32:
+            for vk in ("vals", "long_vals"):
+                self.dev[vk] = self.dev[vk].float()
+        self.val_codec = best
+
+    @property
+    def codec(self) -> str:
+        return CODEC_NAMES[self.val_codec]
 
     def tensors(self):
         return tuple(self.dev.values())
@@ -276,9 +339,11 @@ class DeviceCsr:
         return s
 
     def bytes_per_product(self) -> int:
-        """Algorithmic bytes of one product: 12/nnz + row pointers + one read
-        of the gathered vector + one FP64 result per row."""
-        return 12 * self.nnz + 4 * (self.num_rows + 1) + 8 * self.num_cols + 8 * self.num_rows
+        """Algorithmic bytes of one product: 12/nnz (8 / 4 with the F32 / UNIT
+        value codecs) + row pointers + one read of the gathered vector + one
+        FP64 result per row."""
+        per = 4 + (8, 4, 0)[self.val_codec]
+        return per * self.nnz + 4 * (self.num_rows + 1) + 8 * self.num_cols + 8 * self.num_rows
 
 
 def parts_src(parts, num_rows: int) -> native.Src:
@@ -553,7 +618,8 @@ class DeviceSetup:
                       self._stream())
         return dict(vals=sell_val, cols=sell_col, slice_off=slice_off, lane_info=lane_info,
                     num_slices=ns, long_rows=long_rows[:nh].clone() if nh else long_rows[:0],
-                    long_ptr=long_ptr[: nh + 1].clone(), long_cols=hcol, long_vals=hval)
+                    long_ptr=long_ptr[: nh + 1].clone(), long_cols=hcol, long_vals=hval,
+                    src_vals=a.val[: a.nnz])
 
     def release(self):
         for name in ("src_ptr", "src_col", "src_val", "col_perm", "inv_col", "row_perm", "ws"):

@@ -110,6 +110,45 @@ __device__ __forceinline__ int ld_stream(const int* p, uint64_t pol) {
                : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ float ld_stream(const float* p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// ------------------------------------------------------- value codecs
+// gridlp_csr_t.val_codec (GRIDLP_VALS_*): how a block's values are stored.
+// Every codec rebuilds the exact FP64 value before the same dmul, so the
+// products are those of FP64 storage bit for bit; only the stream bytes
+// change (12 / 8 / 4 B per nonzero).
+template <int VC> struct Vals;
+template <> struct Vals<GRIDLP_VALS_F64> {
+  using T = double;
+  static __device__ __forceinline__ T ld(const void* p, int64_t k, uint64_t pol) {
+    return ld_stream(static_cast<const double*>(p) + k, pol);
+  }
+  static __device__ __forceinline__ T zero() { return 0.0; }
+  static __device__ __forceinline__ double val(T v, int) { return v; }
+  static __device__ __forceinline__ int col(int c) { return c; }
+};
+template <> struct Vals<GRIDLP_VALS_F32> {
+  using T = float;
+  static __device__ __forceinline__ T ld(const void* p, int64_t k, uint64_t pol) {
+    return ld_stream(static_cast<const float*>(p) + k, pol);
+  }
+  static __device__ __forceinline__ T zero() { return 0.0f; }
+  static __device__ __forceinline__ double val(T v, int) { return (double)v; }   // exact widening
+  static __device__ __forceinline__ int col(int c) { return c; }
+};
+template <> struct Vals<GRIDLP_VALS_UNIT> {
+  struct T {};
+  static __device__ __forceinline__ T ld(const void*, int64_t, uint64_t) { return T{}; }
+  static __device__ __forceinline__ T zero() { return T{}; }
+  static __device__ __forceinline__ double val(T, int c) { return c < 0 ? -1.0 : 1.0; }   // sign bit
+  static __device__ __forceinline__ int col(int c) { return c & 0x7fffffff; }
+};
+
 // column-band carry: coherent (the kernel may rewrite the row), first to leave L2
 __device__ __forceinline__ double ld_carry(const double* p, uint64_t pol) {
   double v;
@@ -594,7 +633,7 @@ __device__ __forceinline__ void cta_partials(double (&acc)[Op::NRED > 0 ? Op::NR
 // a row adds the chunk sums in chunk order (deterministic) and applies the
 // fused epilogue. Launched before the slice kernel of the same product; its
 // reduction partials occupy slots [0, num_chunks).
-template <class Op>
+template <class Op, int VC>
 __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
                                                               double* __restrict__ partials, double* __restrict__ terms,
                                                               int cross_wait) {
@@ -618,22 +657,26 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
   const int64_t p0 = (int64_t)A.long_ptr[h] + (c - c0) * (int64_t)GRIDLP_HEAVY_CHUNK;
   const int64_t pe = A.long_ptr[h + 1];
   const int64_t p1 = p0 + GRIDLP_HEAVY_CHUNK < pe ? p0 + GRIDLP_HEAVY_CHUNK : pe;
+  using V = Vals<VC>;
   double s = 0.0;
   for (int64_t k0 = p0 + tid; k0 < p1; k0 += (int64_t)SELL_NT * U) {
     int cc[U];
-    double vv[U], xx[U];
+    typename V::T vv[U];
+    double xx[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t k = k0 + (int64_t)u * SELL_NT;
       cc[u] = k < p1 ? ld_stream(A.long_cols + k, pf) : 0;
-      vv[u] = k < p1 ? ld_stream(A.long_vals + k, pf) : 0.0;
+      vv[u] = k < p1 ? V::ld(A.long_vals, k, pf) : V::zero();
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int cu = V::col(cc[u]);
+      xx[u] = k0 + (int64_t)u * SELL_NT < p1 ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      xx[u] = k0 + (int64_t)u * SELL_NT < p1 ? ld_gather(g + cc[u], gather_policy(cc[u], hot, pl, pf)) : 0.0;
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (k0 + (int64_t)u * SELL_NT < p1) s = dadd(s, dmul(vv[u], xx[u]));
+      if (k0 + (int64_t)u * SELL_NT < p1) s = dadd(s, dmul(V::val(vv[u], cc[u]), xx[u]));
   }
   s = warp_sum(s);
   __shared__ double hs[SELL_WPB];
@@ -676,7 +719,7 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
 // csr_matvec. The next block's gathers and the block after's streams are in
 // flight while lane 0 runs the add chain, so a row costs about one FP64
 // add latency per entry. Reduction partials follow the heavy kernel's.
-template <class Op>
+template <class Op, int VC>
 __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const double* __restrict__ g, Op op,
                                                            double* __restrict__ partials, double* __restrict__ terms,
                                                            int cross_wait) {
@@ -699,26 +742,30 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
     const int h = A.exact_long[q];
     const int64_t p0 = A.long_ptr[h];
     const int len = A.long_ptr[h + 1] - A.long_ptr[h];
+    using V = Vals<VC>;
     const int* __restrict__ cp = A.long_cols + p0;
-    const double* __restrict__ vp = A.long_vals + p0;
+    const int64_t vp = p0;   // value index base (codec-typed loads)
     int ca[U], cb[U];
-    double va[U], vb[U], x[U];
+    typename V::T va[U], vb[U];
+    double x[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int k = 32 * u + lane, k2 = B + 32 * u + lane;
       ca[u] = k < len ? ld_stream(cp + k, pf) : 0;
-      va[u] = k < len ? ld_stream(vp + k, pf) : 0.0;
+      va[u] = k < len ? V::ld(A.long_vals, vp + k, pf) : V::zero();
       cb[u] = k2 < len ? ld_stream(cp + k2, pf) : 0;
-      vb[u] = k2 < len ? ld_stream(vp + k2, pf) : 0.0;
+      vb[u] = k2 < len ? V::ld(A.long_vals, vp + k2, pf) : V::zero();
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      x[u] = 32 * u + lane < len ? ld_gather(g + ca[u], gather_policy(ca[u], hot, pl, pf)) : 0.0;
+    for (int u = 0; u < U; ++u) {
+      const int cu = V::col(ca[u]);
+      x[u] = 32 * u + lane < len ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
+    }
     double s = A.carry ? ld_carry(A.carry + A.long_rows[h], pf) : 0.0;   // column bands: continue the chain
     for (int j0 = 0; j0 < len; j0 += B) {
       double p[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) p[u] = dmul(va[u], x[u]);
+      for (int u = 0; u < U; ++u) p[u] = dmul(V::val(va[u], ca[u]), x[u]);
       __syncwarp();
 #pragma unroll
       for (int u = 0; u < U; ++u) prod[warp][32 * u + lane] = p[u];
@@ -726,12 +773,13 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
       // in flight during the add chain: gathers of block j0+B, streams of block j0+2B
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        x[u] = j0 + B + 32 * u + lane < len ? ld_gather(g + cb[u], gather_policy(cb[u], hot, pl, pf)) : 0.0;
+        const int cu = V::col(cb[u]);
+        x[u] = j0 + B + 32 * u + lane < len ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
         ca[u] = cb[u];
         va[u] = vb[u];
         const int k = j0 + 2 * B + 32 * u + lane;
         cb[u] = k < len ? ld_stream(cp + k, pf) : 0;
-        vb[u] = k < len ? ld_stream(vp + k, pf) : 0.0;
+        vb[u] = k < len ? V::ld(A.long_vals, vp + k, pf) : V::zero();
       }
       if (lane == 0) {
         const int cnt = len - j0 < B ? len - j0 : B;
@@ -755,7 +803,7 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
 // kernels' in the slot array. Lane l of a slice's warp owns row 32 s + l,
 // sums it in a register and applies the epilogue to it directly — no shared
 // memory and no barrier on the light path.
-template <class Op>
+template <class Op, int VC>
 __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t A, const double* __restrict__ g,
                                                                    Op op, double* __restrict__ partials,
                                                                    double* __restrict__ terms, int cross_wait) {
@@ -781,25 +829,28 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
     const int info = A.lane_info[slice * 32 + lane];
     if (info >= 0) {
       const int len = info >> 8;
+      using V = Vals<VC>;
       const int64_t base = A.slice_off[slice] + lane;
       const int* __restrict__ cp = A.sell_cols + base;
-      const double* __restrict__ vp = A.sell_vals + base;
       double s = A.carry ? ld_carry(A.carry + r, pf) : 0.0;   // column bands: continue the chain
       for (int j = 0; j < len; j += U) {
         int c[U];
-        double v[U], x[U];
+        typename V::T v[U];
+        double x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const bool ok = j + u < len;
           c[u] = ok ? ld_stream(cp + 32 * (j + u), pf) : 0;
-          v[u] = ok ? ld_stream(vp + 32 * (j + u), pf) : 0.0;
+          v[u] = ok ? V::ld(A.sell_vals, base + 32 * (j + u), pf) : V::zero();
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int cu = V::col(c[u]);
+          x[u] = (j + u < len) ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
-        x[u] = (j + u < len) ? ld_gather(g + c[u], gather_policy(c[u], hot, pl, pf)) : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
+          if (j + u < len) s = dadd(s, dmul(V::val(v[u], c[u]), x[u]));
       }
       // epilogue operands are loaded after the sums: issuing them first costs
       // registers (occupancy) and measured slower (profiles/r1, variant 10)
@@ -825,7 +876,7 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
 #define GRIDLP_PIPE_U SELL_U
 #endif
 constexpr int PIPE_MINB = GRIDLP_PIPE_MINB;
-template <class Op>
+template <class Op, int VC>
 __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
                                                                         Op op, double* __restrict__ partials,
                                                                         double* __restrict__ terms, int cross_wait) {
@@ -834,18 +885,19 @@ __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int64_t slice = (int64_t)blockIdx.x * SELL_WPB + warp;
+  using V = Vals<VC>;
   const uint64_t pf = policy_evict_first();
   int info = -1, len = 0;
   const int* __restrict__ cp = nullptr;
-  const double* __restrict__ vp = nullptr;
+  int64_t vb = 0;   // value index base (codec-typed loads)
   int c[U];
-  double v[U];
+  typename V::T v[U];
   if (slice < A.num_slices) {
     info = A.lane_info[slice * 32 + lane];
     len = info >= 0 ? info >> 8 : 0;
     const int64_t base = A.slice_off[slice] + lane;
     cp = A.sell_cols + base;
-    vp = A.sell_vals + base;
+    vb = base;
   }
   // the first block's streams are constant matrix data: issued before the
   // wait on a chained predecessor product
@@ -853,7 +905,7 @@ __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_
   for (int u = 0; u < U; ++u) {
     const bool ok = u < len;
     c[u] = ok ? ld_stream(cp + 32 * u, pf) : 0;
-    v[u] = ok ? ld_stream(vp + 32 * u, pf) : 0.0;
+    v[u] = ok ? V::ld(A.sell_vals, vb + 32 * u, pf) : V::zero();
   }
   if (cross_wait) pdl_wait();
   pdl_launch_dependents();
@@ -869,20 +921,22 @@ __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_
     for (int j = 0; j < len; j += U) {
       double x[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        x[u] = (j + u < len) ? ld_gather(g + c[u], gather_policy(c[u], hot, pl, pf)) : 0.0;
+      for (int u = 0; u < U; ++u) {
+        const int cu = V::col(c[u]);
+        x[u] = (j + u < len) ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
+      }
       int cn[U];
-      double vn[U];
+      typename V::T vn[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int k = j + U + u;
         const bool ok = k < len;
         cn[u] = ok ? ld_stream(cp + 32 * k, pf) : 0;
-        vn[u] = ok ? ld_stream(vp + 32 * k, pf) : 0.0;
+        vn[u] = ok ? V::ld(A.sell_vals, vb + 32 * k, pf) : V::zero();
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (j + u < len) s = dadd(s, dmul(v[u], x[u]));
+        if (j + u < len) s = dadd(s, dmul(V::val(v[u], c[u]), x[u]));
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         c[u] = cn[u];
@@ -1495,8 +1549,12 @@ int check_csr(const gridlp_csr_t* A) {
   if (A->num_exact_long > 0 && !A->exact_long) return fail(GRIDLP_ERR_ARG, "missing exact_long");
   if (A->num_slices != (A->num_rows + 31) / 32) return fail(GRIDLP_ERR_ARG, "num_slices must be ceil(rows/32)");
   if (A->num_rows > 0 && (!A->slice_off || !A->lane_info)) return fail(GRIDLP_ERR_ARG, "missing SELL slices");
-  if (A->nnz > 0 && (!A->sell_cols || !A->sell_vals)) return fail(GRIDLP_ERR_ARG, "missing SELL arrays");
-  if (A->num_long_rows > 0 && (!A->long_rows || !A->long_ptr || !A->long_cols || !A->long_vals))
+  if (A->val_codec < GRIDLP_VALS_F64 || A->val_codec > GRIDLP_VALS_UNIT)
+    return fail(GRIDLP_ERR_ARG, "unknown val_codec");
+  const bool need_vals = A->val_codec != GRIDLP_VALS_UNIT;
+  if (A->nnz > 0 && (!A->sell_cols || (need_vals && !A->sell_vals)))
+    return fail(GRIDLP_ERR_ARG, "missing SELL arrays");
+  if (A->num_long_rows > 0 && (!A->long_rows || !A->long_ptr || !A->long_cols || (need_vals && !A->long_vals)))
     return fail(GRIDLP_ERR_ARG, "missing long-row CSR");
   if (A->num_chunks > 0 && (!A->chunk_first || !A->chunk_row || !A->chunk_sums || !A->chunk_done))
     return fail(GRIDLP_ERR_ARG, "missing heavy-row chunk directory");
@@ -1547,14 +1605,42 @@ cudaError_t launch_part(K kern, int64_t blocks, int threads, int smem, bool prog
   return cudaLaunchKernelEx(&cfg, kern, M, gather, op, partials, terms, cross_wait);
 }
 
-template <class Op>
+template <class Op, int VC>
 cudaError_t launch_light(int64_t blocks, bool programmatic, int cross_wait, cudaStream_t s, const gridlp_csr_t& M,
                          const double* gather, Op op, double* partials, double* terms) {
   if (g_sell_variant == 1)
-    return launch_part(&sell32_pipe_kernel<Op>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
+    return launch_part(&sell32_pipe_kernel<Op, VC>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
                        partials, terms);
-  return launch_part(&sell32_kernel<Op>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op, partials,
-                     terms);
+  return launch_part(&sell32_kernel<Op, VC>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
+                     partials, terms);
+}
+
+// The up-to-three kernels of one product over block M (heavy chunks, exact
+// long rows, SELL lanes), for value codec VC.
+template <class Op, int VC>
+cudaError_t launch_product(const gridlp_csr_t& M, int64_t slots, bool cross, cudaStream_t s, const double* gather,
+                           Op op, double* kpartials, double* terms) {
+  const int64_t nlong = long_blocks(&M);
+  const int64_t nlight = slots - M.num_chunks - nlong;
+  bool prev = cross;           // programmatic edge to the previous kernel
+  int cw = cross ? 1 : 0;      // the first kernel launched waits for the previous product
+  cudaError_t e = cudaSuccess;
+  if (M.num_chunks > 0) {
+    e = launch_part(&heavy_chunk_kernel<Op, VC>, M.num_chunks, SELL_NT, 0, prev, cw, s, M, gather, op, kpartials,
+                    terms);
+    prev = true;
+    cw = 0;
+  }
+  if (e == cudaSuccess && nlong > 0) {
+    e = launch_part(&long_row_kernel<Op, VC>, nlong, SELL_NT, 0, prev, cw, s, M, gather, op,
+                    kpartials ? kpartials + M.num_chunks * GRIDLP_MAX_RED : nullptr, terms);
+    prev = true;
+    cw = 0;
+  }
+  if (e == cudaSuccess && nlight > 0)
+    e = launch_light<Op, VC>(nlight, prev, cw, s, M, gather, op,
+                             kpartials ? kpartials + (M.num_chunks + nlong) * GRIDLP_MAX_RED : nullptr, terms);
+  return e;
 }
 
 // One op. `cross`: the product's first kernel is chained to the previous
@@ -1609,26 +1695,13 @@ int launch_op(const gridlp_src_t* src, Op op, const gridlp_red_t* red, void* str
   if (slots > 0) {
     if (src->A) {
       const gridlp_csr_t& M = *src->A;
-      const int64_t nlong = long_blocks(&M);
-      const int64_t nlight = slots - M.num_chunks - nlong;
-      bool prev = cross;           // programmatic edge to the previous kernel
-      int cw = cross ? 1 : 0;      // the first kernel launched waits for the previous product
-      cudaError_t e = cudaSuccess;
-      if (M.num_chunks > 0) {
-        e = launch_part(&heavy_chunk_kernel<Op>, M.num_chunks, SELL_NT, 0, prev, cw, s, M, src->gather, op,
-                        kpartials, terms);
-        prev = true;
-        cw = 0;
-      }
-      if (e == cudaSuccess && nlong > 0) {
-        e = launch_part(&long_row_kernel<Op>, nlong, SELL_NT, 0, prev, cw, s, M, src->gather, op,
-                        kpartials ? kpartials + M.num_chunks * GRIDLP_MAX_RED : nullptr, terms);
-        prev = true;
-        cw = 0;
-      }
-      if (e == cudaSuccess && nlight > 0)
-        e = launch_light(nlight, prev, cw, s, M, src->gather, op,
-                         kpartials ? kpartials + (M.num_chunks + nlong) * GRIDLP_MAX_RED : nullptr, terms);
+      cudaError_t e;
+      if (M.val_codec == GRIDLP_VALS_UNIT)
+        e = launch_product<Op, GRIDLP_VALS_UNIT>(M, slots, cross, s, src->gather, op, kpartials, terms);
+      else if (M.val_codec == GRIDLP_VALS_F32)
+        e = launch_product<Op, GRIDLP_VALS_F32>(M, slots, cross, s, src->gather, op, kpartials, terms);
+      else
+        e = launch_product<Op, GRIDLP_VALS_F64>(M, slots, cross, s, src->gather, op, kpartials, terms);
       if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
     } else
       rows_kernel<Op><<<(unsigned)slots, TPB, 0, s>>>(*src, n, op, partials,
@@ -1901,6 +1974,8 @@ int gridlp_cluster_plan(const gridlp_src_t* primal_src, const gridlp_src_t* dual
     return fail(GRIDLP_ERR_ARG, "cluster_plan: A and A^T shapes disagree");
   if (AT->num_long_rows > 0 || A->num_long_rows > 0 || AT->carry || A->carry)
     return fail(GRIDLP_ERR_UNSUPPORTED, "cluster_plan: long rows / column bands need the graph path");
+  if (AT->val_codec != GRIDLP_VALS_F64 || A->val_codec != GRIDLP_VALS_F64)
+    return fail(GRIDLP_ERR_UNSUPPORTED, "cluster_plan: compact value codecs need the graph path");
   const int64_t n = AT->num_rows, m = A->num_rows;
   constexpr int64_t SMEM_MAX = 227 * 1024;
   if (8 * (n + m) + 12 * (AT->nnz + A->nnz) / CLUSTER_CTAS > SMEM_MAX || AT->num_slices > (1 << 16) ||
@@ -2069,6 +2144,8 @@ int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_
   if (rc) return rc;
   if (AT->num_chunks > 0 || A->num_chunks > 0)
     return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_persistent: heavy (chunked) rows need the graph path");
+  if (AT->val_codec != GRIDLP_VALS_F64 || A->val_codec != GRIDLP_VALS_F64)
+    return fail(GRIDLP_ERR_UNSUPPORTED, "pdhg_iterate_persistent: compact value codecs need the graph path");
   if (AT->num_rows != pv->n || A->num_rows != dv->m)
     return fail(GRIDLP_ERR_ARG, "pdhg_iterate_persistent: length mismatch");
   if (n_iters == 0) return GRIDLP_OK;

@@ -99,6 +99,15 @@ class EngineOptions:
     # band problems on the single-process grid: length-class order from a
     # counting pass over the generated blocks (False: layout order)
     band_class_order: bool = True
+    # value storage per block (gridlp_csr_t.val_codec): "auto" = the
+    # narrowest LOSSLESS codec of the block's values (+-1 only: sign bit in
+    # the column index, 4 B/nnz; all exactly float: 8 B/nnz; else FP64,
+    # 12 B/nnz) for blocks of at least value_codec_min_nnz nonzeros (smaller
+    # blocks sit in L2 / in one cluster's shared memory, where the bytes do
+    # not matter and the cluster launch needs FP64); "f64" = always FP64.
+    # Products are bit-identical either way.
+    value_codec: str = "auto"
+    value_codec_min_nnz: int = 1 << 20
     device_setup: bool = True
     # gathered vectors larger than this many bytes keep only their first
     # hot_gather_bytes (the highest-degree columns / longest rows in the
@@ -456,7 +465,8 @@ class PdhgEngine:
                     ho = self._host_order
                     hb = permute_csr(hb, ho(self.row_order[i]), ho(self.col_inv[j]))
                     ht = permute_csr(ht, ho(self.col_order[j]), ho(self.row_inv[i]))
-                self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, **kw), DeviceCsr(ht, dev, **kw))
+                self.blocks[(i, j)] = BlockState(i, j, DeviceCsr(hb, dev, value_codec=self._codec_for(hb.nnz), **kw),
+                                                 DeviceCsr(ht, dev, value_codec=self._codec_for(ht.nnz), **kw))
         if on_device:
             t0 = time.perf_counter()
             setup.release()     # the freed setup buffers stay in torch's caching allocator for reuse
@@ -475,6 +485,9 @@ class PdhgEngine:
                                          for (i, j), b in self.blocks.items() for k in ("A", "AT")}
         self.choices["column_bands"] = {f"{k}{i},{j}": len(getattr(getattr(b, k), "bands", [None]))
                                         for (i, j), b in self.blocks.items() for k in ("A", "AT")}
+        self.choices["value_codec"] = {
+            f"{k}{i},{j}": ",".join(sorted({d.codec for d in getattr(getattr(b, k), "bands", [getattr(b, k)])}))
+            for (i, j), b in self.blocks.items() for k in ("A", "AT")}
         self._banded = any(isinstance(m, BandedCsr) for b in self.blocks.values() for m in (b.A, b.AT))
         hot = int(self.opts.hot_gather_bytes) // 8
         for b in self.blocks.values():
@@ -493,10 +506,15 @@ class PdhgEngine:
         self.passes = 0
 
     # ------------------------------------------------- layout choices
+    def _codec_for(self, nnz: int) -> str:
+        o = self.opts
+        return o.value_codec if nnz >= o.value_codec_min_nnz else "f64"
+
     def _sell_csr(self, setup, arr, light: int) -> DeviceCsr:
         d = setup.sell(arr, light)
         d["shape"] = (arr.num_rows, arr.num_cols, arr.nnz)
-        return DeviceCsr(d, self.device, exact_row_max=self.opts.exact_row_max, light_row_max=light)
+        return DeviceCsr(d, self.device, exact_row_max=self.opts.exact_row_max, light_row_max=light,
+                         value_codec=self._codec_for(arr.nnz))
 
     def _time_products(self, mats) -> float:
         """Median device time of one product with each matrix (summed), on

@@ -37,6 +37,11 @@ NVCC_FLAGS = [
 ]
 
 
+ABI_VERSION = 2
+# gridlp_csr_t.val_codec (include/gridlp_b200.h GRIDLP_VALS_*)
+VALS_F64, VALS_F32, VALS_UNIT = 0, 1, 2
+
+
 class Csr(ctypes.Structure):
     _fields_ = [("num_rows", c_int64), ("num_cols", c_int64), ("nnz", c_int64),
                 ("sell_vals", c_void_p), ("sell_cols", c_void_p), ("slice_off", c_void_p),
@@ -47,7 +52,7 @@ class Csr(ctypes.Structure):
                 ("chunk_first", c_void_p), ("chunk_row", c_void_p), ("num_chunks", c_int64),
                 ("chunk_sums", c_void_p), ("chunk_done", c_void_p),
                 ("light_row_max", c_int32), ("exact_row_max", c_int32), ("carry", c_void_p),
-                ("hot_cols", c_int64)]
+                ("hot_cols", c_int64), ("val_codec", c_int32), ("reserved_codec", c_int32)]
 
 
 class Peer(ctypes.Structure):
@@ -201,8 +206,8 @@ class Library:
             fn.argtypes = args
             fn.restype = res
         ver = self._lib.gridlp_abi_version()
-        if ver != 1:
-            raise GridlpError(f"ABI version {ver} != 1")
+        if ver != ABI_VERSION:
+            raise GridlpError(f"ABI version {ver} != {ABI_VERSION}")
 
     def symbols(self):
         return list(SIGNATURES)

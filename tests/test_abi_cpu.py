@@ -34,7 +34,7 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_abi_version_and_error_string(lib):
-    assert lib._lib.gridlp_abi_version() == 1
+    assert lib._lib.gridlp_abi_version() == 2
     assert isinstance(lib.last_error(), str)
 
 
