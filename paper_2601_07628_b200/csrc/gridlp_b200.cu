@@ -876,8 +876,10 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
 #define GRIDLP_PIPE_U SELL_U
 #endif
 constexpr int PIPE_MINB = GRIDLP_PIPE_MINB;
-template <class Op, int VC>
-__global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
+// the EARLY variant holds the epilogue operands across the row: a 56-register
+// budget (36 warps/SM) instead of 48 keeps it spill-free
+template <class Op, int VC, bool EARLY = false>
+__global__ void __launch_bounds__(SELL_NT, EARLY ? 36 / GRIDLP_SELL_WPB : PIPE_MINB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
                                                                         Op op, double* __restrict__ partials,
                                                                         double* __restrict__ terms, int cross_wait) {
   constexpr int U = GRIDLP_PIPE_U;
@@ -917,6 +919,12 @@ __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_
   const int64_t hot = hot_limit(A);
   if (info >= 0) {
     const int64_t r = slice * 32 + lane;
+    // EARLY (sell_variant 2): the epilogue operands are requested before the
+    // row's gathers, so a short row costs one memory round trip less (they
+    // do not depend on the sum; every producer of them completed before the
+    // chained wait above)
+    typename Op::Data d_early;
+    if constexpr (EARLY) d_early = op.load(r);
     double s = A.carry ? ld_carry(A.carry + r, pf) : 0.0;   // column bands: continue the chain
     for (int j = 0; j < len; j += U) {
       double x[U];
@@ -943,8 +951,12 @@ __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_
         v[u] = vn[u];
       }
     }
-    const typename Op::Data d = op.load(r);
-    emit_row(op, r, s, d, acc, terms, A.num_rows);
+    if constexpr (EARLY) {
+      emit_row(op, r, s, d_early, acc, terms, A.num_rows);
+    } else {
+      const typename Op::Data d = op.load(r);
+      emit_row(op, r, s, d, acc, terms, A.num_rows);
+    }
   }
   cta_partials<Op>(acc, partials);
   product_cta_done(op);
@@ -1564,10 +1576,13 @@ int check_csr(const gridlp_csr_t* A) {
 int64_t long_blocks(const gridlp_csr_t* A) { return (A->num_exact_long + SELL_WPB - 1) / SELL_WPB; }
 
 // ---- light-row kernel variant (gridlp_set_tuning "sell_variant"):
-//  0 = sell32_kernel, 1 = sell32_pipe_kernel (streams one step block ahead).
+//  0 = sell32_kernel, 1 = sell32_pipe_kernel (streams one step block ahead),
+//  2 = sell32_pipe_kernel with the epilogue operands requested before the
+//      gathers (default: cfg2 175.1-175.6 vs 178.4-180.2 us per iteration,
+//      cfg3 / cfg4 within noise; profiles/r2/README.md).
 // (TMA-staged streams with persistent warps were measured 1.9-2.3x slower on
 // cfg2 / cfg3 and removed: profiles/r2/ncu_cfg2_tma_8x2_dual_rejected.md.)
-int g_sell_variant = 1;
+int g_sell_variant = 2;
 int g_chain_products = 1;           // pdhg_iterate: programmatic launch between products
 
 int64_t light_blocks(const gridlp_csr_t* A) {
@@ -1611,6 +1626,9 @@ cudaError_t launch_light(int64_t blocks, bool programmatic, int cross_wait, cuda
   if (g_sell_variant == 1)
     return launch_part(&sell32_pipe_kernel<Op, VC>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
                        partials, terms);
+  if (g_sell_variant == 2)
+    return launch_part(&sell32_pipe_kernel<Op, VC, true>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M,
+                       gather, op, partials, terms);
   return launch_part(&sell32_kernel<Op, VC>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
                      partials, terms);
 }
@@ -1778,7 +1796,7 @@ int gridlp_set_tuning(const char* key, int64_t value) {
   if (!key) return fail(GRIDLP_ERR_ARG, "set_tuning: null key");
   const std::string k(key);
   if (k == "sell_variant") {
-    if (value < 0 || value > 1) return fail(GRIDLP_ERR_ARG, "set_tuning: sell_variant must be 0 or 1");
+    if (value < 0 || value > 2) return fail(GRIDLP_ERR_ARG, "set_tuning: sell_variant must be 0, 1 or 2");
     g_sell_variant = (int)value;
   } else if (k == "chain_products") {
     g_chain_products = value != 0;
