@@ -615,8 +615,6 @@ def run_ours(args, rank, world, local_rank):
         over["first_touch_cols"] = False
     if args.graph_nccl:
         over["graph_nccl"] = True
-    if args.hot_mb is not None:
-        over["hot_gather_bytes"] = int(args.hot_mb) << 20
     if args.value_codec is not None:
         over["value_codec"] = args.value_codec
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
@@ -803,7 +801,6 @@ def main():
     ap.add_argument("--band-mb", type=int, default=None, help="EngineOptions.band_bytes in MiB")
     ap.add_argument("--no-first-touch", action="store_true", help="EngineOptions.first_touch_cols=False")
     ap.add_argument("--graph-nccl", action="store_true", help="capture NCCL iterations in CUDA graphs (default now)")
-    ap.add_argument("--hot-mb", type=int, default=None, help="EngineOptions.hot_gather_bytes in MiB (0 = off)")
     ap.add_argument("--value-codec", choices=("auto", "f64"), default=None,
                     help="EngineOptions.value_codec (lossless compact value storage; default auto)")
     ap.add_argument("--grid", default=None, help="RxC virtual grid on one GPU (load-balance study)")

@@ -128,11 +128,9 @@ typedef struct gridlp_csr {
    * Chunked rows (> exact_row_max) must lie wholly in the last band (their
    * carry is then 0 and ignored). NULL = start from 0.0. */
   const double* carry;
-  /* L2 residency of the gathered vector: entries [0, hot_cols) are gathered
-   * with L2 evict_last, the rest with evict_first, so that when the vector
-   * is larger than L2 its most-used prefix stays resident (the engine's
-   * length-class order puts the highest-degree columns first). <= 0: every
-   * gather evict_last. Picks a cache policy, never a value. */
+  /* Reserved (ignored). Round 2 used it to split the gathers' L2 policy at
+   * a hot prefix; measured without gain and removed from the kernels (every
+   * gather is L2 evict_last). */
   int64_t hot_cols;
   /* GRIDLP_VALS_*: how sell_vals / long_vals store the values (F32: cast the
    * pointers to const float*; UNIT: both NULL allowed, sell_cols / long_cols
@@ -251,6 +249,11 @@ typedef struct gridlp_red {
 
 /* --- library / device ---------------------------------------------------- */
 int gridlp_abi_version(void);
+/* Build variant: GRIDLP_BUILD_CHECKED set in the bounds-checked test build
+ * (-DGRIDLP_CHECKED: gather indices, SELL lane extents, long-row ranges and
+ * written rows verified in the kernels, trap on violation); 0 otherwise. */
+#define GRIDLP_BUILD_CHECKED 1
+int gridlp_build_flags(void);
 const char* gridlp_last_error(void);
 /* SM count and L2 size of `device` (host ints). */
 int gridlp_device_info(int device, int32_t* sm_count, int64_t* l2_bytes);

@@ -57,6 +57,25 @@ int check_launch(const char* what) {
 }
 
 // ---------------------------------------------------------------- device math
+// Bounds-checked build (-DGRIDLP_CHECKED, native.build(checked=True),
+// tests/test_gpu_bounds.py): every gather index, SELL lane extent, long-row
+// range and written row is verified in the kernel; a violation prints where
+// and traps. The product build compiles the checks away.
+#ifdef GRIDLP_CHECKED
+#define GRIDLP_CHECK(cond, what)                                                                      \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("GRIDLP_CHECK failed: %s at %s:%d (block %d, thread %d)\n", what, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                      \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define GRIDLP_CHECK(cond, what) \
+  do {                           \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -170,13 +189,11 @@ __device__ __forceinline__ double ld_once(const double* p, uint64_t pol) {
 __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
-// gather policy of column c: the hot prefix [0, hot) stays in L2
-__device__ __forceinline__ uint64_t gather_policy(int64_t c, int64_t hot, uint64_t pl, uint64_t pf) {
-  return c < hot ? pl : pf;
-}
-__device__ __forceinline__ int64_t hot_limit(const gridlp_csr_t& A) {
-  return A.hot_cols > 0 ? A.hot_cols : (int64_t)0x7fffffffffffffffLL;
-}
+// Gathers are L2 evict_last (a warp-uniform policy descriptor). A per-column
+// policy split (hot prefix evict_last, rest evict_first: gridlp_csr_t
+// .hot_cols in round 2) was measured without gain on cfg3 and cost ~10
+// instructions per gather (a per-lane descriptor moved into a uniform
+// register), so it was removed; hot_cols is reserved.
 
 // ------------------------------------------- programmatic dependent launch
 // The heavy-chunk, long-row and SELL kernels of one product touch disjoint
@@ -585,6 +602,7 @@ constexpr int SELL_MINB = 48 / SELL_WPB;   // 48 warps per SM at <= 42 registers
 template <class Op>
 __device__ __forceinline__ void emit_row(const Op& op, int64_t r, double s, const typename Op::Data& d,
                                          double* acc, double* __restrict__ terms, int64_t n) {
+  GRIDLP_CHECK(r >= 0 && r < n, "row index outside the block");
   if constexpr (Op::NRED > 0) {
     if (terms) {
       double t[Op::NRED];
@@ -647,7 +665,6 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
-  const int64_t hot = hot_limit(A);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int64_t c = blockIdx.x;
@@ -657,6 +674,8 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
   const int64_t p0 = (int64_t)A.long_ptr[h] + (c - c0) * (int64_t)GRIDLP_HEAVY_CHUNK;
   const int64_t pe = A.long_ptr[h + 1];
   const int64_t p1 = p0 + GRIDLP_HEAVY_CHUNK < pe ? p0 + GRIDLP_HEAVY_CHUNK : pe;
+  GRIDLP_CHECK(h >= 0 && h < A.num_long_rows && c0 >= 0 && c - c0 < nch && p0 < pe && pe <= A.nnz,
+               "heavy chunk outside its row / the block");
   using V = Vals<VC>;
   double s = 0.0;
   for (int64_t k0 = p0 + tid; k0 < p1; k0 += (int64_t)SELL_NT * U) {
@@ -672,7 +691,8 @@ __global__ void __launch_bounds__(SELL_NT) heavy_chunk_kernel(gridlp_csr_t A, co
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int cu = V::col(cc[u]);
-      xx[u] = k0 + (int64_t)u * SELL_NT < p1 ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
+      GRIDLP_CHECK(k0 + (int64_t)u * SELL_NT >= p1 || (cu >= 0 && cu < A.num_cols), "heavy-row gather index");
+      xx[u] = k0 + (int64_t)u * SELL_NT < p1 ? ld_gather(g + cu, pl) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -735,13 +755,13 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
-  const int64_t hot = hot_limit(A);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t q = (int64_t)blockIdx.x * SELL_WPB + warp;
   if (q < A.num_exact_long) {
     const int h = A.exact_long[q];
     const int64_t p0 = A.long_ptr[h];
     const int len = A.long_ptr[h + 1] - A.long_ptr[h];
+    GRIDLP_CHECK(h >= 0 && h < A.num_long_rows && len >= 0 && p0 + len <= A.nnz, "long row outside the block");
     using V = Vals<VC>;
     const int* __restrict__ cp = A.long_cols + p0;
     const int64_t vp = p0;   // value index base (codec-typed loads)
@@ -759,7 +779,8 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int cu = V::col(ca[u]);
-      x[u] = 32 * u + lane < len ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
+      GRIDLP_CHECK(32 * u + lane >= len || (cu >= 0 && cu < A.num_cols), "long-row gather index");
+      x[u] = 32 * u + lane < len ? ld_gather(g + cu, pl) : 0.0;
     }
     double s = A.carry ? ld_carry(A.carry + A.long_rows[h], pf) : 0.0;   // column bands: continue the chain
     for (int j0 = 0; j0 < len; j0 += B) {
@@ -774,7 +795,8 @@ __global__ void __launch_bounds__(SELL_NT) long_row_kernel(gridlp_csr_t A, const
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int cu = V::col(cb[u]);
-        x[u] = j0 + B + 32 * u + lane < len ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
+        GRIDLP_CHECK(j0 + B + 32 * u + lane >= len || (cu >= 0 && cu < A.num_cols), "long-row gather index");
+        x[u] = j0 + B + 32 * u + lane < len ? ld_gather(g + cu, pl) : 0.0;
         ca[u] = cb[u];
         va[u] = vb[u];
         const int k = j0 + 2 * B + 32 * u + lane;
@@ -821,7 +843,6 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
   op.prepare();
   const uint64_t pf = policy_evict_first();
   const uint64_t pl = policy_evict_last();
-  const int64_t hot = hot_limit(A);
   const int64_t slice = (int64_t)blockIdx.x * SELL_WPB + warp;
   if (slice < A.num_slices) {
     // lane = row & 31 (sell_plan): the lane's sum is its own row's
@@ -831,6 +852,8 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
       const int len = info >> 8;
       using V = Vals<VC>;
       const int64_t base = A.slice_off[slice] + lane;
+      GRIDLP_CHECK((info & 31) == lane && (len == 0 || base + 32 * (int64_t)(len - 1) < A.slice_off[slice + 1]),
+                   "SELL lane outside its slice");
       const int* __restrict__ cp = A.sell_cols + base;
       double s = A.carry ? ld_carry(A.carry + r, pf) : 0.0;   // column bands: continue the chain
       for (int j = 0; j < len; j += U) {
@@ -846,7 +869,8 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int cu = V::col(c[u]);
-          x[u] = (j + u < len) ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
+          GRIDLP_CHECK(j + u >= len || (cu >= 0 && cu < A.num_cols), "SELL gather index");
+          x[u] = (j + u < len) ? ld_gather(g + cu, pl) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -898,6 +922,9 @@ __global__ void __launch_bounds__(SELL_NT, EARLY ? 36 / GRIDLP_SELL_WPB : PIPE_M
     info = A.lane_info[slice * 32 + lane];
     len = info >= 0 ? info >> 8 : 0;
     const int64_t base = A.slice_off[slice] + lane;
+    GRIDLP_CHECK(info < 0 || ((info & 31) == lane && (len == 0 || base + 32 * (int64_t)(len - 1) <
+                                                                      A.slice_off[slice + 1])),
+                 "SELL lane outside its slice");
     cp = A.sell_cols + base;
     vb = base;
   }
@@ -916,7 +943,6 @@ __global__ void __launch_bounds__(SELL_NT, EARLY ? 36 / GRIDLP_SELL_WPB : PIPE_M
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
   op.prepare();
   const uint64_t pl = policy_evict_last();
-  const int64_t hot = hot_limit(A);
   if (info >= 0) {
     const int64_t r = slice * 32 + lane;
     // EARLY (sell_variant 2): the epilogue operands are requested before the
@@ -931,7 +957,8 @@ __global__ void __launch_bounds__(SELL_NT, EARLY ? 36 / GRIDLP_SELL_WPB : PIPE_M
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int cu = V::col(c[u]);
-        x[u] = (j + u < len) ? ld_gather(g + cu, gather_policy(cu, hot, pl, pf)) : 0.0;
+        GRIDLP_CHECK(j + u >= len || (cu >= 0 && cu < A.num_cols), "SELL gather index");
+        x[u] = (j + u < len) ? ld_gather(g + cu, pl) : 0.0;
       }
       int cn[U];
       typename V::T vn[U];
@@ -1758,6 +1785,14 @@ gridlp_src_t rows_src(int64_t n) {
 extern "C" {
 
 int gridlp_abi_version(void) { return GRIDLP_ABI_VERSION; }
+
+int gridlp_build_flags(void) {
+#ifdef GRIDLP_CHECKED
+  return GRIDLP_BUILD_CHECKED;
+#else
+  return 0;
+#endif
+}
 
 const char* gridlp_last_error(void) { return g_err.c_str(); }
 

@@ -109,12 +109,6 @@ class EngineOptions:
     value_codec: str = "auto"
     value_codec_min_nnz: int = 1 << 20
     device_setup: bool = True
-    # gathered vectors larger than this many bytes keep only their first
-    # hot_gather_bytes (the highest-degree columns / longest rows in the
-    # length-class order) at L2 evict_last; the rest is gathered evict_first
-    # (gridlp_csr_t.hot_cols). 0 = every gather evict_last. Cache policy
-    # only: results are unchanged.
-    hot_gather_bytes: int = 0
     use_graphs: bool = True
     # capture the NCCL executor's iterations (kernels + NCCL collectives) in
     # a CUDA graph too, as the single-GPU and peer executors do
@@ -489,12 +483,6 @@ class PdhgEngine:
             f"{k}{i},{j}": ",".join(sorted({d.codec for d in getattr(getattr(b, k), "bands", [getattr(b, k)])}))
             for (i, j), b in self.blocks.items() for k in ("A", "AT")}
         self._banded = any(isinstance(m, BandedCsr) for b in self.blocks.values() for m in (b.A, b.AT))
-        hot = int(self.opts.hot_gather_bytes) // 8
-        for b in self.blocks.values():
-            for m in (b.A, b.AT):
-                if isinstance(m, DeviceCsr) and self.sorted and hot > 0 and m.num_cols > hot:
-                    m.struct.hot_cols = hot
-        self.choices["hot_gather_bytes"] = int(self.opts.hot_gather_bytes) if self.sorted else 0
         tensors = [t for b in self.blocks.values() for d in (b.A, b.AT) for t in d.tensors()]
         tensors += [t for c in self.cols.values() for t in (c.c, c.lo, c.hi)]
         tensors += [t for r in self.rows.values() for t in (r.lo, r.hi)]

@@ -16,6 +16,11 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libgridlp_b200.so"
+# the bounds-checked build (-DGRIDLP_CHECKED: every gather index, SELL lane
+# extent, long-row range and written row verified in the kernels, a trap on
+# violation) — test infrastructure (tests/test_gpu_bounds.py), selected by
+# the GRIDLP_LIB environment variable, never by the product path
+CHECKED_LIB_PATH = LIB_DIR / "libgridlp_b200_checked.so"
 SOURCES = [PKG / "csrc" / "gridlp_b200.cu", PKG / "csrc" / "gridlp_setup.cu", PKG / "csrc" / "gridlp_gen.cu",
            PKG / "csrc" / "gridlp_scale.cu"]
 HEADER = ROOT / "include" / "gridlp_b200.h"
@@ -98,6 +103,7 @@ class Red(ctypes.Structure):
 _P = c_void_p
 SIGNATURES = {
     "gridlp_abi_version": ([], c_int),
+    "gridlp_build_flags": ([], c_int),
     "gridlp_last_error": ([], ctypes.c_char_p),
     "gridlp_device_info": ([c_int, POINTER(c_int32), POINTER(c_int64)], c_int),
     "gridlp_enable_peer_access": ([c_int], c_int),
@@ -168,22 +174,24 @@ SIGNATURES = {
 }
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, checked: bool = False) -> Path:
     """nvcc the library for sm_100a into the package (in-tree, so it ships
-    with the repo snapshot to the GPU box)."""
+    with the repo snapshot to the GPU box). checked=True builds the
+    bounds-checked test variant (CHECKED_LIB_PATH) instead."""
     LIB_DIR.mkdir(exist_ok=True)
+    out = CHECKED_LIB_PATH if checked else LIB_PATH
     newest = max(p.stat().st_mtime for p in SOURCES + [HEADER])
-    if not force and LIB_PATH.exists() and LIB_PATH.stat().st_mtime >= newest:
-        return LIB_PATH
+    if not force and out.exists() and out.stat().st_mtime >= newest:
+        return out
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-Xptxas", "-v" if verbose else "-O3",
-           "-I", str(ROOT / "include"), "-o", str(LIB_PATH), *map(str, SOURCES)]
+    cmd = [nvcc, *NVCC_FLAGS, "-Xptxas", "-v" if verbose else "-O3", *(["-DGRIDLP_CHECKED"] if checked else []),
+           "-I", str(ROOT / "include"), "-o", str(out), *map(str, SOURCES)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
     if verbose:
         print(res.stderr)
-    return LIB_PATH
+    return out
 
 
 class GridlpError(RuntimeError):
@@ -244,5 +252,6 @@ _LIB: Library | None = None
 def load() -> Library:
     global _LIB
     if _LIB is None:
-        _LIB = Library()
+        alt = os.environ.get("GRIDLP_LIB")
+        _LIB = Library(Path(alt)) if alt else Library()
     return _LIB

@@ -74,7 +74,7 @@ def test_products_bitwise_every_variant(tuning, variant, light):
     ops0.store(Fused(A, xd), out0, slot=0)
     assert torch.equal(out, out0)
     assert sq == float(ops0.read_slots(1)[0, 0])     # canonical row-order reduction
-    A.struct.hot_cols = h.num_cols // 3              # L2 policy split of the gathers: same values
+    A.struct.hot_cols = h.num_cols // 3              # reserved field: ignored by the kernels
     out1 = torch.empty_like(out)
     ops0.store(Fused(A, xd), out1)
     assert torch.equal(out, out1)
