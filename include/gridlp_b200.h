@@ -264,10 +264,8 @@ int gridlp_enable_peer_access(int peer_device);
 int64_t gridlp_op_slots(const gridlp_src_t* src);
 /* Process-wide kernel knobs (no reference counterpart; results are
  * bit-identical for every value — they pick kernels, not arithmetic):
- *   "sell_variant"    2 = SELL lanes with the column/value streams issued
- *                     one step block ahead of the gathers and the epilogue
- *                     operands requested before them (default),
- *                     1 = the same without the early epilogue loads,
+ *   "sell_variant"    1 = SELL lanes with the column/value streams issued
+ *                     one step block ahead of the gathers (default),
  *                     0 = the round-1 kernel (streams, then gathers)
  *   "chain_products"  gridlp_pdhg_iterate chains its products by
  *                     programmatic dependent launch (default 1)

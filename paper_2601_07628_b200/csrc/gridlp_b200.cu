@@ -900,10 +900,8 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
 #define GRIDLP_PIPE_U SELL_U
 #endif
 constexpr int PIPE_MINB = GRIDLP_PIPE_MINB;
-// the EARLY variant holds the epilogue operands across the row: a 56-register
-// budget (36 warps/SM) instead of 48 keeps it spill-free
-template <class Op, int VC, bool EARLY = false>
-__global__ void __launch_bounds__(SELL_NT, EARLY ? 36 / GRIDLP_SELL_WPB : PIPE_MINB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
+template <class Op, int VC>
+__global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
                                                                         Op op, double* __restrict__ partials,
                                                                         double* __restrict__ terms, int cross_wait) {
   constexpr int U = GRIDLP_PIPE_U;
@@ -945,12 +943,6 @@ __global__ void __launch_bounds__(SELL_NT, EARLY ? 36 / GRIDLP_SELL_WPB : PIPE_M
   const uint64_t pl = policy_evict_last();
   if (info >= 0) {
     const int64_t r = slice * 32 + lane;
-    // EARLY (sell_variant 2): the epilogue operands are requested before the
-    // row's gathers, so a short row costs one memory round trip less (they
-    // do not depend on the sum; every producer of them completed before the
-    // chained wait above)
-    typename Op::Data d_early;
-    if constexpr (EARLY) d_early = op.load(r);
     double s = A.carry ? ld_carry(A.carry + r, pf) : 0.0;   // column bands: continue the chain
     for (int j = 0; j < len; j += U) {
       double x[U];
@@ -978,12 +970,8 @@ __global__ void __launch_bounds__(SELL_NT, EARLY ? 36 / GRIDLP_SELL_WPB : PIPE_M
         v[u] = vn[u];
       }
     }
-    if constexpr (EARLY) {
-      emit_row(op, r, s, d_early, acc, terms, A.num_rows);
-    } else {
-      const typename Op::Data d = op.load(r);
-      emit_row(op, r, s, d, acc, terms, A.num_rows);
-    }
+    const typename Op::Data d = op.load(r);
+    emit_row(op, r, s, d, acc, terms, A.num_rows);
   }
   cta_partials<Op>(acc, partials);
   product_cta_done(op);
@@ -1603,13 +1591,12 @@ int check_csr(const gridlp_csr_t* A) {
 int64_t long_blocks(const gridlp_csr_t* A) { return (A->num_exact_long + SELL_WPB - 1) / SELL_WPB; }
 
 // ---- light-row kernel variant (gridlp_set_tuning "sell_variant"):
-//  0 = sell32_kernel, 1 = sell32_pipe_kernel (streams one step block ahead),
-//  2 = sell32_pipe_kernel with the epilogue operands requested before the
-//      gathers (default: cfg2 175.1-175.6 vs 178.4-180.2 us per iteration,
-//      cfg3 / cfg4 within noise; profiles/r2/README.md).
+//  0 = sell32_kernel, 1 = sell32_pipe_kernel (streams one step block ahead).
+// (Requesting the epilogue operands before the gathers was measured slower
+// in an interleaved A/B: profiles/r2/ab_sell_variant_cfg*.json.)
 // (TMA-staged streams with persistent warps were measured 1.9-2.3x slower on
 // cfg2 / cfg3 and removed: profiles/r2/ncu_cfg2_tma_8x2_dual_rejected.md.)
-int g_sell_variant = 2;
+int g_sell_variant = 1;
 int g_chain_products = 1;           // pdhg_iterate: programmatic launch between products
 
 int64_t light_blocks(const gridlp_csr_t* A) {
@@ -1653,9 +1640,6 @@ cudaError_t launch_light(int64_t blocks, bool programmatic, int cross_wait, cuda
   if (g_sell_variant == 1)
     return launch_part(&sell32_pipe_kernel<Op, VC>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
                        partials, terms);
-  if (g_sell_variant == 2)
-    return launch_part(&sell32_pipe_kernel<Op, VC, true>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M,
-                       gather, op, partials, terms);
   return launch_part(&sell32_kernel<Op, VC>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
                      partials, terms);
 }
@@ -1831,7 +1815,7 @@ int gridlp_set_tuning(const char* key, int64_t value) {
   if (!key) return fail(GRIDLP_ERR_ARG, "set_tuning: null key");
   const std::string k(key);
   if (k == "sell_variant") {
-    if (value < 0 || value > 2) return fail(GRIDLP_ERR_ARG, "set_tuning: sell_variant must be 0, 1 or 2");
+    if (value < 0 || value > 1) return fail(GRIDLP_ERR_ARG, "set_tuning: sell_variant must be 0 or 1");
     g_sell_variant = (int)value;
   } else if (k == "chain_products") {
     g_chain_products = value != 0;

@@ -227,7 +227,7 @@ def test_tuning_knobs_are_host_only_and_validated(lib):
     finally:
         for k, v in saved.items():
             lib.set_tuning(k, v)
-    assert saved == {"sell_variant": 2, "chain_products": 1}
+    assert saved == {"sell_variant": 1, "chain_products": 1}
 
 
 def test_cluster_and_persistent_entry_points_validate_arguments(lib):

@@ -21,7 +21,7 @@ from paper_2601_07628_b200.blocks import DeviceCsr, HostCsr  # noqa: E402
 from paper_2601_07628_b200.ops import CudaOps, Fused  # noqa: E402
 
 DEV = torch.device("cuda", 0)
-VARIANTS = [0, 1, 2]
+VARIANTS = [0, 1]
 
 
 @pytest.fixture
@@ -80,7 +80,7 @@ def test_products_bitwise_every_variant(tuning, variant, light):
     assert torch.equal(out, out1)
 
 
-@pytest.mark.parametrize("variant,chain", [(0, 0), (0, 1), (1, 1), (1, 0), (2, 1)])
+@pytest.mark.parametrize("variant,chain", [(0, 0), (0, 1), (1, 1), (1, 0)])
 def test_fixed_step_trajectory_every_variant(tuning, variant, chain):
     tuning.set_tuning("sell_variant", variant)
     tuning.set_tuning("chain_products", chain)

@@ -33,7 +33,7 @@ def problem(seed=0, m=700, n=900):
 def main():
     p = problem(0, 700, 6000)
     lib = native.load()
-    for variant in (0, 1, 2):
+    for variant in (0, 1):
         lib.set_tuning("sell_variant", variant)
         for grid in ((1, 1), (2, 2)):
             r = solve(p, SolverConfig(tolerance=1e-6, max_iterations=192, seed=1, n_procs=grid[0] * grid[1],
