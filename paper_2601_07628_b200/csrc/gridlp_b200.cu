@@ -179,6 +179,11 @@ __device__ __forceinline__ double ld_gather(const double* p, uint64_t pol) {
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
+// (Gathers allocate in L1: with L1::no_allocate cfg3 ran 3144 vs 2174 us per
+// iteration and cfg4 4859 vs 4168 — the hot columns of power-law and MCF
+// matrices hit in L1; profiles/r2/ab_gather_l1_noalloc_cfg*.json. A minimum
+// shared-memory carveout (largest L1) gave cfg3 -0.9 %, cfg2 / cfg4 no
+// change: ab_l1_carveout_cfg*.json; not applied.)
 
 // coherent read-once load (the thread rewrites the element later), first to leave L2
 __device__ __forceinline__ double ld_once(const double* p, uint64_t pol) {
