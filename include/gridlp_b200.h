@@ -403,6 +403,49 @@ int gridlp_iterate_graph_create(const gridlp_src_t* primal_src, const gridlp_pri
                                 gridlp_step_t* d_step, int32_t n_iters, uint32_t flags, void** graph_exec);
 int gridlp_graph_launch(void* graph_exec, void* stream);
 int gridlp_graph_destroy(void* graph_exec);
+
+/* --- device-side main loop (iterate_epoch, pdhg_engine.py:364-476) ----------
+ * A CUDA graph with a WHILE conditional node whose body is one KKT interval
+ * — the chunk of iterations, the KKT / restart-probe pass and
+ * gridlp_loop_graph_decide's one-thread kernel — so consecutive intervals run
+ * back to back without a host round trip. The decide kernel evaluates the
+ * reference's per-pass logic on the pass's reduction slots exactly as the
+ * host does (solver_driver / pdhg_engine expressions, IEEE-rounded sqrt and
+ * divisions): relative KKT report, numerical failure, termination at the
+ * tolerance, the fixed-point error and restart_decision (pdhg_engine.py:
+ * 245-282), the iteration limit; the body repeats while none of them stops it
+ * and fewer than max_passes passes ran. Each pass's slot values go to a ring
+ * (GRIDLP_LOOP_REC doubles per pass) from which the host replays its
+ * bookkeeping (reports, log lines, ledger, restart handling) after the
+ * launch. Single-block grids only.
+ *
+ * Build: gridlp_loop_graph_begin starts capturing `stream` into the body;
+ * the caller then issues the interval's launches on `stream`;
+ * gridlp_loop_graph_decide appends the decide kernel; gridlp_loop_graph_end
+ * instantiates (launch with gridlp_graph_launch, free with
+ * gridlp_graph_destroy). gridlp_loop_graph_abort ends a failed capture. */
+#define GRIDLP_LOOP_REC 12   /* kkt_rows[4], kkt_cols[4], probe[2], fp, stop flag */
+typedef struct gridlp_loop {
+  /* host-written before each launch */
+  double eta, omega;                     /* constant between restarts */
+  double bnorm, cnorm, obj_const, tolerance;
+  double beta_sufficient, beta_necessary, beta_artificial;
+  double base_fp, prev_fp;               /* valid when has_base / has_prev */
+  int64_t total, inner_k;                /* iterations / Halpern counter before the launch */
+  int64_t max_iterations, kkt_interval;
+  int64_t max_passes;                    /* ring capacity: stop after this many passes */
+  int32_t has_base, has_prev;
+  int32_t restarts;                      /* EngineConfig.restarts */
+  int32_t slot_rows, slot_cols, slot_probe;   /* reduction slots (rows of GRIDLP_MAX_RED doubles) */
+  /* device-written */
+  int64_t passes;                        /* passes completed by the launch (host sets 0) */
+  int32_t stopped;
+  int32_t reserved;
+} gridlp_loop_t;
+int gridlp_loop_graph_begin(void* stream, void** ctx);
+int gridlp_loop_graph_decide(void* ctx, const double* slots, gridlp_loop_t* d_loop, double* d_ring);
+int gridlp_loop_graph_end(void* ctx, void** graph_exec);
+int gridlp_loop_graph_abort(void* ctx);
 size_t gridlp_persistent_scratch_bytes(void);
 /* n_iters fused iterations of a TINY single-block LP in ONE thread-block
  * cluster launch (8 CTAs x 512 threads): x_bar / y replicated in every CTA's shared

@@ -2171,6 +2171,167 @@ int gridlp_graph_destroy(void* graph_exec) {
   return GRIDLP_OK;
 }
 
+// ------------------------------------------------ device-side main loop
+}  // extern "C"
+
+namespace {
+
+struct LoopCtx {
+  cudaGraph_t parent = nullptr;
+  cudaGraph_t body = nullptr;
+  cudaGraphConditionalHandle handle = 0;
+  cudaStream_t stream = nullptr;
+  bool capturing = false;
+};
+
+// Python's max(a, b): a unless b > a (NaN a stays, NaN b never wins)
+__device__ __forceinline__ double py_max(double a, double b) { return b > a ? b : a; }
+
+// One thread: the host's per-pass logic of PdhgEngine.step / _kkt on the
+// pass's slots (single block: every axis sum is the single term), in the
+// same IEEE operations and order. Sets the WHILE condition.
+__global__ void loop_decide_kernel(const double* __restrict__ slots, gridlp_loop_t* L, double* __restrict__ ring,
+                                   cudaGraphConditionalHandle h) {
+  const int64_t p = L->passes;
+  const int64_t K = L->kkt_interval;
+  const int64_t total = L->total + K;
+  const int64_t inner_k = L->inner_k + K;
+  const double* kr = slots + (int64_t)L->slot_rows * GRIDLP_MAX_RED;
+  const double* kc = slots + (int64_t)L->slot_cols * GRIDLP_MAX_RED;
+  const double* pr = slots + (int64_t)L->slot_probe * GRIDLP_MAX_RED;
+  const bool restarts = L->restarts != 0;
+  double* rec = ring + p * GRIDLP_LOOP_REC;
+  for (int q = 0; q < 4; ++q) {
+    rec[q] = kr[q];
+    rec[4 + q] = kc[q];
+  }
+  rec[8] = restarts ? pr[0] : 0.0;
+  rec[9] = restarts ? pr[1] : 0.0;
+  rec[10] = 0.0;
+  // _kkt: report (pdhg_engine.py:192-216, solver_driver)
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const double pen = kr[3] > 0.0 ? inf : dsub(kr[1], kr[2]);
+  const double obj_p = kc[1];
+  const double obj_d = dadd(-pen, kc[2]);
+  const double r_p = ddiv(__dsqrt_rn(kr[0]), dadd(1.0, L->bnorm));
+  const double r_d = ddiv(__dsqrt_rn(kc[0]), dadd(1.0, L->cnorm));
+  double r_g;
+  if (!isfinite(obj_d) || !isfinite(obj_p))
+    r_g = inf;
+  else
+    r_g = ddiv(fabs(dsub(obj_p, obj_d)), dadd(1.0, py_max(fabs(obj_p), fabs(obj_d))));
+  bool stop = !isfinite(r_p) || !isfinite(r_d) || isnan(dadd(obj_p, L->obj_const));   // _broken
+  double overall = r_p;                                   // Report.overall = max(r_p, r_d, r_gap)
+  if (r_d > overall) overall = r_d;
+  if (r_g > overall) overall = r_g;
+  if (!stop && overall <= L->tolerance) stop = true;      // optimal
+  if (!stop && restarts) {
+    const double eta = L->eta, om = L->omega;
+    const double value = dadd(dadd(dmul(ddiv(om, eta), kc[3]), ddiv(pr[0], dmul(eta, om))), dmul(2.0, pr[1]));
+    const double fp = __dsqrt_rn(py_max(value, 0.0));
+    rec[10] = fp;
+    const double base = L->has_base ? L->base_fp : fp;
+    bool r = false;                                       // restart_decision (pdhg_engine.py:262-282)
+    if (fp <= dmul(L->beta_sufficient, base))
+      r = true;
+    else if (L->has_prev && fp <= dmul(L->beta_necessary, base) && fp > L->prev_fp)
+      r = true;
+    if (!r) r = (double)inner_k >= dmul(L->beta_artificial, (double)total);
+    if (r) {
+      stop = true;                                        // the host applies the restart
+    } else {
+      L->base_fp = base;
+      L->has_base = 1;
+      L->prev_fp = fp;
+      L->has_prev = 1;
+    }
+  }
+  if (!stop && total + K > L->max_iterations) stop = true;   // the next interval would pass the limit
+  if (!stop && p + 1 >= L->max_passes) stop = true;          // ring full
+  rec[11] = stop ? 1.0 : 0.0;
+  L->passes = p + 1;
+  L->stopped = stop ? 1 : 0;
+  if (!stop) {
+    L->total = total;
+    L->inner_k = inner_k;
+  }
+  cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gridlp_loop_graph_begin(void* stream, void** ctx) {
+  if (!ctx) return fail(GRIDLP_ERR_ARG, "loop_graph_begin: null ctx");
+  *ctx = nullptr;
+  auto* c = new LoopCtx;
+  c->stream = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaGraphCreate(&c->parent, 0);
+  if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&c->handle, c->parent, 1, cudaGraphCondAssignDefault);
+  cudaGraphNode_t node = nullptr;
+  if (e == cudaSuccess) {
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = c->handle;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    e = cudaGraphAddNode(&node, c->parent, nullptr, 0, &np);
+    if (e == cudaSuccess) c->body = np.conditional.phGraph_out[0];
+  }
+  if (e == cudaSuccess)
+    e = cudaStreamBeginCaptureToGraph(c->stream, c->body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    if (c->parent) cudaGraphDestroy(c->parent);
+    delete c;
+    return fail(GRIDLP_ERR_CUDA, std::string("loop_graph_begin: ") + cudaGetErrorString(e));
+  }
+  c->capturing = true;
+  *ctx = c;
+  return GRIDLP_OK;
+}
+
+int gridlp_loop_graph_decide(void* ctx, const double* slots, gridlp_loop_t* d_loop, double* d_ring) {
+  auto* c = static_cast<LoopCtx*>(ctx);
+  if (!c || !c->capturing || !slots || !d_loop || !d_ring) return fail(GRIDLP_ERR_ARG, "loop_graph_decide: bad argument");
+  loop_decide_kernel<<<1, 1, 0, c->stream>>>(slots, d_loop, d_ring, c->handle);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(GRIDLP_ERR_CUDA, std::string("loop_graph_decide: ") + cudaGetErrorString(e));
+  return GRIDLP_OK;
+}
+
+int gridlp_loop_graph_abort(void* ctx) {
+  auto* c = static_cast<LoopCtx*>(ctx);
+  if (!c) return GRIDLP_OK;
+  if (c->capturing) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c->stream, &g);
+    cudaGetLastError();
+  }
+  if (c->parent) cudaGraphDestroy(c->parent);
+  delete c;
+  return GRIDLP_OK;
+}
+
+int gridlp_loop_graph_end(void* ctx, void** graph_exec) {
+  auto* c = static_cast<LoopCtx*>(ctx);
+  if (!c || !graph_exec) return fail(GRIDLP_ERR_ARG, "loop_graph_end: bad argument");
+  *graph_exec = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+  c->capturing = false;
+  cudaGraphExec_t ge = nullptr;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, c->parent, 0);
+  cudaGraphDestroy(c->parent);
+  delete c;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GRIDLP_ERR_CUDA, std::string("loop_graph_end: ") + cudaGetErrorString(e));
+  }
+  *graph_exec = ge;
+  return GRIDLP_OK;
+}
+
 size_t gridlp_persistent_scratch_bytes(void) { return 64; }
 
 int gridlp_pdhg_iterate_persistent(const gridlp_src_t* primal_src, const gridlp_primal_t* pv,

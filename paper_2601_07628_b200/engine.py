@@ -22,6 +22,7 @@ pdhg_engine.py:405-462 does, with the same collective ledger.
 
 from __future__ import annotations
 
+import ctypes
 import dataclasses
 import logging
 import math
@@ -122,6 +123,15 @@ class EngineOptions:
     # two global-memory grid barriers per iteration cost more than the
     # kernel boundaries PDL already hides
     persistent_max_nnz: int = 0
+    # single-block solves: the main loop runs on the device — one CUDA graph
+    # with a WHILE node whose body is a KKT interval (iterations, pass, and a
+    # one-thread kernel evaluating the reference's termination / restart
+    # logic on the pass's slots), so intervals follow each other without a
+    # host round trip; the host replays each pass's bookkeeping afterwards
+    # and handles restarts (gridlp_loop_graph_*). Bit-identical iterates
+    # and decisions (checked pass by pass).
+    device_loop: bool = True
+    device_loop_passes: int = 1024
     # tiny single-block LPs (vectors + matrix within one 8-CTA cluster's
     # shared memory, e.g. BASELINE configs[0]) run each chunk of iterations
     # in one thread-block-cluster launch (gridlp_pdhg_iterate_cluster,
@@ -1217,6 +1227,12 @@ class PdhgEngine:
     def _kkt(self, tau: float, restarts: bool):
         """One evaluation pass (+ the speculative restart probe). Returns
         (report, pieces) with host scalars reduced in the reference order."""
+        self._kkt_launch(restarts)
+        return self._kkt_collect(self.ops.read_slots(self.nslots), restarts)
+
+    def _kkt_launch(self, restarts: bool):
+        """The pass's device work (products, fused KKT / probe terms, slot
+        reductions), no host read."""
         ops = self.ops
         self._sync_shards()
         fused_pass = self.__dict__.pop("_pass_in_launch", 0)
@@ -1251,7 +1267,9 @@ class PdhgEngine:
                         if blk is not None:
                             ops.halfdiff_dot(blk.bufs["pAx_A"], blk.bufs["pPr_A"], row.dy,
                                              self.slot[("cross", (i, j))])
-        vals = ops.read_slots(self.nslots)
+
+    def _kkt_collect(self, vals, restarts: bool):
+        """Report and per-block table of a pass from its reduction slots."""
         local = {}
         for (i, j) in self.comm.local:
             r = np.zeros(NFIELDS)
@@ -1323,14 +1341,18 @@ class PdhgEngine:
         self._started = time.monotonic()
         self._t_loop = time.perf_counter()
 
-    def step(self) -> bool:
+    def step(self, device_loop: bool = False) -> bool:
         """Iterations up to the next KKT pass, then the pass. True when the
-        loop terminated (status set)."""
+        loop terminated (status set). device_loop: run as many KKT intervals
+        as the device-side loop decides to (run() does; bench.py times single
+        intervals)."""
         o, ops, st = self.opts, self.ops, self._s
         K = o.kkt_interval
         if st["total"] >= o.max_iterations:
             st["status"] = ITERATION_LIMIT
             return True
+        if device_loop and st["total"] % K == 0 and st["total"] + K <= o.max_iterations and self._loop_ok():
+            return self._step_device_loop()
         eta, omega = st["eta"], st["omega"]
         tau, sigma = eta / omega, eta * omega
         total = st["total"]
@@ -1366,6 +1388,13 @@ class PdhgEngine:
             return False
         with nvtx_range("gridlp.kkt_pass"):
             report, tab = self._kkt(tau, o.restarts)
+        return self._post_pass(report, tab, total, eta, omega)
+
+    def _post_pass(self, report, tab, total: int, eta: float, omega: float) -> bool:
+        """The host logic after a KKT pass (pdhg_engine.py:402-476):
+        log, termination, restart decision and PID update. True when the
+        loop terminated."""
+        o, st = self.opts, self._s
         self.passes += 1
         st["report"], st["report_at"] = report, total
         if st["log_hook"] is not None:
@@ -1404,6 +1433,101 @@ class PdhgEngine:
                 return True
         return False
 
+    # ------------------------------------------------ device-side loop
+    def _loop_ok(self) -> bool:
+        o, st = self.opts, self._s
+        return (o.device_loop and not getattr(self, "_loop_off", False) and self.comm.kind == "virtual"
+                and self.R == 1 and self.C == 1 and not self._banded and o.use_graphs
+                and hasattr(self.ops, "loop_graph") and o.time_limit_seconds is None and st["trace"] is None
+                and self.iteration_events is None and not self._persistent() and self.device.type == "cuda")
+
+    def _loop_build(self):
+        o, ops = self.opts, self.ops
+        K = o.kkt_interval
+        cap = max(1, int(o.device_loop_passes))
+        self._loop_cap = cap
+        self._loop_dev = torch.zeros(ctypes.sizeof(native.Loop), dtype=torch.uint8, device=self.device)
+        self._ring_dev = torch.zeros((cap, native.LOOP_REC), dtype=torch.float64, device=self.device)
+        (i, _), = self.rows.items()
+        (j, _), = self.cols.items()
+        self._loop_slots = (self.slot[("kkt_rows", i)], self.slot[("kkt_cols", j)],
+                            self.slot[("probe", i)] if o.restarts else self.slot[("kkt_rows", i)])
+
+        def interval():
+            if self.opts.cluster_fused_pass and self._cluster():
+                self._fuse_pass_mode = 2 if o.restarts else 1
+            self._launch_iterations(K)
+            self._kkt_launch(o.restarts)
+
+        cur = torch.cuda.current_stream(self.device)
+        ts = torch.cuda.Stream(self.device)
+        ts.wait_stream(cur)
+        with torch.cuda.stream(ts):
+            self._loop_graph = ops.loop_graph(interval, self._loop_dev, self._ring_dev)
+        cur.wait_stream(ts)
+
+    def _step_device_loop(self) -> bool:
+        """KKT intervals on the device until a pass terminates, restarts or
+        reaches a limit (one graph launch), then the host replays every
+        pass's bookkeeping in order — the same code as step() — and checks
+        that its decisions are the device's."""
+        o, ops, st = self.opts, self.ops, self._s
+        K = o.kkt_interval
+        eta, omega = st["eta"], st["omega"]
+        tau, sigma = eta / omega, eta * omega
+        key = (tau, sigma, o.gamma, st["inner_k"])
+        if key != st.get("device_step"):
+            ops.set_step(tau, sigma, o.gamma, st["inner_k"])
+        if getattr(self, "_loop_graph", None) is None:
+            try:
+                self._loop_build()
+            except native.GridlpError as exc:
+                log.warning("device-side loop unavailable (%s); host-driven intervals", exc)
+                self._loop_off = True
+                return self.step()
+        L = native.Loop()
+        L.eta, L.omega, L.bnorm, L.cnorm = eta, omega, self.bnorm, self.cnorm
+        L.obj_const, L.tolerance = self.const, o.tolerance
+        L.beta_sufficient, L.beta_necessary, L.beta_artificial = o.beta_sufficient, o.beta_necessary, o.beta_artificial
+        L.has_base = int(st["base_fp"] is not None)
+        L.base_fp = st["base_fp"] if st["base_fp"] is not None else 0.0
+        L.has_prev = int(st["prev_fp"] is not None)
+        L.prev_fp = st["prev_fp"] if st["prev_fp"] is not None else 0.0
+        L.total, L.inner_k, L.max_iterations, L.kkt_interval = st["total"], st["inner_k"], o.max_iterations, K
+        L.max_passes, L.restarts = self._loop_cap, int(o.restarts)
+        L.slot_rows, L.slot_cols, L.slot_probe = self._loop_slots
+        L.passes, L.stopped = 0, 0
+        self._loop_dev.copy_(torch.frombuffer(bytearray(L), dtype=torch.uint8))
+        with nvtx_range("gridlp.device_loop"):
+            self._loop_graph.replay()
+            out = native.Loop.from_buffer_copy(self._loop_dev.cpu().numpy().tobytes())
+        n = int(out.passes)
+        ring = self._ring_dev[:n].cpu().numpy()
+        ops.launches += self._loop_graph.launches * (n - 1)
+        vals = np.zeros((self.nslots, native.MAX_RED))
+        sr, sc, sp = self._loop_slots
+        done = False
+        for p in range(n):
+            rec = ring[p]
+            self.count_iterations(K)
+            st["inner_k"] += K
+            st["total"] += K
+            st["device_step"] = (tau, sigma, o.gamma, st["inner_k"])
+            vals[sr, :4] = rec[0:4]
+            vals[sc, :4] = rec[4:8]
+            if o.restarts:
+                vals[sp, :2] = rec[8:10]
+            epoch = st["epoch"]
+            report, tab = self._kkt_collect(vals, o.restarts)
+            done = self._post_pass(report, tab, st["total"], eta, omega)
+            host_stop = done or st["epoch"] != epoch
+            dev_stop = rec[11] != 0.0
+            limit = st["total"] + K > o.max_iterations or p + 1 >= self._loop_cap
+            if (p < n - 1 and (host_stop or dev_stop)) or (p == n - 1 and (not dev_stop or (not host_stop and not limit))):
+                raise RuntimeError(f"device-side loop diverged from the host decision at pass {p} of {n} "
+                                   f"(iteration {st['total']})")
+        return done
+
     def finish(self):
         o, ops, st = self.opts, self.ops, self._s
         eta, omega = st["eta"], st["omega"]
@@ -1423,7 +1547,7 @@ class PdhgEngine:
     def run(self, eta: float, omega: float, trace=None, log_hook=None):
         """iterate_epoch (pdhg_engine.py:364-476). Returns a dict outcome."""
         self.start(eta, omega, trace, log_hook)
-        while not self.step():
+        while not self.step(device_loop=True):
             pass
         return self.finish()
 

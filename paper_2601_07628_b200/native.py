@@ -47,6 +47,20 @@ ABI_VERSION = 2
 VALS_F64, VALS_F32, VALS_UNIT = 0, 1, 2
 
 
+LOOP_REC = 12     # GRIDLP_LOOP_REC
+
+
+class Loop(ctypes.Structure):
+    """gridlp_loop_t: the device-side main loop's state (include/gridlp_b200.h)."""
+    _fields_ = [("eta", c_double), ("omega", c_double), ("bnorm", c_double), ("cnorm", c_double),
+                ("obj_const", c_double), ("tolerance", c_double), ("beta_sufficient", c_double),
+                ("beta_necessary", c_double), ("beta_artificial", c_double), ("base_fp", c_double),
+                ("prev_fp", c_double), ("total", c_int64), ("inner_k", c_int64), ("max_iterations", c_int64),
+                ("kkt_interval", c_int64), ("max_passes", c_int64), ("has_base", c_int32), ("has_prev", c_int32),
+                ("restarts", c_int32), ("slot_rows", c_int32), ("slot_cols", c_int32), ("slot_probe", c_int32),
+                ("passes", c_int64), ("stopped", c_int32), ("reserved", c_int32)]
+
+
 class Csr(ctypes.Structure):
     _fields_ = [("num_rows", c_int64), ("num_cols", c_int64), ("nnz", c_int64),
                 ("sell_vals", c_void_p), ("sell_cols", c_void_p), ("slice_off", c_void_p),
@@ -103,6 +117,10 @@ class Red(ctypes.Structure):
 _P = c_void_p
 SIGNATURES = {
     "gridlp_abi_version": ([], c_int),
+    "gridlp_loop_graph_begin": ([_P, _P], c_int),
+    "gridlp_loop_graph_decide": ([_P, _P, _P, _P], c_int),
+    "gridlp_loop_graph_end": ([_P, _P], c_int),
+    "gridlp_loop_graph_abort": ([_P], c_int),
     "gridlp_build_flags": ([], c_int),
     "gridlp_last_error": ([], ctypes.c_char_p),
     "gridlp_device_info": ([c_int, POINTER(c_int32), POINTER(c_int64)], c_int),

@@ -295,6 +295,29 @@ class CudaOps:
         launches = count * (2 + _heavy(psrc) + _heavy(dsrc)) + 1
         return _IterateGraph(self, h, launches)
 
+    def loop_graph(self, build, loop_dev: torch.Tensor, ring_dev: torch.Tensor):
+        """The device-side main loop (gridlp_loop_graph_*): build() issues one
+        KKT interval's launches on this ops' current stream while it is
+        captured into the body of a WHILE-conditional graph, followed by the
+        decide kernel over this ops' reduction slots. Returns a graph whose
+        `launches` counts one interval; the caller adds the passes run."""
+        ctx = ctypes.c_void_p()
+        before = self.launches
+        self.lib.call("gridlp_loop_graph_begin", self.stream(), ctypes.byref(ctx))
+        try:
+            build()
+            self.lib.call("gridlp_loop_graph_decide", ctx, self.slots.data_ptr(), loop_dev.data_ptr(),
+                          ring_dev.data_ptr())
+        except BaseException:
+            self.lib._lib.gridlp_loop_graph_abort(ctx)
+            self.launches = before
+            raise
+        h = ctypes.c_void_p()
+        per_interval = self.launches - before + 1
+        self.launches = before
+        self.lib.call("gridlp_loop_graph_end", ctx, ctypes.byref(h))
+        return _IterateGraph(self, h, per_interval)
+
     def cluster_plan(self, psrc, dsrc):
         """gridlp_cluster_plan for a matrix pair: the host plan array, or None
         when the LP does not fit one cluster (GRIDLP_ERR_UNSUPPORTED)."""
