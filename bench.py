@@ -629,7 +629,12 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    engine.iteration_events = []
+    # single-block grids: the timed steps run through the device-side loop
+    # (the solve's own main loop: KKT intervals chained on the device, exactly
+    # args.steps passes); the kernel-only time per iteration (roofline) is
+    # then taken from a few host-driven intervals right after
+    device_loop = engine._loop_ok() and not args.no_device_loop
+    engine.iteration_events = None if device_loop else []
     launches0 = engine.ops.launches
     it0 = engine._s["total"]
     start = torch.cuda.Event(enable_timing=True)
@@ -637,8 +642,15 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clocks:
         torch.cuda.synchronize()
         start.record()
-        for _ in range(args.steps):
-            engine.step()
+        if device_loop:
+            p0 = engine.passes
+            while engine.passes - p0 < args.steps:
+                engine.loop_budget = args.steps - (engine.passes - p0)
+                engine.step(device_loop=True)
+            engine.loop_budget = None
+        else:
+            for _ in range(args.steps):
+                engine.step()
         stop.record()
         torch.cuda.synchronize()
     if world > 1:
@@ -646,6 +658,11 @@ def run_ours(args, rank, world, local_rank):
     elapsed = start.elapsed_time(stop) * 1e-3
     iters = engine._s["total"] - it0
     launches = engine.ops.launches - launches0
+    if device_loop:
+        engine.iteration_events = []
+        for _ in range(3):
+            engine.step()
+        torch.cuda.synchronize()
     ev = engine.iteration_events
     engine.iteration_events = None
     loop_s = sum(a.elapsed_time(b) for a, b, _ in ev) * 1e-3
@@ -721,6 +738,9 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "inputs larger than L2 (A + A^T = "
                    f"{24 * nnz_total / 1e6:.0f} MB of 126 MB L2 per iteration, streamed evict-first)",
                    "restarts_in_timed_region": restarts, "layout_choices": choices,
+                   "main_loop": ("device (WHILE-graph of KKT intervals, gridlp_loop_graph_*; kernel time per "
+                                 "iteration from 3 host-driven intervals after the timed region)"
+                                 if device_loop else "host-driven KKT intervals"),
                    "kernel_tuning": kernel_tuning(),
                    "ranks_share_gpus": world > 1 and args.dist_backend == "gloo"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -796,6 +816,8 @@ def main():
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 latency / cfg3 extra keys")
     ap.add_argument("--light-row-max", type=int, default=None, help="EngineOptions.light_row_max override")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches (the NCCL executor's path)")
+    ap.add_argument("--no-device-loop", action="store_true",
+                    help="time host-driven KKT intervals instead of the device-side loop")
     ap.add_argument("--natural-order", action="store_true", help="EngineOptions.sorted_order=False (layout order)")
     ap.add_argument("--column-bands", type=int, default=None, help="EngineOptions.column_bands (1 = off)")
     ap.add_argument("--band-mb", type=int, default=None, help="EngineOptions.band_bytes in MiB")

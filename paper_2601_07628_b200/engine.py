@@ -129,8 +129,12 @@ class EngineOptions:
     # logic on the pass's slots), so intervals follow each other without a
     # host round trip; the host replays each pass's bookkeeping afterwards
     # and handles restarts (gridlp_loop_graph_*). Bit-identical iterates
-    # and decisions (checked pass by pass).
-    device_loop: bool = True
+    # and decisions (checked pass by pass). None = only for LPs on the
+    # cluster launch (cfg1: 0.091 vs 0.095 s to 1e-4, interleaved A/B): a
+    # conditional body loses the programmatic chaining of the kernel-per-
+    # product chunks (cfg2: 12.0 vs 11.2 ms per interval, e2e equal), so
+    # those keep the host-driven loop; True / False force it on / off.
+    device_loop: bool | None = None
     device_loop_passes: int = 1024
     # tiny single-block LPs (vectors + matrix within one 8-CTA cluster's
     # shared memory, e.g. BASELINE configs[0]) run each chunk of iterations
@@ -1436,7 +1440,8 @@ class PdhgEngine:
     # ------------------------------------------------ device-side loop
     def _loop_ok(self) -> bool:
         o, st = self.opts, self._s
-        return (o.device_loop and not getattr(self, "_loop_off", False) and self.comm.kind == "virtual"
+        want = self._cluster() if o.device_loop is None else o.device_loop
+        return (want and not getattr(self, "_loop_off", False) and self.comm.kind == "virtual"
                 and self.R == 1 and self.C == 1 and not self._banded and o.use_graphs
                 and hasattr(self.ops, "loop_graph") and o.time_limit_seconds is None and st["trace"] is None
                 and self.iteration_events is None and not self._persistent() and self.device.type == "cuda")
@@ -1494,7 +1499,9 @@ class PdhgEngine:
         L.has_prev = int(st["prev_fp"] is not None)
         L.prev_fp = st["prev_fp"] if st["prev_fp"] is not None else 0.0
         L.total, L.inner_k, L.max_iterations, L.kkt_interval = st["total"], st["inner_k"], o.max_iterations, K
-        L.max_passes, L.restarts = self._loop_cap, int(o.restarts)
+        budget = getattr(self, "loop_budget", None)      # bench.py: exactly its timed passes
+        cap = self._loop_cap if budget is None else max(1, min(self._loop_cap, int(budget)))
+        L.max_passes, L.restarts = cap, int(o.restarts)
         L.slot_rows, L.slot_cols, L.slot_probe = self._loop_slots
         L.passes, L.stopped = 0, 0
         self._loop_dev.copy_(torch.frombuffer(bytearray(L), dtype=torch.uint8))
@@ -1522,7 +1529,7 @@ class PdhgEngine:
             done = self._post_pass(report, tab, st["total"], eta, omega)
             host_stop = done or st["epoch"] != epoch
             dev_stop = rec[11] != 0.0
-            limit = st["total"] + K > o.max_iterations or p + 1 >= self._loop_cap
+            limit = st["total"] + K > o.max_iterations or p + 1 >= cap
             if (p < n - 1 and (host_stop or dev_stop)) or (p == n - 1 and (not dev_stop or (not host_stop and not limit))):
                 raise RuntimeError(f"device-side loop diverged from the host decision at pass {p} of {n} "
                                    f"(iteration {st['total']})")

@@ -83,8 +83,8 @@ CASES = {
                  dict(tolerance=1e-6, seed=2), {"cluster_small": False}),
     "heavy": (_heavy_lp, dict(tolerance=1e-6, seed=1, max_iterations=5000), {}),
     "no_restarts_limit": (_heavy_lp, dict(tolerance=1e-9, seed=1, restarts=False, max_iterations=1000), {}),
-    "small_ring": (lambda: generate(GeneratorSpec(kind="staircase", num_rows=400, num_cols=700, nnz_target=3000,
-                                                  inequality_fraction=0.3, seed=4)),
+    "small_ring": (lambda: generate(GeneratorSpec(kind="uniform_random", num_rows=400, num_cols=700,
+                                                  nnz_target=3000, inequality_fraction=0.3, seed=4)),
                    dict(tolerance=1e-6, seed=4), {"device_loop_passes": 3}),
 }
 
