@@ -617,6 +617,8 @@ def run_ours(args, rank, world, local_rank):
         over["graph_nccl"] = True
     if args.value_codec is not None:
         over["value_codec"] = args.value_codec
+    if args.device_loop:
+        over["device_loop"] = True
     engine, layout, eta, omega, tim = prepare(p, cfg, device=dev, engine_overrides=over)
     log(f"[bench] rank {rank}: setup {time.perf_counter() - t0:.1f}s {tim}")
     R, C = layout.topology.rows, layout.topology.cols
@@ -817,7 +819,9 @@ def main():
     ap.add_argument("--light-row-max", type=int, default=None, help="EngineOptions.light_row_max override")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches (the NCCL executor's path)")
     ap.add_argument("--no-device-loop", action="store_true",
-                    help="time host-driven KKT intervals instead of the device-side loop")
+                    help="time host-driven KKT intervals even where the device-side loop is on")
+    ap.add_argument("--device-loop", action="store_true",
+                    help="EngineOptions.device_loop=True (default: cluster-launched LPs only)")
     ap.add_argument("--natural-order", action="store_true", help="EngineOptions.sorted_order=False (layout order)")
     ap.add_argument("--column-bands", type=int, default=None, help="EngineOptions.column_bands (1 = off)")
     ap.add_argument("--band-mb", type=int, default=None, help="EngineOptions.band_bytes in MiB")
