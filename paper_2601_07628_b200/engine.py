@@ -129,12 +129,13 @@ class EngineOptions:
     # logic on the pass's slots), so intervals follow each other without a
     # host round trip; the host replays each pass's bookkeeping afterwards
     # and handles restarts (gridlp_loop_graph_*). Bit-identical iterates
-    # and decisions (checked pass by pass). None = only for LPs on the
-    # cluster launch (cfg1: 0.091 vs 0.095 s to 1e-4, interleaved A/B): a
-    # conditional body loses the programmatic chaining of the kernel-per-
-    # product chunks (cfg2: 12.0 vs 11.2 ms per interval, e2e equal), so
-    # those keep the host-driven loop; True / False force it on / off.
-    device_loop: bool | None = None
+    # and decisions (checked pass by pass). Opt-in: a conditional body
+    # loses the programmatic chaining of the kernel-per-product chunks
+    # (cfg2: 12.0 vs 11.2 ms per interval, e2e equal), and on the cluster
+    # launch (cfg1) it is faster on average but bimodal (0.087-0.098 s and
+    # 0.088-0.116 s vs a steady 0.095 s host-driven); None = cluster-launched
+    # LPs only, True = every single-block LP, False = never (default).
+    device_loop: bool | None = False
     device_loop_passes: int = 1024
     # tiny single-block LPs (vectors + matrix within one 8-CTA cluster's
     # shared memory, e.g. BASELINE configs[0]) run each chunk of iterations

@@ -50,6 +50,9 @@ def main():
                                inequality_fraction=0.3, seed=2))
     r = solve(q, SolverConfig(tolerance=1e-6, max_iterations=192, seed=2))   # all rows light: cluster launch
     print(f"cluster: {r.status} it={r.iterations} obj={r.objective:.10g}")
+    r = _solve(q, SolverConfig(tolerance=1e-6, max_iterations=192, seed=2),
+               engine_overrides={"device_loop": True})          # the device-side loop (WHILE graph)
+    print(f"device loop: {r.status} it={r.iterations} obj={r.objective:.10g}")
     print("SANITIZER_CASE_DONE")
 
 
