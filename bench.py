@@ -812,7 +812,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-runs", type=int, default=3, help="complete solves timed for e2e (median reported)")
+    ap.add_argument("--e2e-runs", type=int, default=5, help="complete solves timed for e2e (median reported)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spmv", action="store_true", help="skip the SpMV-only comparison with cuSPARSE")
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 latency / cfg3 extra keys")
