@@ -318,7 +318,7 @@ def kernel_tuning() -> dict:
     from paper_2601_07628_b200 import native
 
     lib = native.load()
-    return {k: lib.get_tuning(k) for k in ("sell_variant", "chain_products")}
+    return {k: lib.get_tuning(k) for k in ("sell_variant", "chain_products", "wide_ctas")}
 
 
 def workload_name(cfg: str) -> str:

@@ -138,8 +138,13 @@ typedef struct gridlp_csr {
    * the values themselves (lp_model.py:53-55 stores FP64 values; integer
    * and +-1 coefficients are exact in the narrower forms). */
   int32_t val_codec;
-  int32_t reserved_codec;
+  /* GRIDLP_CSR_* launch hints (never change a value): GRIDLP_CSR_WIDE_CTAS
+   * runs the main-loop products' SELL lanes in 4-warp CTAs instead of 2 —
+   * fewer CTA launches for blocks of very short rows (network / MCF columns:
+   * cfg4's A^T K1 2652 -> 2441 us). */
+  int32_t launch_flags;
 } gridlp_csr_t;
+#define GRIDLP_CSR_WIDE_CTAS 1
 
 /*
  * Peer-memory exchange of one grid axis group (G ranks: a grid row for the

@@ -25,6 +25,7 @@ from . import native
 DEFAULT_LIGHT_ROW_MAX = 128     # SELL-32 lanes (one lane per row); sweep in profiles/r1/row_classes.md
 LIGHT_ROW_CANDIDATES = (128, 256, 512, 1024, 2048)   # the engine's per-block choices (profiles/r1/layout_autotune.md)
 DEFAULT_EXACT_ROW_MAX = 4096    # one warp per row, still sequential sums; longer rows are chunked
+WIDE_CTA_MAX_MEAN_ROW = 6.0     # mean light-row length at or below which SELL lanes use 4-warp CTAs
 
 
 @dataclass
@@ -286,6 +287,14 @@ class DeviceCsr:
                                  ptr("chunk_first"), ptr("chunk_row"), self.num_chunks, ptr("chunk_sums"),
                                  ptr("chunk_done"), light_row_max, exact_row_max)
         self.struct.val_codec = self.val_codec
+        # launch hint: blocks of very short light rows (network / MCF columns)
+        # run the main-loop SELL lanes in 4-warp CTAs (fewer CTA launches;
+        # cfg4's A^T 2652 -> 2441 us, cfg2 / cfg3 rows of 10-20 stay at 2)
+        if self.nnz and self.num_rows and torch.device(device).type == "cuda":
+            hnnz = int(self.dev["long_ptr"][-1].item()) if self.long_rows else 0
+            light_rows = self.num_rows - self.long_rows
+            if light_rows > 0 and (self.nnz - hnnz) / light_rows <= WIDE_CTA_MAX_MEAN_ROW:
+                self.struct.launch_flags |= native.CSR_WIDE_CTAS
 
     def _apply_codec(self, want: str, real):
         """Re-store the values in codec `want` ("auto": the narrowest lossless

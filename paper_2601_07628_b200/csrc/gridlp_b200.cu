@@ -905,15 +905,16 @@ __global__ void __launch_bounds__(SELL_NT, SELL_MINB) sell32_kernel(gridlp_csr_t
 #define GRIDLP_PIPE_U SELL_U
 #endif
 constexpr int PIPE_MINB = GRIDLP_PIPE_MINB;
-template <class Op, int VC>
-__global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
+// WPB warps (slices) per CTA: SELL_WPB, or 4 for GRIDLP_CSR_WIDE_CTAS blocks
+template <class Op, int VC, int WPB = SELL_WPB>
+__global__ void __launch_bounds__(WPB * 32, 40 / WPB) sell32_pipe_kernel(gridlp_csr_t A, const double* __restrict__ g,
                                                                         Op op, double* __restrict__ partials,
                                                                         double* __restrict__ terms, int cross_wait) {
   constexpr int U = GRIDLP_PIPE_U;
   constexpr int NR = Op::NRED > 0 ? Op::NRED : 1;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int64_t slice = (int64_t)blockIdx.x * SELL_WPB + warp;
+  const int64_t slice = (int64_t)blockIdx.x * WPB + warp;
   using V = Vals<VC>;
   const uint64_t pf = policy_evict_first();
   int info = -1, len = 0;
@@ -978,7 +979,7 @@ __global__ void __launch_bounds__(SELL_NT, PIPE_MINB) sell32_pipe_kernel(gridlp_
     const typename Op::Data d = op.load(r);
     emit_row(op, r, s, d, acc, terms, A.num_rows);
   }
-  cta_partials<Op>(acc, partials);
+  cta_partials_n<Op, WPB>(acc, partials);
   product_cta_done(op);
   pdl_wait();
 }
@@ -1603,6 +1604,7 @@ int64_t long_blocks(const gridlp_csr_t* A) { return (A->num_exact_long + SELL_WP
 // cfg2 / cfg3 and removed: profiles/r2/ncu_cfg2_tma_8x2_dual_rejected.md.)
 int g_sell_variant = 1;
 int g_chain_products = 1;           // pdhg_iterate: programmatic launch between products
+int g_wide_ctas = 1;                // honour GRIDLP_CSR_WIDE_CTAS (0: always SELL_WPB-warp CTAs)
 
 int64_t light_blocks(const gridlp_csr_t* A) {
   return A->num_slices > 0 ? (A->num_slices + SELL_WPB - 1) / SELL_WPB : 0;
@@ -1642,6 +1644,12 @@ cudaError_t launch_part(K kern, int64_t blocks, int threads, int smem, bool prog
 template <class Op, int VC>
 cudaError_t launch_light(int64_t blocks, bool programmatic, int cross_wait, cudaStream_t s, const gridlp_csr_t& M,
                          const double* gather, Op op, double* partials, double* terms) {
+  if constexpr (Op::NRED == 0) {
+    // main-loop products over blocks of very short rows: 4-warp CTAs
+    if (g_sell_variant == 1 && g_wide_ctas && (M.launch_flags & GRIDLP_CSR_WIDE_CTAS) && SELL_WPB < 4)
+      return launch_part(&sell32_pipe_kernel<Op, VC, 4>, (M.num_slices + 3) / 4, 128, 0, programmatic, cross_wait,
+                         s, M, gather, op, partials, terms);
+  }
   if (g_sell_variant == 1)
     return launch_part(&sell32_pipe_kernel<Op, VC>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
                        partials, terms);
@@ -1824,6 +1832,8 @@ int gridlp_set_tuning(const char* key, int64_t value) {
     g_sell_variant = (int)value;
   } else if (k == "chain_products") {
     g_chain_products = value != 0;
+  } else if (k == "wide_ctas") {
+    g_wide_ctas = value != 0;
   } else {
     return fail(GRIDLP_ERR_ARG, "set_tuning: unknown key " + k);
   }
@@ -1835,6 +1845,7 @@ int64_t gridlp_get_tuning(const char* key) {
   const std::string k(key);
   if (k == "sell_variant") return g_sell_variant;
   if (k == "chain_products") return g_chain_products;
+  if (k == "wide_ctas") return g_wide_ctas;
   return -1;
 }
 

@@ -45,6 +45,7 @@ NVCC_FLAGS = [
 ABI_VERSION = 2
 # gridlp_csr_t.val_codec (include/gridlp_b200.h GRIDLP_VALS_*)
 VALS_F64, VALS_F32, VALS_UNIT = 0, 1, 2
+CSR_WIDE_CTAS = 1   # gridlp_csr_t.launch_flags
 
 
 LOOP_REC = 12     # GRIDLP_LOOP_REC
@@ -71,7 +72,7 @@ class Csr(ctypes.Structure):
                 ("chunk_first", c_void_p), ("chunk_row", c_void_p), ("num_chunks", c_int64),
                 ("chunk_sums", c_void_p), ("chunk_done", c_void_p),
                 ("light_row_max", c_int32), ("exact_row_max", c_int32), ("carry", c_void_p),
-                ("hot_cols", c_int64), ("val_codec", c_int32), ("reserved_codec", c_int32)]
+                ("hot_cols", c_int64), ("val_codec", c_int32), ("launch_flags", c_int32)]
 
 
 class Peer(ctypes.Structure):

@@ -40,5 +40,5 @@ def test_chunked_scan_matches_one_pass(monkeypatch):
 
 def test_struct_carries_codec_field():
     fields = [f for f, _ in native.Csr._fields_]
-    assert fields[-2:] == ["val_codec", "reserved_codec"]
+    assert fields[-2:] == ["val_codec", "launch_flags"]
     assert native.ABI_VERSION == 2

@@ -27,7 +27,7 @@ VARIANTS = [0, 1]
 @pytest.fixture
 def tuning():
     lib = native.load()
-    keys = ("sell_variant", "chain_products")
+    keys = ("sell_variant", "chain_products", "wide_ctas")
     saved = {k: lib.get_tuning(k) for k in keys}
     yield lib
     for k, v in saved.items():
@@ -150,3 +150,36 @@ def test_cluster_launch_equals_graph_path(seed):
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
     assert a.report == b.report
+
+
+@pytest.mark.parametrize("light", [128, 1024])
+def test_wide_cta_launch_hint_bitwise(tuning, light):
+    """GRIDLP_CSR_WIDE_CTAS (4-warp CTAs for the SELL lanes of main-loop /
+    store products) computes the same rows bit for bit, including a slice
+    count that is not a multiple of 4; the engine sets it for blocks of very
+    short rows only (blocks.WIDE_CTA_MAX_MEAN_ROW)."""
+    from paper_2601_07628_b200.blocks import WIDE_CTA_MAX_MEAN_ROW
+
+    h, lens = _matrix(11 + light)
+    x = torch.as_tensor(np.random.default_rng(3).standard_normal(h.num_cols), device=DEV)
+    A = DeviceCsr(h, DEV, light_row_max=light)
+    assert (A.struct.launch_flags & native.CSR_WIDE_CTAS) == 0       # mean row length > 6
+    ops = CudaOps(DEV, A.slots() + 8, 4)
+    want = torch.empty(h.num_rows, dtype=torch.float64, device=DEV)
+    ops.store(Fused(A, x), want)
+    A.struct.launch_flags |= native.CSR_WIDE_CTAS
+    got = torch.full_like(want, np.nan)
+    ops.store(Fused(A, x), got)
+    assert torch.equal(got, want)
+    tuning.set_tuning("wide_ctas", 0)
+    off = torch.full_like(want, np.nan)
+    ops.store(Fused(A, x), off)
+    assert torch.equal(off, want)
+    tuning.set_tuning("wide_ctas", 1)
+    # a block of 3-entry rows (an MCF column's shape) gets the hint
+    m, n = 1000, 700
+    ptr = np.arange(0, 3 * m + 1, 3)
+    col = np.sort(np.random.default_rng(5).integers(0, n, (m, 3)), axis=1).ravel()
+    col[1::3] = np.minimum(col[1::3] + 1, n - 1)
+    short = DeviceCsr(HostCsr(m, n, ptr, col.astype(np.int64), np.ones(3 * m)), DEV)
+    assert 3.0 <= WIDE_CTA_MAX_MEAN_ROW and short.struct.launch_flags & native.CSR_WIDE_CTAS
