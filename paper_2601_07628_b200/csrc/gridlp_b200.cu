@@ -1644,11 +1644,13 @@ cudaError_t launch_part(K kern, int64_t blocks, int threads, int smem, bool prog
 template <class Op, int VC>
 cudaError_t launch_light(int64_t blocks, bool programmatic, int cross_wait, cudaStream_t s, const gridlp_csr_t& M,
                          const double* gather, Op op, double* partials, double* terms) {
-  if constexpr (Op::NRED == 0) {
-    // main-loop products over blocks of very short rows: 4-warp CTAs
-    if (g_sell_variant == 1 && g_wide_ctas && (M.launch_flags & GRIDLP_CSR_WIDE_CTAS) && SELL_WPB < 4)
+  if constexpr (Op::NRED == 0 && !HasCtaDone<Op>::value) {
+    // main-loop products over blocks of very short rows: 4-warp CTAs (not for
+    // ops that count their CTAs, e.g. the peer store's arrival protocol)
+    if (g_sell_variant == 1 && g_wide_ctas && (M.launch_flags & GRIDLP_CSR_WIDE_CTAS) && SELL_WPB < 4) {
       return launch_part(&sell32_pipe_kernel<Op, VC, 4>, (M.num_slices + 3) / 4, 128, 0, programmatic, cross_wait,
                          s, M, gather, op, partials, terms);
+    }
   }
   if (g_sell_variant == 1)
     return launch_part(&sell32_pipe_kernel<Op, VC>, blocks, SELL_NT, 0, programmatic, cross_wait, s, M, gather, op,
