@@ -70,7 +70,8 @@ enum gridlp_status {
  * a compact CSR of its long rows. Replaces SparseMatrix
  * (lp_model.py:40-150) for a LocalBlock matrix / matrix_transpose
  * (partition.py:93-122): int32 column indices, FP64 values — 12 B/nnz
- * instead of the reference's 16. Every row is summed in one of three ways:
+ * instead of the reference's 16 (8 or 4 B/nnz with the lossless value codecs,
+ * val_codec below). Every row is summed in one of three ways:
  *
  * light (length <= light_row_max): SELL-32. Rows are cut into slices of 32
  *   consecutive rows; inside a slice the lanes are ordered by row length
